@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the Walsh->wavelet change-of-basis hot path (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+metric : forward+adjoint matvecs/s (a matvec = one U W^-1 or one W U* application
+         to one vector/image) and the achieved fraction of the HBM roofline.
+step   : config 1-4: one forward of the whole batch + one adjoint of the whole
+         batch (2*batch matvecs); config 5: 50 iterations of the normal operator
+         U*U on the image (100 matvecs).  Default config: 2 (BASELINE configs[1]).
+value  : whole-job throughput, inputs resident in HBM, device-timed with CUDA
+         events per step, L2 flushed (256 MiB write) between steps, max over ranks.
+e2e    : the same metric through the public API with the step's inputs copied
+         from pinned host memory and the results copied back, inside the timed
+         region.
+roofline: dominant kernel (largest device time), algorithmic bytes
+          / its CUDA-event time, vs MEASURED_PEAKS.json.
+cpu_baseline: the reference library itself (oracle/_ref, built from
+         /root/reference) on the host cores, rank 0 at N = 1, bounded sample.
+Multi-GPU: one process per GPU (torchrun); independent batches per rank,
+         no data-path collective ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+# (family, nu, boundary, j, q, dim, r0, batch, input kind, density, workload name)
+CONFIGS = {
+    1: (0, 1, 0, 10, 1, 1, 1, 1, 0, 1.0, "cfg1: 1D Haar r0=1 M=2^10 q=1, single vector"),
+    2: (0, 4, 1, 16, 2, 1, 4, 64, 1, 1.0, "cfg2: 1D db4 boundary-VMP r0=4 M=2^16 q=2 (N=2^18), batch 64, level-decaying coeffs"),
+    3: (0, 3, 1, 21, 2, 1, 4, 32, 0, 0.1, "cfg3: 1D db3 boundary-VMP r0=4 M=2^21 q=2 (N=2^23), batch 32, 10% nonzeros"),
+    4: (0, 4, 1, 10, 1, 2, 4, 16, 1, 0.05, "cfg4: 2D db4 boundary-VMP r0=4 M=1024^2 q=1 (N=2048^2), batch 16, 5% nonzeros"),
+    5: (0, 2, 1, 12, 1, 2, 3, 1, 0, 0.02, "cfg5: 2D db2 boundary-VMP r0=3 M=4096^2 q=1 (N=8192^2), 50 U*U iterations, 2% nonzeros"),
+}
+CFG5_ITERS = 50
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(cfg, kernel: str, batch: int) -> float:
+    """Minimal DRAM bytes of one step's launches of `kernel`."""
+    fam, nu, bnd, j, q, dim, r0 = cfg[:7]
+    M, N = 1 << j, 1 << (j + q)
+    if dim == 2:
+        mats = CFG5_ITERS if cfg is CONFIGS[5] else 1
+        # small_fwd: row pass (M^2 -> MN) + column pass (MN -> N^2); small_adj mirrored
+        return 8.0 * batch * mats * (M * M + 2 * M * N + N * N)
+    CW = 32 + 2 * (nu - 1)
+    A = M // 32
+    lc = min(j - 1, 13)
+    per = {
+        "small_fwd": M + N, "small_adj": M + N,
+        "large_fwd1": M + A * CW, "large_fwd2": A * CW + N,
+        "large_adj2": N + A * CW, "large_adj1": A * CW + M,
+        "idwt_level": sum(2 * (1 << lev) for lev in range(lc + 1, j + 1)),
+        "dwt_level": sum(2 * (1 << lev) for lev in range(lc + 1, j + 1)),
+        "wav_coarse": 2 * 2 * (1 << lc),
+    }
+    return 8.0 * batch * per.get(kernel, 0)
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference's own CPU implementation, all host threads."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import numpy as np
+    fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = cfg
+    threads = os.cpu_count() or 1
+    kind_s = "reference"
+    try:
+        from oracle_py import Reference
+        R = Reference()
+        op = R.op(fam, nu, bnd, j, q, dim, r0)
+    except Exception as e:  # noqa: BLE001 -- reference not built: the C restatement
+        from oracle_py import Oracle
+        kind_s = "port"
+        op = None
+        err = str(e)
+    # bounded sample per step: config 1-4 up to `threads` vectors/images, config 5: 1 iteration
+    if cfg is CONFIGS[5]:
+        sample, iters, matv = 1, 1, 2
+    else:
+        sample = min(batch, max(1, threads)) if dim == 1 else 1
+        iters, matv = 1, 2 * sample
+    from paper_2106_00554_b200 import synth  # input generator only (host, no GPU)
+    M, N = 1 << j, 1 << (j + q)
+    nin, nout = (M, N) if dim == 1 else (M * M, N * N)
+    xs = np.stack([synth(kind, 1000 * args.config + b, j, r0, dens, dim) for b in range(sample)])
+    rng = np.random.default_rng(args.config)
+    ys = rng.standard_normal((sample, nout))
+    outf = np.empty((sample, nout))
+    outa = np.empty((sample, nin))
+
+    def one_step():
+        if op is None:
+            raise RuntimeError("reference library unavailable: " + err)
+        if cfg is CONFIGS[5]:
+            t = op.bench(2, xs, outa, 1, threads, iters)
+        else:
+            t = op.bench(0, xs, outf, sample, threads)
+            t += op.bench(1, ys, outa, sample, threads)
+        return t
+
+    for _ in range(args.warmup):
+        one_step()
+    ts = [one_step() for _ in range(args.steps)]
+    total = sum(ts)
+    value = matv * args.steps / total
+    line = {
+        "impl": "reference", "metric": "forward+adjoint matvecs/s", "value": value, "unit": "matvec/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded test_rng inputs, SURVEY.md 8d)",
+        "config": {"workload": name, "batch": batch, "sample_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": threads, "kind": kind_s,
+                         "sample": f"{sample} vector(s) forward + adjoint per step" if cfg is not CONFIGS[5]
+                         else "1 U*U iteration per step (of the 50-iteration config)"},
+        "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline(cfg, config_id):
+    """Reference CPU path on a bounded sample (rank 0, N = 1)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import numpy as np
+    fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = cfg
+    threads = os.cpu_count() or 1
+    try:
+        from oracle_py import Reference
+        op = Reference().op(fam, nu, bnd, j, q, dim, r0)
+        kind_s = "reference"
+    except Exception:  # noqa: BLE001
+        from oracle_py import Oracle
+        op = None
+        kind_s = "port"
+    from paper_2106_00554_b200 import synth
+    M, N = 1 << j, 1 << (j + q)
+    nin, nout = (M, N) if dim == 1 else (M * M, N * N)
+    if cfg is CONFIGS[5]:
+        sample = 1
+    else:
+        sample = min(batch, threads) if dim == 1 else 1
+    xs = np.stack([synth(kind, 1000 * config_id + b, j, r0, dens, dim) for b in range(sample)])
+    ys = np.random.default_rng(0).standard_normal((sample, nout))
+    outf, outa = np.empty((sample, nout)), np.empty((sample, nin))
+    if op is None:
+        from oracle_py import Oracle
+        o = Oracle().op(fam, nu, bnd, j, q, dim, r0)
+        t0 = time.perf_counter()
+        for b in range(sample):
+            o.forward(xs[b])
+            o.adjoint(ys[b])
+        t = time.perf_counter() - t0
+        return {"value": 2 * sample / t, "unit": "matvec/s", "cores": 1, "kind": "port",
+                "sample": f"{sample} vector(s) forward + adjoint"}
+    total, mv, reps = 0.0, 0, 0
+    while total < 8.0 and reps < 50:
+        if cfg is CONFIGS[5]:
+            total += op.bench(2, xs, outa, 1, threads, 1)
+            mv += 2
+        else:
+            total += op.bench(0, xs, outf, sample, threads) + op.bench(1, ys, outa, sample, threads)
+            mv += 2 * sample
+        reps += 1
+    return {"value": mv / total, "unit": "matvec/s", "cores": threads, "kind": kind_s,
+            "sample": (f"{reps} x ({sample} vector(s) forward + adjoint), one std::thread per vector"
+                       if cfg is not CONFIGS[5] else f"{reps} U*U iteration(s), FastOp::set_threads({threads})"),
+            "seconds": total}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = cfg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2106_00554_b200 as cw
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    spec = cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd))
+    if nu == 1:
+        op = cw.HaarFullRankOp(j, q, r0)
+    else:
+        op = cw.ComposedOp(cw.FastOp(spec, j, q, dim), None, True, r0)
+    nin, nout = op.cols(), op.rows()
+    # per-rank inputs (weak scaling: each rank owns a full batch)
+    xs = np.stack([cw.synth(kind, 1000 * args.config + rank * batch + b, j, r0, dens, dim)
+                   for b in range(batch)])
+    g = torch.Generator(device="cpu").manual_seed(1000 * args.config + 500 + rank)
+    ys = torch.randn((batch, nout), generator=g, dtype=torch.float64)
+    x_pin = torch.from_numpy(xs).pin_memory()
+    y_pin = ys.pin_memory()
+    x_dev, y_dev = x_pin.to(dev), y_pin.to(dev)
+    fo_dev = torch.empty((batch, nout), dtype=torch.float64, device=dev)
+    ao_dev = torch.empty((batch, nin), dtype=torch.float64, device=dev)
+    fo_pin = torch.empty((batch, nout), dtype=torch.float64).pin_memory()
+    ao_pin = torch.empty((batch, nin), dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 << 20 >> 3, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    is5 = args.config == 5
+    mv_per_step = 2 * CFG5_ITERS if is5 else 2 * batch
+
+    def step_device():
+        if is5:
+            ao_dev.copy_(x_dev)
+            op.normal(ao_dev, iters=CFG5_ITERS, work=fo_dev)
+        else:
+            op.forward(x_dev, fo_dev)
+            op.adjoint(y_dev, ao_dev)
+
+    def step_e2e():
+        x_dev.copy_(x_pin, non_blocking=True)
+        if is5:
+            ao_dev.copy_(x_dev)
+            op.normal(ao_dev, iters=CFG5_ITERS, work=fo_dev)
+            ao_pin.copy_(ao_dev, non_blocking=True)
+        else:
+            y_dev.copy_(y_pin, non_blocking=True)
+            op.forward(x_dev, fo_dev)
+            op.adjoint(y_dev, ao_dev)
+            fo_pin.copy_(fo_dev, non_blocking=True)
+            ao_pin.copy_(ao_dev, non_blocking=True)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def timed(fn, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        barrier()
+        torch.cuda.synchronize(dev)
+        for a, b in evs:
+            flush.zero_()  # evict L2 between steps (outside the event pair)
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize(dev)
+
+    l0 = cw.kernel_launches()
+    cw.profile_enable(True)
+    cw.profile_dump()
+    with Clocks(local) as clk:
+        ms = timed(step_device, args.steps)
+    cw.profile_enable(False)
+    launches = cw.kernel_launches() - l0
+    prof = cw.profile_dump()
+
+    for _ in range(2):
+        step_e2e()
+    ms_e2e = timed(step_e2e, args.steps)
+
+    total_mv = mv_per_step * args.steps * world
+    value = total_mv / (ms / 1e3)
+    e2e = total_mv / (ms_e2e / 1e3)
+    h2d = x_pin.numel() * 8 + (0 if is5 else y_pin.numel() * 8)
+    d2h = ao_pin.numel() * 8 + (0 if is5 else fo_pin.numel() * 8)
+
+    # roofline of the dominant kernel
+    peak, peak_kind = peaks()
+    roof = None
+    if prof:
+        kname = max(prof, key=lambda k: prof[k][0])
+        kms, kn = prof[kname]
+        steps_bytes = algorithmic_bytes(cfg, kname, batch) * args.steps
+        achieved = steps_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "kernel_ms_per_launch": kms / kn, "launches": kn,
+                "kernel_share_of_step": round(kms / ms, 4)}
+    M, N = 1 << j, 1 << (j + q)
+    per_mv = 8 * ((M + N) if dim == 1 else (M * M + N * N))
+    path_gbs = per_mv * total_mv / world / (ms / 1e3) / 1e9
+
+    line = {
+        "metric": "forward+adjoint matvecs/s", "value": round(value, 3), "unit": "matvec/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded test_rng inputs, SURVEY.md 8d)",
+        "config": {"workload": name, "batch_per_gpu": batch,
+                   "step": (f"{CFG5_ITERS} x U*U on the image" if is5 else "forward + adjoint of the batch"),
+                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (independent batches)"},
+        "path_gbs_per_gpu": round(path_gbs, 1), "path_frac": round(path_gbs / peak, 4),
+        "roofline": roof,
+        "kernels": {k: [round(v[0] / args.steps, 4), v[1] // args.steps] for k, v in prof.items()},
+        "gpu_launches": launches,
+        "e2e": {"value": round(e2e, 3), "unit": "matvec/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 4)},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg, args.config)
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+// Dispatch over the wavelet order and the non-templated utility kernels
+// (standalone FWHT, sequency permutation table, Walsh sign rows).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cww_device.cuh"
+#include "cww_launch.h"
+
+namespace cww {
+
+#define DECL(N)                                                                     \
+    cudaError_t launch_small_nu##N(const SmallArgs&, bool, cudaStream_t);           \
+    long long small_smem_nu##N(int, int, int, bool, bool);                                \
+    cudaError_t launch_large_nu##N(int, const LargeArgs&, cudaStream_t);            \
+    cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);
+DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6)
+#undef DECL
+
+#define SWITCH_NU(nu, call)                  \
+    switch (nu) {                            \
+        case 1: return call(1);              \
+        case 2: return call(2);              \
+        case 3: return call(3);              \
+        case 4: return call(4);              \
+        case 5: return call(5);              \
+        case 6: return call(6);              \
+    }
+
+cudaError_t launch_small(int nu, const SmallArgs& a, bool adj, cudaStream_t st) {
+#define C(N) launch_small_nu##N(a, adj, st)
+    SWITCH_NU(nu, C)
+#undef C
+    return cudaErrorInvalidValue;
+}
+
+long long small_smem_query(int nu, int V, int j, int q, bool adj, bool vf) {
+#define C(N) small_smem_nu##N(V, j, q, adj, vf)
+    SWITCH_NU(nu, C)
+#undef C
+    return -1;
+}
+
+cudaError_t launch_large(int nu, int which, const LargeArgs& a, cudaStream_t st) {
+#define C(N) launch_large_nu##N(which, a, st)
+    SWITCH_NU(nu, C)
+#undef C
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st) {
+#define C(N) launch_wav_nu##N(w, st)
+    SWITCH_NU(nu, C)
+#undef C
+    return cudaErrorInvalidValue;
+}
+
+long long large_nslot(int q, int j, int kl, int ng) {
+    (void)q;
+    const int nt = 256;
+    const int kh = (j - kLogB) - kl, R1 = 1 << kl, R2 = 1 << kh;
+    int items = ng * R2;
+    int iters = (items + nt - 1) / nt;
+    return (long long)(R1 / ng) * (nt / 32) * iters;
+}
+
+
+// In-place natural / sequency FWHT of vectors of length 2^bits <= 2^13 (one
+// CTA per vector, shared memory).
+__global__ void k_fwht_small(double* v, int bits, int sequency) {
+    extern __shared__ double sm[];
+    const int n = 1 << bits, tid = threadIdx.x, nt = blockDim.x;
+    double* x = v + (long long)blockIdx.x * n;
+    for (int i = tid; i < n; i += nt) sm[i] = x[i];
+    __syncthreads();
+    for (int hb = 0; hb < bits; ++hb) {
+        int h = 1 << hb;
+        for (int i = tid; i < n / 2; i += nt) {
+            int lo = ((i >> hb) << (hb + 1)) | (i & (h - 1));
+            double a = sm[lo], b = sm[lo + h];
+            sm[lo] = a + b;
+            sm[lo + h] = a - b;
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < n; i += nt) {
+        unsigned src = sequency ? brev_bits((unsigned)(i ^ (i >> 1)), bits) : (unsigned)i;
+        x[i] = sm[src];
+    }
+}
+
+// One radix-2 stage h of a large FWHT in global memory.
+__global__ void k_fwht_stage(double* v, int bits, int hb, long long nvec) {
+    const long long n = 1ll << bits, h = 1ll << hb;
+    const long long tot = nvec * (n >> 1);
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
+         f += (long long)gridDim.x * blockDim.x) {
+        long long vv = f / (n >> 1), i = f % (n >> 1);
+        long long lo = ((i >> hb) << (hb + 1)) | (i & (h - 1));
+        double* x = v + vv * n;
+        double a = x[lo], b = x[lo + h];
+        x[lo] = a + b;
+        x[lo + h] = a - b;
+    }
+}
+
+__global__ void k_permute_seq(const double* src, double* dst, int bits, long long nvec) {
+    const long long n = 1ll << bits, tot = nvec * n;
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
+         f += (long long)gridDim.x * blockDim.x) {
+        long long vv = f / n, i = f % n;
+        unsigned g = (unsigned)(i ^ (i >> 1));
+        dst[f] = src[vv * n + brev_bits(g, bits)];
+    }
+}
+
+__global__ void k_seq_perm(uint32_t* perm, int bits) {
+    const long long n = 1ll << bits;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        unsigned g = (unsigned)(i ^ (i >> 1));
+        perm[i] = brev_bits(g, bits);
+    }
+}
+
+__global__ void k_sign_rows(const uint64_t* pos, long long npos, int jb, double* out) {
+    const long long n = 1ll << jb, tot = npos * n;
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
+         f += (long long)gridDim.x * blockDim.x) {
+        long long ip = f / n, r = f % n;
+        unsigned long long vv = jb ? (__brevll(pos[ip]) >> (64 - jb)) : 0ull;
+        unsigned long long mask = vv ^ (vv << 1);
+        out[f] = (__popcll((unsigned long long)r & mask) & 1) ? -1.0 : 1.0;
+    }
+}
+
+
+cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, double* scratch,
+                        cudaStream_t st) {
+    if (bits <= 13) {
+        long long smem = (1ll << bits) * 8;
+        cudaFuncSetAttribute(k_fwht_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_fwht_small<<<(unsigned)batch, 256, smem, st>>>(v, bits, sequency);
+        return cudaGetLastError();
+    }
+    for (int hb = 0; hb < bits; ++hb) k_fwht_stage<<<148 * 8, 256, 0, st>>>(v, bits, hb, batch);
+    if (sequency) {
+        k_permute_seq<<<148 * 8, 256, 0, st>>>(v, scratch, bits, batch);
+        cudaMemcpyAsync(v, scratch, (size_t)(batch << bits) * 8, cudaMemcpyDeviceToDevice, st);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seq_perm(uint32_t* perm, int bits, cudaStream_t st) {
+    k_seq_perm<<<148 * 4, 256, 0, st>>>(perm, bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sign_rows(const uint64_t* pos, long long npos, int j, double* out,
+                             cudaStream_t st) {
+    k_sign_rows<<<148 * 4, 256, 0, st>>>(pos, npos, j, out);
+    return cudaGetLastError();
+}
+
+}  // namespace cww

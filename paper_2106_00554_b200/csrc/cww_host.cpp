@@ -1,0 +1,1131 @@
+// Host side of the B200 operator: spec validation, CWWF filter loading, the
+// Walsh-coefficient (kernel) table, edge-term tables, the per-op device table
+// block, call orchestration and the extern "C" ABI declared in
+// include/cww_b200.h.
+//
+// Reference correspondence (paths under /root/reference/proj):
+//   WaveletSpec::min_level / validate        src/wavelet.cpp:16-39
+//   load_filters (CWWF + CRC32)              src/wavelet.cpp:123-186, include/cww/crc32.hpp
+//   cascade / refine / left-edge cascade     src/wavelet.cpp:192-311
+//   cell_masses / compute_kernel_table       src/kernel.cpp:14-77
+//   FastOp ctor checks, build_edge_terms     src/fastop.cpp:27-98
+//   FastOp / ComposedOp forward & adjoint    src/fastop.cpp:100-281 (run on the GPU here)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <atomic>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/cww_b200.h"
+#include "cww_launch.h"
+
+using cww::Layout;
+
+namespace {
+
+thread_local std::string g_err;
+
+cww_status fail(cww_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess) return fail(CWW_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// filters
+// ---------------------------------------------------------------------------
+struct Filters {
+    int family = 0, nu = 1;
+    std::vector<double> h, g, phi;         // 2nu each
+    std::vector<double> E[2], A[2], B[2], Aw[2], Bw[2];  // [0] left, [1] right
+};
+
+uint32_t crc32_zlib(const unsigned char* p, size_t n) {
+    static uint32_t table[256];
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            table[i] = c;
+        }
+    });
+    uint32_t c = 0xFFFFFFFFu;
+    for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFFu] ^ (c >> 8);
+    return c ^ 0xFFFFFFFFu;
+}
+
+int spec_min_level(int nu) {
+    if (nu == 1) return 0;
+    int j = 0;
+    while ((1 << j) < 2 * nu) ++j;
+    return j;
+}
+
+std::string default_data_dir();
+
+cww_status load_filters(int family, int nu, const char* dir_in, Filters& f) {
+    f = Filters{};
+    f.family = family;
+    f.nu = nu;
+    if (nu == 1) {  // Haar, built in
+        double s = 1.0 / std::sqrt(2.0);
+        f.h = {s, s};
+        f.g = {s, -s};
+        f.phi = {1.0, 0.0};
+        return CWW_OK;
+    }
+    std::string dir = (dir_in && *dir_in) ? dir_in : default_data_dir();
+    std::string path = dir + "/" + (family == 0 ? "db" : "sym") + std::to_string(nu) + ".cwwf";
+    FILE* fp = std::fopen(path.c_str(), "rb");
+    if (!fp) return fail(CWW_ERR_DATA_IO, "cannot open filter data file: %s", path.c_str());
+    std::vector<unsigned char> b;
+    unsigned char buf[4096];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) b.insert(b.end(), buf, buf + got);
+    std::fclose(fp);
+    if (b.size() < 20) return fail(CWW_ERR_DATA_IO, "truncated filter data file: %s", path.c_str());
+    uint32_t stored;
+    std::memcpy(&stored, b.data() + b.size() - 4, 4);
+    if (crc32_zlib(b.data(), b.size() - 4) != stored)
+        return fail(CWW_ERR_DATA_IO, "checksum failure in filter data file: %s", path.c_str());
+    if (std::memcmp(b.data(), "CWWF", 4) != 0)
+        return fail(CWW_ERR_DATA_IO, "bad magic in filter data file: %s", path.c_str());
+    size_t pos = 4, end = b.size() - 4;
+    auto u32 = [&](uint32_t& v) {
+        if (pos + 4 > end) return false;
+        std::memcpy(&v, b.data() + pos, 4);
+        pos += 4;
+        return true;
+    };
+    auto mat = [&](uint32_t rows, uint32_t cols, std::vector<double>& dst) {
+        uint32_t r, c;
+        if (!u32(r) || !u32(c) || r != rows || c != cols) return false;
+        size_t n = size_t(r) * c;
+        if (pos + 8 * n > end) return false;
+        dst.resize(n);
+        std::memcpy(dst.data(), b.data() + pos, 8 * n);
+        pos += 8 * n;
+        return true;
+    };
+    uint32_t ver, fam, fnu, nmat;
+    if (!u32(ver) || !u32(fam) || !u32(fnu) || !u32(nmat))
+        return fail(CWW_ERR_DATA_IO, "truncated filter data file: %s", path.c_str());
+    if (ver != 1) return fail(CWW_ERR_DATA_IO, "unsupported filter data version in %s", path.c_str());
+    if (fam != uint32_t(family) || fnu != uint32_t(nu))
+        return fail(CWW_ERR_DATA_IO, "filter data header does not match requested wavelet: %s", path.c_str());
+    if (nmat != 13) return fail(CWW_ERR_DATA_IO, "unexpected matrix count in %s", path.c_str());
+    uint32_t L = 2 * nu, W = L - 1, V = nu;
+    bool ok = mat(1, L, f.h) && mat(1, L, f.g) && mat(1, L, f.phi);
+    for (int e = 0; e < 2 && ok; ++e)
+        ok = mat(V, W, f.E[e]) && mat(V, V, f.A[e]) && mat(V, W, f.B[e]) && mat(V, V, f.Aw[e]) &&
+             mat(V, W, f.Bw[e]);
+    if (!ok) return fail(CWW_ERR_DATA_IO, "filter data shape mismatch or truncation in %s", path.c_str());
+    double s = 0;
+    for (double x : f.h) s += x;
+    if (std::fabs(s - std::sqrt(2.0)) > 1e-10)
+        return fail(CWW_ERR_DATA_IO, "corrupt filter data (lowpass sum != sqrt2): %s", path.c_str());
+    return CWW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cascade and kernel table (host precompute, untimed)
+// ---------------------------------------------------------------------------
+struct Samples {
+    std::vector<double> v;
+    long left = 0;  // support_left (integer)
+    int R = 0;
+    double at(long g) const {
+        long i = g - left * (1l << R);
+        return (i < 0 || i >= long(v.size())) ? 0.0 : v[size_t(i)];
+    }
+};
+
+// phi(x) = sqrt2 sum_u h_u phi(2x-u) on the 2^-r grid over [a, b]
+std::vector<double> refine(const std::vector<double>& prev, int r, int a, int b,
+                           const std::vector<double>& h, int nu) {
+    long n = long(b - a) * (1l << r) + 1, half = 1l << (r - 1), lo = long(a) * half;
+    std::vector<double> cur(size_t(n), 0.0);
+    const double s2 = std::sqrt(2.0);
+    for (long t = 0; t < n; ++t) {
+        long x2 = long(a) * (1l << r) + t;  // 2x on the (r-1) grid
+        double acc = 0.0;
+        for (int u = -nu + 1; u <= nu; ++u) {
+            long i = x2 - u * half - lo;
+            if (i >= 0 && i < long(prev.size())) acc += h[size_t(u + nu - 1)] * prev[size_t(i)];
+        }
+        cur[size_t(t)] = s2 * acc;
+    }
+    return cur;
+}
+
+// left-edge functions 0..nu-1 in construction coordinates (support [0, nu+m])
+std::vector<std::vector<double>> cascade_edges(const std::vector<double>& h,
+                                               const std::vector<double>& phi,
+                                               const std::vector<double>& E,
+                                               const std::vector<double>& A,
+                                               const std::vector<double>& B, int nu, int R) {
+    const int a = -nu + 1, W = 2 * nu - 1;
+    std::vector<std::vector<double>> lev(static_cast<size_t>(R) + 1);
+    lev[0] = phi;
+    for (int r = 1; r <= R; ++r) lev[size_t(r)] = refine(lev[size_t(r - 1)], r, a, nu, h, nu);
+    std::vector<std::vector<double>> cur(static_cast<size_t>(nu));
+    for (int m = 0; m < nu; ++m) {
+        cur[size_t(m)].assign(size_t(nu + m + 1), 0.0);
+        for (long k = 0; k <= nu + m; ++k) {
+            double acc = 0.0;
+            for (int i = 0; i < W; ++i) {
+                long arg = k - (-nu + 1 + i);
+                if (arg > -nu && arg < nu) acc += E[size_t(m * W + i)] * phi[size_t(arg + nu - 1)];
+            }
+            cur[size_t(m)][size_t(k)] = acc;
+        }
+    }
+    const double s2 = std::sqrt(2.0);
+    for (int r = 1; r <= R; ++r) {
+        std::vector<std::vector<double>> nxt(static_cast<size_t>(nu));
+        const auto& il = lev[size_t(r - 1)];
+        for (int m = 0; m < nu; ++m) {
+            long n = long(nu + m) * (1l << r) + 1;
+            nxt[size_t(m)].assign(size_t(n), 0.0);
+            for (long t = 0; t < n; ++t) {
+                double acc = 0.0;
+                for (int k = 0; k < nu; ++k)
+                    if (t < long(cur[size_t(k)].size())) acc += A[size_t(m * nu + k)] * cur[size_t(k)][size_t(t)];
+                for (int li = 0; li <= 2 * m; ++li) {
+                    long idx = t - long(nu + li) * (1l << (r - 1)) - long(a) * (1l << (r - 1));
+                    double iv = (idx >= 0 && idx < long(il.size())) ? il[size_t(idx)] : 0.0;
+                    acc += B[size_t(m * W + li)] * iv;
+                }
+                nxt[size_t(m)][size_t(t)] = s2 * acc;
+            }
+        }
+        cur.swap(nxt);
+    }
+    return cur;
+}
+
+void fwht_seq_host(std::vector<double>& v) {
+    size_t n = v.size();
+    for (size_t h = 1; h < n; h <<= 1)
+        for (size_t i = 0; i < n; i += 2 * h)
+            for (size_t k = i; k < i + h; ++k) {
+                double a = v[k], b = v[k + h];
+                v[k] = a + b;
+                v[k + h] = a - b;
+            }
+    unsigned bits = 0;
+    while ((size_t(1) << bits) < n) ++bits;
+    std::vector<double> t(v);
+    for (size_t i = 0; i < n; ++i) {
+        size_t g = i ^ (i >> 1), r = 0;
+        for (unsigned b = 0; b < bits; ++b) r |= ((g >> b) & 1u) << (bits - 1 - b);
+        v[i] = t[r];
+    }
+}
+
+std::vector<double> cell_masses(const Samples& s, long x0, int q) {
+    const int R = s.R;
+    size_t cells = size_t(1) << q;
+    long per = 1l << (R - q);
+    double h = std::ldexp(1.0, -R);
+    std::vector<double> out(cells, 0.0);
+    long base = x0 * (1l << R);
+    for (size_t c = 0; c < cells; ++c) {
+        long st = base + long(c) * per;
+        double acc = 0.5 * (s.at(st) + s.at(st + per));
+        for (long i = 1; i < per; ++i) acc += s.at(st + i);
+        out[c] = acc * h;
+    }
+    return out;
+}
+
+struct KernelTable {
+    std::vector<double> interior, left, right;
+};
+
+cww_status kernel_table(const Filters& f, int vmp, int q, int R, KernelTable& t) {
+    const int nu = f.nu, W = 2 * nu - 1;
+    const size_t S = size_t(1) << q;
+    if (R < q) return fail(CWW_ERR_SPEC, "kernel quadrature requires R >= q");
+    t.interior.assign(size_t(W) * S, 0.0);
+    if (nu == 1) {  // Haar: kappa_0(s) = delta_{s0} exactly
+        t.interior[0] = 1.0;
+        return CWW_OK;
+    }
+    Samples in;
+    in.R = R;
+    in.left = -nu + 1;
+    in.v = f.phi;
+    for (int r = 1; r <= R; ++r) in.v = refine(in.v, r, -nu + 1, nu, f.h, nu);
+    for (int l = -nu + 1; l <= nu - 1; ++l) {
+        auto m = cell_masses(in, l, q);
+        fwht_seq_host(m);
+        std::copy(m.begin(), m.end(), t.interior.begin() + long(l + nu - 1) * long(S));
+    }
+    if (!vmp) return CWW_OK;
+    t.left.assign(size_t(nu * W) * S, 0.0);
+    t.right.assign(size_t(nu * W) * S, 0.0);
+    auto L = cascade_edges(f.h, f.phi, f.E[0], f.A[0], f.B[0], nu, R);
+    std::vector<double> hr(f.h.rbegin(), f.h.rend()), pr(f.phi.rbegin(), f.phi.rend());
+    auto Rt = cascade_edges(hr, pr, f.E[1], f.A[1], f.B[1], nu, R);
+    for (int m = 0; m < nu; ++m) {
+        Samples sl;
+        sl.R = R;
+        sl.left = 0;
+        sl.v = L[size_t(m)];
+        Samples sr;
+        sr.R = R;
+        sr.left = -(nu + m);
+        sr.v.assign(Rt[size_t(m)].rbegin(), Rt[size_t(m)].rend());
+        for (int l = 0; l <= nu - 1 + m; ++l) {
+            auto ms = cell_masses(sl, l, q);
+            fwht_seq_host(ms);
+            std::copy(ms.begin(), ms.end(), t.left.begin() + long(m * W + l) * long(S));
+        }
+        for (int tt = 0; tt <= nu + m - 1; ++tt) {
+            auto ms = cell_masses(sr, tt - (nu + m), q);
+            fwht_seq_host(ms);
+            std::copy(ms.begin(), ms.end(), t.right.begin() + long(m * W + tt) * long(S));
+        }
+    }
+    return CWW_OK;
+}
+
+std::string default_data_dir() {
+    if (const char* e = std::getenv("CWW_DATA_DIR"); e && *e) return e;
+#ifdef CWW_DEFAULT_DATA_DIR
+    return CWW_DEFAULT_DATA_DIR;
+#else
+    return "data";
+#endif
+}
+
+// ---- launch instrumentation ------------------------------------------------
+std::atomic<unsigned long long> g_launches{0};
+std::atomic<int> g_prof_on{0};
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+
+struct Prof {  // RAII bracket around one launcher call
+    const char* name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    int kernels;
+    Prof(const char* n, cudaStream_t s, int k = 1) : name(n), st(s), kernels(k) {
+        if (g_prof_on.load()) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~Prof() {
+        g_launches += (unsigned long long)kernels;
+        if (a) {
+            cudaEventRecord(b, st);
+            std::lock_guard<std::mutex> lk(g_prof_mu);
+            g_prof.push_back({name, a, b});
+        }
+    }
+};
+
+struct EdgeTerm {
+    uint64_t p;
+    int col;
+    long row;  // offset into the concatenated table interior|left|right
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// the op
+// ---------------------------------------------------------------------------
+struct cww_op {
+    cww_op_desc d{};
+    int nu = 1, vmp = 0, r0 = 0, dim = 1, device = 0;
+    unsigned j = 0, q = 0;
+    long long M = 1, N = 1, S = 1;
+    Filters f;
+    KernelTable kt;
+    std::vector<EdgeTerm> terms;
+    cww::Tables tabs{};
+    double* d_tab = nullptr;
+    std::string data_dir;
+};
+
+namespace {
+
+// device table block: kap | em | h | g | edge filters
+cww_status build_tables(cww_op& op) {
+    const int nu = op.nu, W = 2 * nu - 1, NP = 2 * nu - 1;
+    const long long S = op.S, M = op.M;
+    const double scale = 1.0 / std::sqrt(double(M));
+    std::vector<double> tab;
+    cww::Tables& t = op.tabs;
+    t.o_kap = 0;
+    for (int l = 0; l < W; ++l)
+        for (long long s = 0; s < S; ++s) tab.push_back(scale * op.kt.interior[size_t(l * S + s)]);
+    t.o_em = int(tab.size());
+    std::vector<double> em(size_t(S * 2 * NP * 2 * nu), 0.0);
+    if (nu > 1) {
+        const long long ofs_left = W * S, ofs_right = W * S + nu * W * S;
+        (void)ofs_left;
+        (void)ofs_right;
+        for (const auto& e : op.terms) {
+            int pi = e.p < uint64_t(NP) ? int(e.p) : NP + int(e.p - uint64_t(M - NP));
+            int c = e.col < nu ? e.col : nu + int(e.col - (M - nu));
+            const double* kap = nullptr;
+            std::vector<double> all;
+            all.insert(all.end(), op.kt.interior.begin(), op.kt.interior.end());
+            all.insert(all.end(), op.kt.left.begin(), op.kt.left.end());
+            all.insert(all.end(), op.kt.right.begin(), op.kt.right.end());
+            kap = all.data() + e.row;
+            for (long long s = 0; s < S; ++s) em[size_t(((s * 2 * NP) + pi) * 2 * nu + c)] += scale * kap[s];
+        }
+    }
+    tab.insert(tab.end(), em.begin(), em.end());
+    t.o_h = int(tab.size());
+    tab.insert(tab.end(), op.f.h.begin(), op.f.h.end());
+    t.o_g = int(tab.size());
+    tab.insert(tab.end(), op.f.g.begin(), op.f.g.end());
+    t.o_ef = int(tab.size());
+    for (int side = 0; side < 2; ++side) {
+        auto put = [&](const std::vector<double>& m, size_t n) {
+            for (size_t i = 0; i < n; ++i) tab.push_back(i < m.size() ? m[i] : 0.0);
+        };
+        put(op.f.A[side], size_t(nu * nu));
+        put(op.f.B[side], size_t(nu * W));
+        put(op.f.Aw[side], size_t(nu * nu));
+        put(op.f.Bw[side], size_t(nu * W));
+    }
+    t.n = int(tab.size());
+    CUDA_TRY(cudaMalloc(&op.d_tab, tab.size() * sizeof(double)));
+    CUDA_TRY(cudaMemcpy(op.d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return CWW_OK;
+}
+
+// Prop. 4.1 edge decomposition, grouped by position (fastop.cpp:54-98)
+void build_edge_terms(cww_op& op) {
+    op.terms.clear();
+    if (op.nu < 2) return;
+    const int nu = op.nu, W = 2 * nu - 1;
+    const long long S = op.S, M = op.M;
+    const long ofs_left = long(W * S), ofs_right = long(W * S + nu * W * S);
+    if (op.vmp) {
+        for (int m = 0; m < nu; ++m)
+            for (int l = 0; l <= nu - 1 + m; ++l) op.terms.push_back({uint64_t(l), m, ofs_left + long(m * W + l) * long(S)});
+        for (int mb = 0; mb < nu; ++mb)
+            for (int t = 0; t <= nu + mb - 1; ++t)
+                op.terms.push_back({uint64_t(M + t - (nu + mb)), int(M - 1 - mb), ofs_right + long(mb * W + t) * long(S)});
+    } else {
+        for (int side = 0; side < 2; ++side)
+            for (int k = 0; k < nu; ++k) {
+                int col = side ? int(M - nu + k) : k;
+                for (int l = -nu + 1; l <= nu - 1; ++l) {
+                    long long pos = (col + l) % M;
+                    if (pos < 0) pos += M;
+                    op.terms.push_back({uint64_t(pos), col, long(l + nu - 1) * long(S)});
+                }
+            }
+    }
+    std::stable_sort(op.terms.begin(), op.terms.end(),
+                     [](const EdgeTerm& a, const EdgeTerm& b) { return a.p < b.p; });
+}
+
+cww_status validate(const cww_op_desc* d) {
+    if (d->family != 0 && d->family != 1) return fail(CWW_ERR_INVALID_ARG, "bad family");
+    if (d->boundary != 0 && d->boundary != 1) return fail(CWW_ERR_INVALID_ARG, "bad boundary");
+    if (d->nu < 1 || d->nu > 6)
+        return fail(CWW_ERR_SPEC, "unsupported vanishing moments: %d (supported: 1..6)", d->nu);
+    if (d->nu == 1 && d->boundary == 1)
+        return fail(CWW_ERR_SPEC, "vmp boundary requires nu >= 2 (Haar has no boundary functions)");
+    if (d->nu == 1 && d->family == 1) return fail(CWW_ERR_SPEC, "sym1 is identical to Haar; use db1");
+    if (d->dim != 1 && d->dim != 2) return fail(CWW_ERR_SPEC, "FastOp dim must be 1 or 2");
+    const int J0 = spec_min_level(d->nu);
+    if (int(d->j) < J0) return fail(CWW_ERR_SPEC, "FastOp: j must be >= ceil(log2(2 nu))");
+    if (d->nu >= 2 && d->q < 1) return fail(CWW_ERR_SPEC, "FastOp: q must be >= 1");
+    if (d->j + d->q > 30) return fail(CWW_ERR_UNSUPPORTED, "j + q must be <= 30");
+    if (d->q > 10) return fail(CWW_ERR_UNSUPPORTED, "q must be <= 10");
+    if (d->dim == 2 && int(d->j) > cww::kSmallMaxLog)
+        return fail(CWW_ERR_UNSUPPORTED, "2D operator supports j <= %d", cww::kSmallMaxLog);
+    int r0 = d->min_level < 0 ? J0 : d->min_level;
+    if (r0 > int(d->j)) return fail(CWW_ERR_SPEC, "dwt: j below the coarsest admissible level");
+    if (d->boundary == 1 && r0 < J0)
+        return fail(CWW_ERR_SPEC, "vmp DWT requires min_level >= ceil(log2(2 nu)) = %d", J0);
+    int R = d->kernel_resolution > 0 ? d->kernel_resolution : 14;
+    if (R < int(d->q) || R > 24) return fail(CWW_ERR_SPEC, "kernel resolution must be in [q, 24]");
+    return CWW_OK;
+}
+
+cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
+
+// 1D layout helpers
+Layout lay_contig(long long len) { return Layout{0, len, 0, 1, 62, 62}; }
+
+// largest power of two V <= cap with V*M <= 2^13
+int small_V(long long M, long long nvec, int cap = 32) {
+    int V = 1;
+    while (V * 2 <= cap && (V * 2) * M <= (1ll << cww::kSmallMaxLog) && V * 2 <= nvec) V *= 2;
+    return V;
+}
+
+struct DevBuf {
+    double* p = nullptr;
+    cudaStream_t st = nullptr;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    cudaError_t alloc(size_t n, cudaStream_t s) {
+        st = s;
+        return cudaMallocAsync(&p, n * sizeof(double), s);
+    }
+};
+
+cww::SmallArgs small_args(const cww_op* op, const double* in, Layout lin, double* out,
+                          Layout lout, long long nvec, int V) {
+    cww::SmallArgs a{};
+    a.tab = op->d_tab;
+    a.t = op->tabs;
+    a.in = in;
+    a.out = out;
+    a.lin = lin;
+    a.lout = lout;
+    a.nvec = nvec;
+    a.V = V;
+    a.j = int(op->j);
+    a.q = int(op->q);
+    a.r0 = op->r0;
+    a.use_idwt = op->d.use_idwt;
+    a.vmp = op->vmp;
+    return a;
+}
+
+cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
+                     long long nvec, bool adj, cudaStream_t st) {
+    if (nvec == 0) return CWW_OK;
+    int V = small_V(op->M, nvec);
+    const bool vf = adj ? lin.vfast() : lout.vfast();
+    while (V > 1 && cww::small_smem_query(op->nu, V, int(op->j), int(op->q), adj, vf) > 200 * 1024) V /= 2;
+    if (cww::small_smem_query(op->nu, V, int(op->j), int(op->q), adj, vf) > 227 * 1024)
+        return fail(CWW_ERR_UNSUPPORTED, "shared-memory footprint too large for nu=%d j=%u q=%u", op->nu, op->j, op->q);
+    auto a = small_args(op, in, lin, out, lout, nvec, V);
+    Prof pr(adj ? "small_adj" : "small_fwd", st);
+    CUDA_TRY(cww::launch_small(op->nu, a, adj, st));
+    return CWW_OK;
+}
+
+// ---- large path (1D, M > 2^13) ----
+struct LargePlan {
+    int kl, ng;
+};
+LargePlan large_plan(unsigned j) {
+    int a = int(j) - cww::kLogB;
+    int kl = (a + 1) / 2;
+    if (kl > 8) kl = 8;
+    int kh = a - kl;
+    int ng = 1;
+    while (ng * (1 << kh) < 128 && ng * 2 <= (1 << kl)) ng *= 2;
+    return {kl, ng};
+}
+
+cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
+                     long long nvec, bool adj, cudaStream_t st) {
+    if (nvec == 0) return CWW_OK;
+    const long long M = op->M;
+    const int nu = op->nu, NP = 2 * nu - 1, CW = 32 + 2 * (nu - 1);
+    const long long A = M >> cww::kLogB;
+    const auto pl = large_plan(op->j);
+    const int Lc = std::min<int>(int(op->j) - 1, cww::kSmallMaxLog);
+    const bool idwt = op->d.use_idwt && op->r0 < int(op->j);
+    const long long nslot = cww::large_nslot(int(op->q), int(op->j), pl.kl, pl.ng);
+    DevBuf w0, w1, G, ev, epw;
+    CUDA_TRY(G.alloc(size_t(nvec * A * CW), st));
+    CUDA_TRY(ev.alloc(size_t(nvec * 2 * nu), st));
+    if (idwt) {
+        CUDA_TRY(w0.alloc(size_t(nvec * M), st));
+        CUDA_TRY(w1.alloc(size_t(nvec * M), st));
+    }
+    if (adj) CUDA_TRY(epw.alloc(size_t(nvec * nslot * op->S * 2 * NP + 1), st));
+
+    cww::LargeArgs a{};
+    a.tab = op->d_tab;
+    a.t = op->tabs;
+    a.j = int(op->j);
+    a.q = int(op->q);
+    a.kl = pl.kl;
+    a.ng = pl.ng;
+    a.nvec = nvec;
+    a.v0 = 0;
+    a.in = in;
+    a.lin = lin;
+    a.G = G.p;
+    a.ev = ev.p;
+    a.epw = epw.p;
+    a.nslot = nslot;
+    a.out = out;
+    a.lout = lout;
+
+    cww::WavArgs w{};
+    w.tab = op->d_tab;
+    w.t = op->tabs;
+    w.nvec = nvec;
+    w.r0 = op->r0;
+    w.vmp = op->vmp;
+
+    if (!adj) {
+        const double* xi = nullptr;
+        if (idwt) {
+            // coarse levels r0+1..Lc in shared memory, then one pass per fine level
+            int lc = std::max(Lc, op->r0);
+            w.kind = 0;
+            w.lev = lc;
+            w.inverse = 1;
+            w.src = in;
+            w.ls = lin;
+            w.sv0 = 0;
+            w.dst = w0.p;
+            w.dst_vs = M;
+            {
+                Prof pr("wav_coarse", st);
+                CUDA_TRY(cww::launch_wav(nu, w, st));
+            }
+            double* cur = w0.p;
+            double* nxt = w1.p;
+            for (int lev = lc + 1; lev <= int(op->j); ++lev) {
+                cww::WavArgs l{};
+                l.kind = 1;
+                l.tab = op->d_tab;
+                l.t = op->tabs;
+                l.nvec = nvec;
+                l.lev = lev;
+                l.vmp = op->vmp;
+                l.src = cur;
+                l.src_vs = M;
+                l.x = in;
+                l.lx = lin;
+                l.xv0 = 0;
+                l.dst = nxt;
+                l.dst_vs = M;
+                Prof pr("idwt_level", st);
+                CUDA_TRY(cww::launch_wav(nu, l, st));
+                std::swap(cur, nxt);
+            }
+            xi = cur;
+        }
+        a.xi = xi;
+        a.xi_vs = M;
+        a.xi_is_input = idwt ? 0 : 1;
+        {
+            Prof pr("large_fwd1", st);
+            CUDA_TRY(cww::launch_large(nu, 0, a, st));
+        }
+        {
+            Prof pr("large_fwd2", st);
+            CUDA_TRY(cww::launch_large(nu, 1, a, st));
+        }
+        return CWW_OK;
+    }
+    // adjoint
+    {
+        Prof pr("large_adj2", st);
+        CUDA_TRY(cww::launch_large(nu, 2, a, st));
+    }
+    a.xo = idwt ? w0.p : nullptr;
+    a.xo_vs = M;
+    a.xo_is_output = idwt ? 0 : 1;
+    {
+        Prof pr("large_adj1", st);
+        CUDA_TRY(cww::launch_large(nu, 3, a, st));
+    }
+    if (!idwt) return CWW_OK;
+    int lc = std::max(Lc, op->r0);
+    double* cur = w0.p;
+    double* nxt = w1.p;
+    for (int lev = int(op->j); lev > lc; --lev) {
+        cww::WavArgs l{};
+        l.kind = 2;
+        l.tab = op->d_tab;
+        l.t = op->tabs;
+        l.nvec = nvec;
+        l.lev = lev;
+        l.vmp = op->vmp;
+        l.src = cur;
+        l.src_vs = M;
+        l.dst = nxt;
+        l.dst_vs = M;
+        l.y = out;
+        l.ly = lout;
+        l.yv0 = 0;
+        Prof pr("dwt_level", st);
+        CUDA_TRY(cww::launch_wav(nu, l, st));
+        std::swap(cur, nxt);
+    }
+    w.kind = 0;
+    w.lev = lc;
+    w.inverse = 0;
+    w.src = cur;
+    w.src_vs = M;
+    w.dst = out;
+    w.ld = lout;
+    w.dv0 = 0;
+    Prof pr("wav_coarse", st);
+    CUDA_TRY(cww::launch_wav(nu, w, st));
+    return CWW_OK;
+}
+
+cww_status run_1d(const cww_op* op, const double* in, double* out, long long nvec, bool adj,
+                  cudaStream_t st) {
+    Layout lin = lay_contig(adj ? op->N : op->M), lout = lay_contig(adj ? op->M : op->N);
+    if (op->j <= unsigned(cww::kSmallMaxLog)) return run_small(op, in, lin, out, lout, nvec, adj, st);
+    return run_large(op, in, lin, out, lout, nvec, adj, st);
+}
+
+// 2D: rows then columns (forward), columns then rows (adjoint), with the
+// M x N intermediate stored in column panels of VC columns: [N/VC][M][VC].
+cww_status run_2d(const cww_op* op, const double* in, double* out, long long batch, bool adj,
+                  cudaStream_t st) {
+    const long long M = op->M, N = op->N;
+    const int j = int(op->j), jq = int(op->j + op->q);
+    int VC = small_V(M, N, 16);
+    int lvc = 0;
+    while ((1 << lvc) < VC) ++lvc;
+    DevBuf T;
+    CUDA_TRY(T.alloc(size_t(batch * M * N), st));
+    // row vectors: v = b*M + m ; column vectors: v = b*N + n
+    Layout x_rows{0, M, 0, 1, 62, 62};                     // x[v*M + i]
+    Layout t_rows{M * N, VC, M * VC, 1, j, lvc};           // T: (v>>j)*MN + (v&(M-1))*VC + (i>>lvc)*M*VC + (i&(VC-1))
+    Layout t_cols{M * VC, 1, 0, VC, lvc, 62};              // T: (v>>lvc)*M*VC + (v&(VC-1)) + i*VC
+    Layout y_cols{N * N, 1, 0, N, jq, 62};                 // y: (v>>jq)*N^2 + (v&(N-1)) + i*N
+    cww_status s;
+    if (!adj) {
+        if ((s = run_small(op, in, x_rows, T.p, t_rows, batch * M, false, st)) != CWW_OK) return s;
+        return run_small(op, T.p, t_cols, out, y_cols, batch * N, false, st);
+    }
+    if ((s = run_small(op, in, y_cols, T.p, t_cols, batch * N, true, st)) != CWW_OK) return s;
+    return run_small(op, T.p, t_rows, out, x_rows, batch * M, true, st);
+}
+
+cww_status run(const cww_op* op, const double* in, double* out, long long batch, bool adj,
+               cudaStream_t st) {
+    int cur = -1;
+    CUDA_TRY(cudaGetDevice(&cur));
+    if (cur != op->device) CUDA_TRY(cudaSetDevice(op->device));
+    if (op->dim == 1) return run_1d(op, in, out, batch, adj, st);
+    return run_2d(op, in, out, batch, adj, st);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// extern "C" ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* cww_last_error(void) { return g_err.c_str(); }
+const char* cww_version(void) { return "cww_b200 0.1 (sm_100a)"; }
+
+void cww_op_desc_init(cww_op_desc* d) {
+    if (!d) return;
+    std::memset(d, 0, sizeof *d);
+    d->family = CWW_DAUBECHIES;
+    d->nu = 2;
+    d->boundary = CWW_VMP;
+    d->j = 3;
+    d->q = 1;
+    d->dim = 1;
+    d->min_level = -1;
+    d->use_idwt = 0;
+    d->kernel_resolution = 0;
+    d->device = -1;
+    d->data_dir = nullptr;
+}
+
+cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
+    if (!desc || !out) return fail(CWW_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    cww_status s = validate(desc);
+    if (s != CWW_OK) return s;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(CWW_ERR_CUDA, "no CUDA device available (the operator has no CPU fallback)");
+    auto op = std::make_unique<cww_op>();
+    op->d = *desc;
+    op->nu = desc->nu;
+    op->vmp = desc->boundary;
+    op->j = desc->j;
+    op->q = desc->q;
+    op->dim = desc->dim;
+    op->M = 1ll << desc->j;
+    op->N = 1ll << (desc->j + desc->q);
+    op->S = 1ll << desc->q;
+    op->r0 = desc->min_level < 0 ? spec_min_level(desc->nu) : desc->min_level;
+    op->data_dir = desc->data_dir ? desc->data_dir : "";
+    if (desc->device >= 0) {
+        if (desc->device >= ndev) return fail(CWW_ERR_CUDA, "device %d not present", desc->device);
+        op->device = desc->device;
+    } else {
+        CUDA_TRY(cudaGetDevice(&op->device));
+    }
+    CUDA_TRY(cudaSetDevice(op->device));
+    if ((s = load_filters(desc->family, desc->nu, op->data_dir.c_str(), op->f)) != CWW_OK) return s;
+    int R = desc->kernel_resolution > 0 ? desc->kernel_resolution : 14;
+    if ((s = kernel_table(op->f, desc->boundary, int(desc->q), R, op->kt)) != CWW_OK) return s;
+    build_edge_terms(*op);
+    if ((s = build_tables(*op)) != CWW_OK) return s;
+    // keep freed workspace in the stream-ordered pool between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, op->device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = op.release();
+    return CWW_OK;
+}
+
+cww_status cww_op_destroy(cww_op* op) {
+    if (!op) return CWW_OK;
+    if (op->d_tab) cudaFree(op->d_tab);
+    delete op;
+    return CWW_OK;
+}
+
+cww_status cww_op_sizes(const cww_op* op, size_t* in, size_t* out) {
+    if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
+    size_t i = size_t(op->M), o = size_t(op->N);
+    if (op->dim == 2) i *= i, o *= o;
+    if (in) *in = i;
+    if (out) *out = o;
+    return CWW_OK;
+}
+
+static cww_status check_lens(const cww_op* op, size_t in_len, size_t out_len, size_t batch,
+                             bool adj, const char* what) {
+    if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
+    size_t ni, no;
+    cww_op_sizes(op, &ni, &no);
+    if (adj) std::swap(ni, no);
+    if (in_len != ni * batch || out_len != no * batch)
+        return fail(CWW_ERR_DIMENSION, "%s: dimension mismatch", what);
+    return CWW_OK;
+}
+
+cww_status cww_forward(const cww_op* op, const double* x, size_t x_len, double* y, size_t y_len,
+                       size_t batch, void* stream) {
+    cww_status s = check_lens(op, x_len, y_len, batch, false, "forward");
+    if (s != CWW_OK) return s;
+    if (batch == 0) return CWW_OK;
+    if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    return run(op, x, y, (long long)batch, false, S_(stream));
+}
+
+cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* x, size_t x_len,
+                       size_t batch, void* stream) {
+    cww_status s = check_lens(op, y_len, x_len, batch, true, "adjoint");
+    if (s != CWW_OK) return s;
+    if (batch == 0) return CWW_OK;
+    if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    return run(op, y, x, (long long)batch, true, S_(stream));
+}
+
+cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work, size_t work_len,
+                      size_t batch, int iters, void* stream) {
+    if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
+    size_t ni, no;
+    cww_op_sizes(op, &ni, &no);
+    if (x_len != ni * batch) return fail(CWW_ERR_DIMENSION, "normal: dimension mismatch");
+    if (work && work_len < no * batch) return fail(CWW_ERR_DIMENSION, "normal: work buffer too small");
+    cudaStream_t st = S_(stream);
+    DevBuf wb;
+    double* w = work;
+    if (!w) {
+        CUDA_TRY(wb.alloc(no * batch, st));
+        w = wb.p;
+    }
+    for (int it = 0; it < iters; ++it) {
+        cww_status s = run(op, x, w, (long long)batch, false, st);
+        if (s != CWW_OK) return s;
+        if ((s = run(op, w, x, (long long)batch, true, st)) != CWW_OK) return s;
+    }
+    return CWW_OK;
+}
+
+static cww_status host_call(const cww_op* op, const double* in, size_t in_len, double* out,
+                            size_t out_len, size_t batch, bool adj) {
+    cww_status s = check_lens(op, in_len, out_len, batch, adj, adj ? "adjoint" : "forward");
+    if (s != CWW_OK) return s;
+    if (batch == 0) return CWW_OK;
+    CUDA_TRY(cudaSetDevice(op->device));
+    cudaStream_t st;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double *din = nullptr, *dout = nullptr;
+    cww_status rs = CWW_OK;
+    cudaError_t e = cudaMallocAsync(&din, in_len * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&dout, out_len * 8, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(din, in, in_len * 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rs = fail(CWW_ERR_CUDA, "host staging: %s", cudaGetErrorString(e));
+    if (rs == CWW_OK) rs = run(op, din, dout, (long long)batch, adj, st);
+    if (rs == CWW_OK) {
+        e = cudaMemcpyAsync(out, dout, out_len * 8, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rs = fail(CWW_ERR_CUDA, "host staging: %s", cudaGetErrorString(e));
+    }
+    if (din) cudaFreeAsync(din, st);
+    if (dout) cudaFreeAsync(dout, st);
+    e = cudaStreamSynchronize(st);
+    if (rs == CWW_OK && e != cudaSuccess) rs = fail(CWW_ERR_CUDA, "%s", cudaGetErrorString(e));
+    cudaStreamDestroy(st);
+    return rs;
+}
+
+cww_status cww_forward_host(const cww_op* op, const double* x, size_t x_len, double* y,
+                            size_t y_len, size_t batch) {
+    return host_call(op, x, x_len, y, y_len, batch, false);
+}
+
+cww_status cww_adjoint_host(const cww_op* op, const double* y, size_t y_len, double* x,
+                            size_t x_len, size_t batch) {
+    return host_call(op, y, y_len, x, x_len, batch, true);
+}
+
+cww_status cww_dwt(const cww_op* op, double* data, size_t len, size_t batch, int dir, void* stream) {
+    if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
+    size_t ni;
+    cww_op_sizes(op, &ni, nullptr);
+    if (len != ni * batch) return fail(CWW_ERR_DIMENSION, "dwt: bad input length");
+    if (batch == 0 || op->r0 >= int(op->j)) return CWW_OK;
+    cudaStream_t st = S_(stream);
+    const long long M = op->M;
+    const int nu = op->nu;
+    const bool inverse = dir == CWW_DWT_INVERSE;
+    long long nvec = (long long)batch * (op->dim == 2 ? M : 1);
+    auto pass = [&](Layout l, long long nv) -> cww_status {
+        if (M <= (1ll << cww::kSmallMaxLog)) {
+            cww::WavArgs w{};
+            w.kind = 0;
+            w.tab = op->d_tab;
+            w.t = op->tabs;
+            w.nvec = nv;
+            w.lev = int(op->j);
+            w.r0 = op->r0;
+            w.inverse = inverse;
+            w.vmp = op->vmp;
+            // in place: both sides through the layout (src read fully before writes)
+            DevBuf tmp;
+            CUDA_TRY(tmp.alloc(size_t(nv * M), st));
+            w.src = data;
+            w.ls = l;
+            w.sv0 = 0;
+            w.src_vs = M;
+            if (inverse) {
+                w.dst = tmp.p;
+                w.dst_vs = M;
+                Prof pr("wav_coarse", st, 2);
+                CUDA_TRY(cww::launch_wav(nu, w, st));
+                // copy back through the layout with a forward "coarse" of zero levels
+                cww::WavArgs c = w;
+                c.inverse = 0;
+                c.r0 = int(op->j);
+                c.src = tmp.p;
+                c.src_vs = M;
+                c.dst = data;
+                c.ld = l;
+                c.dv0 = 0;
+                CUDA_TRY(cww::launch_wav(nu, c, st));
+            } else {
+                // gather into contiguous scratch, transform, scatter back
+                cww::WavArgs g = w;
+                g.inverse = 1;
+                g.r0 = int(op->j);
+                g.dst = tmp.p;
+                g.dst_vs = M;
+                Prof pr("wav_coarse", st, 2);
+                CUDA_TRY(cww::launch_wav(nu, g, st));
+                cww::WavArgs f = w;
+                f.inverse = 0;
+                f.src = tmp.p;
+                f.src_vs = M;
+                f.dst = data;
+                f.ld = l;
+                f.dv0 = 0;
+                CUDA_TRY(cww::launch_wav(nu, f, st));
+            }
+            return CWW_OK;
+        }
+        return fail(CWW_ERR_UNSUPPORTED, "standalone DWT supports j <= %d", cww::kSmallMaxLog);
+    };
+    if (op->dim == 1) return pass(lay_contig(M), nvec);
+    // 2D: rows (v = b*M + r: x[v*M + i]) then columns (v = b*M + c: x[(v>>j)*M^2 + (v&(M-1)) + i*M])
+    cww_status s = pass(Layout{0, M, 0, 1, 62, 62}, nvec);
+    if (s != CWW_OK) return s;
+    return pass(Layout{M * M, 1, 0, M, int(op->j), 62}, nvec);
+}
+
+cww_status cww_fwht(double* v, unsigned bits, size_t batch, int sequency, void* stream) {
+    if (!v && batch) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (bits > 30) return fail(CWW_ERR_UNSUPPORTED, "length too large");
+    if (batch == 0) return CWW_OK;
+    cudaStream_t st = S_(stream);
+    DevBuf scr;
+    if (bits > 13 && sequency) CUDA_TRY(scr.alloc(size_t(batch) << bits, st));
+    Prof pr("fwht", st, bits <= 13 ? 1 : int(bits) + (sequency ? 1 : 0));
+    CUDA_TRY(cww::launch_fwht(v, int(bits), (long long)batch, sequency, scr.p, st));
+    return CWW_OK;
+}
+
+cww_status cww_sequency_perm(unsigned bits, uint32_t* perm, void* stream) {
+    if (!perm) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (bits > 31) return fail(CWW_ERR_UNSUPPORTED, "bits must be <= 31");
+    Prof pr("seq_perm", S_(stream));
+    CUDA_TRY(cww::launch_seq_perm(perm, int(bits), S_(stream)));
+    return CWW_OK;
+}
+
+cww_status cww_walsh_sign_rows(const uint64_t* p, size_t npos, unsigned j, double* signs, void* stream) {
+    if ((!p || !signs) && npos) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (j > 30) return fail(CWW_ERR_UNSUPPORTED, "j must be <= 30");
+    if (npos == 0) return CWW_OK;
+    Prof pr("sign_rows", S_(stream));
+    CUDA_TRY(cww::launch_sign_rows(p, (long long)npos, int(j), signs, S_(stream)));
+    return CWW_OK;
+}
+
+cww_status cww_op_kernel_table(const cww_op* op, double* interior, size_t ni, double* left,
+                               size_t nl, double* right, size_t nr) {
+    if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
+    if (interior) {
+        if (ni < op->kt.interior.size()) return fail(CWW_ERR_DIMENSION, "interior buffer too small");
+        std::copy(op->kt.interior.begin(), op->kt.interior.end(), interior);
+    }
+    if (left && !op->kt.left.empty()) {
+        if (nl < op->kt.left.size()) return fail(CWW_ERR_DIMENSION, "left buffer too small");
+        std::copy(op->kt.left.begin(), op->kt.left.end(), left);
+    }
+    if (right && !op->kt.right.empty()) {
+        if (nr < op->kt.right.size()) return fail(CWW_ERR_DIMENSION, "right buffer too small");
+        std::copy(op->kt.right.begin(), op->kt.right.end(), right);
+    }
+    return CWW_OK;
+}
+
+cww_status cww_op_edge_terms(const cww_op* op, uint64_t* p, int32_t* col, int64_t* row, size_t cap,
+                             size_t* n) {
+    if (!op || !n) return fail(CWW_ERR_INVALID_ARG, "null argument");
+    *n = op->terms.size();
+    for (size_t i = 0; i < op->terms.size() && i < cap; ++i) {
+        if (p) p[i] = op->terms[i].p;
+        if (col) col[i] = op->terms[i].col;
+        if (row) row[i] = op->terms[i].row;
+    }
+    return CWW_OK;
+}
+
+// test_rng semantics (proj/tests/test_util.hpp:10-27) + SURVEY.md 8d inputs
+cww_status cww_synth(int kind, uint64_t seed, unsigned j, int r0, double density, int dim, double* out) {
+    if (!out) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (j > 28) return fail(CWW_ERR_UNSUPPORTED, "j too large");
+    struct Rng {
+        uint64_t s;
+        uint64_t u64() {
+            s ^= s << 13;
+            s ^= s >> 7;
+            s ^= s << 17;
+            return s * 0x2545F4914F6CDD1Dull;
+        }
+        double uni() { return double(u64() >> 11) * 0x1.0p-53; }
+        double normal() {
+            double u1 = uni(), u2 = uni();
+            if (u1 < 1e-300) u1 = 1e-300;
+            return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+        }
+    } rng{seed * 0x9E3779B97F4A7C15ull + 1};
+    const size_t side = size_t(1) << j, n = dim == 2 ? side * side : side;
+    auto level = [&](uint64_t i) {
+        if (i < (uint64_t(2) << r0)) return r0;
+        int l = 0;
+        while ((i >> (l + 1)) != 0) ++l;
+        return l;
+    };
+    size_t k = density >= 1.0 ? n : size_t(std::llround(density * double(n)));
+    std::vector<uint32_t> idx;
+    if (k < n) {
+        idx.resize(n);
+        for (size_t i = 0; i < n; ++i) idx[i] = uint32_t(i);
+        for (size_t i = 0; i < k; ++i) {
+            size_t t = i + size_t(rng.u64() % uint64_t(n - i));
+            std::swap(idx[i], idx[t]);
+        }
+        std::memset(out, 0, n * sizeof(double));
+    }
+    for (size_t i = 0; i < k; ++i) {
+        size_t pos = idx.empty() ? i : idx[i];
+        double v = rng.normal();
+        if (kind == 1) {
+            int lev = dim == 2 ? std::max(level(pos / side), level(pos % side)) : level(pos);
+            v = std::ldexp(v, -lev);
+        }
+        out[pos] = v;
+    }
+    return CWW_OK;
+}
+
+void cww_profile_enable(int on) { g_prof_on = on ? 1 : 0; }
+
+unsigned long long cww_kernel_launches(void) { return g_launches.load(); }
+
+cww_status cww_profile_dump(char* json, size_t cap) {
+    std::vector<ProfRec> recs;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        recs.swap(g_prof);
+    }
+    std::map<std::string, std::pair<double, long>> agg;
+    cww_status st = CWW_OK;
+    for (auto& r : recs) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess) st = fail(CWW_ERR_CUDA, "profile: %s", cudaGetErrorString(e));
+        auto& x = agg[r.name];
+        x.first += ms;
+        x.second += 1;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    std::string out = "{";
+    for (auto& [k, v] : agg) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "%s\"%s\": [%.6f, %ld]", out.size() > 1 ? ", " : "", k.c_str(), v.first, v.second);
+        out += buf;
+    }
+    out += "}";
+    if (json && cap) {
+        std::strncpy(json, out.c_str(), cap - 1);
+        json[cap - 1] = 0;
+    }
+    return st;
+}
+
+}  // extern "C"

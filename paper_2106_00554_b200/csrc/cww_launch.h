@@ -1,0 +1,85 @@
+// Kernel argument blocks and launcher prototypes shared by cww_host.cpp and
+// cww_kernels.cu.  Plain structs passed by value (kernel parameter space).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cww_device.cuh"
+
+namespace cww {
+
+constexpr int kSmallMaxLog = 13;  // M <= 2^13: whole map in one CTA's shared memory
+
+struct SmallArgs {
+    const double* tab;  // per-op device table block
+    Tables t;
+    const double* in;
+    double* out;
+    Layout lin, lout;
+    long long nvec;  // vectors in this launch
+    int V;           // vectors per CTA (power of two)
+    int j, q, r0, use_idwt, vmp;
+};
+
+struct LargeArgs {
+    const double* tab;
+    Tables t;
+    int j, q, kl, ng;  // kl: low K bits handled by the contiguous pass; ng: n_lo per CTA
+    long long nvec;
+    long long v0;      // global index of the first vector (for the I/O layouts)
+    // forward pass 1 source: xi workspace (xi_vs per vector) or the op input
+    const double* xi;
+    long long xi_vs;
+    int xi_is_input;
+    const double* in;
+    Layout lin;
+    // intermediate G: [nvec][A][CW]; edge values ev: [nvec][2nu]
+    double* G;
+    double* ev;
+    // adjoint edge partial sums: [nvec][nslot][S][2(2nu-1)]
+    double* epw;
+    long long nslot;
+    // outputs
+    double* out;
+    Layout lout;
+    double* xo;  // adjoint pass-1 destination (workspace) unless xo_is_output
+    long long xo_vs;
+    int xo_is_output;
+};
+
+struct WavArgs {
+    int kind;  // 0 coarse (one CTA per vector, shared memory); 1 idwt level; 2 dwt level
+    const double* tab;
+    Tables t;
+    long long nvec;
+    int lev;  // level (kind 1/2) or Lc (kind 0)
+    int r0, inverse, vmp;
+    // coarse: src via ls (inverse) or src + v*src_vs (forward); dst via dst_vs (inverse) or ld
+    const double* src;
+    Layout ls;
+    long long sv0, src_vs;
+    double* dst;
+    Layout ld;
+    long long dv0, dst_vs;
+    // level kernels: x/lx (idwt detail source), y/ly (dwt detail sink)
+    const double* x;
+    Layout lx;
+    long long xv0;
+    double* y;
+    Layout ly;
+    long long yv0;
+};
+
+cudaError_t launch_small(int nu, const SmallArgs& a, bool adj, cudaStream_t st);
+long long small_smem_query(int nu, int V, int j, int q, bool adj, bool vf);
+cudaError_t launch_large(int nu, int which, const LargeArgs& a, cudaStream_t st);
+long long large_nslot(int q, int j, int kl, int ng);
+cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st);
+cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, double* scratch,
+                        cudaStream_t st);
+cudaError_t launch_seq_perm(uint32_t* perm, int bits, cudaStream_t st);
+cudaError_t launch_sign_rows(const uint64_t* pos, long long npos, int j, double* out,
+                             cudaStream_t st);
+
+}  // namespace cww

@@ -1,0 +1,125 @@
+// Per-wavelet-order launchers.  Each cww_nu<N>.cu defines CWW_NU and includes
+// this file, so the kernel templates for one order compile in their own
+// translation unit (parallel build, bounded compile time).
+#pragma once
+#include "cww_kernels.cuh"
+
+#ifndef CWW_NU
+#error "define CWW_NU before including cww_nu_impl.cuh"
+#endif
+
+#define CWW_CAT2(a, b) a##b
+#define CWW_CAT(a, b) CWW_CAT2(a, b)
+#define CWW_FN(name) CWW_CAT(name, CWW_NU)
+
+namespace cww {
+
+#define CWW_NT 256
+
+namespace {
+constexpr int J0 = CWW_NU == 1 ? 0 : (CWW_NU == 2 ? 2 : (CWW_NU <= 4 ? 3 : 4));
+
+template <int LOGB>
+cudaError_t small_t(const SmallArgs& a, bool adj, cudaStream_t st) {
+    if constexpr (LOGB < J0) {
+        return cudaErrorInvalidValue;  // j >= J0 is validated on the host
+    } else {
+        int grid = (int)((a.nvec + a.V - 1) / a.V);
+        long long smem = small_smem_bytes<CWW_NU, LOGB>(a.V, a.j, a.q, adj, adj ? a.lin.vfast() : a.lout.vfast());
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+        if (adj) {
+            auto k = k_small_adj<CWW_NU, LOGB, CWW_NT>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k<<<grid, CWW_NT, smem, st>>>(a);
+        } else {
+            auto k = k_small_fwd<CWW_NU, LOGB, CWW_NT>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k<<<grid, CWW_NT, smem, st>>>(a);
+        }
+        return cudaGetLastError();
+    }
+}
+}  // namespace
+
+cudaError_t CWW_FN(launch_small_nu)(const SmallArgs& a, bool adj, cudaStream_t st) {
+    switch (a.j < kLogB ? a.j : kLogB) {
+        case 0: return small_t<0>(a, adj, st);
+        case 1: return small_t<1>(a, adj, st);
+        case 2: return small_t<2>(a, adj, st);
+        case 3: return small_t<3>(a, adj, st);
+        case 4: return small_t<4>(a, adj, st);
+        default: return small_t<5>(a, adj, st);
+    }
+}
+
+long long CWW_FN(small_smem_nu)(int V, int j, int q, bool adj, bool vf) {
+    switch (j < kLogB ? j : kLogB) {
+        case 0: return small_smem_bytes<CWW_NU, 0>(V, j, q, adj, vf);
+        case 1: return small_smem_bytes<CWW_NU, 1>(V, j, q, adj, vf);
+        case 2: return small_smem_bytes<CWW_NU, 2>(V, j, q, adj, vf);
+        case 3: return small_smem_bytes<CWW_NU, 3>(V, j, q, adj, vf);
+        case 4: return small_smem_bytes<CWW_NU, 4>(V, j, q, adj, vf);
+        default: return small_smem_bytes<CWW_NU, 5>(V, j, q, adj, vf);
+    }
+}
+
+cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t st) {
+    using Gm = Geo<CWW_NU, kLogB>;
+    const int acnt = a.j - kLogB, kh = acnt - a.kl, R1 = 1 << a.kl, R2 = 1 << kh;
+    const int S = 1 << a.q;
+    dim3 g1(1u << kh, (unsigned)a.nvec), g2((unsigned)(R1 / a.ng), (unsigned)a.nvec);
+    long long s1 = ((long long)R1 * Gm::RS) * 8;
+    long long s2 = ((long long)a.ng * R2 * Gm::RS + S * 2 * Gm::NP) * 8;
+    long long s1a = s1 + (S * 2 * Gm::NP + 2 * CWW_NU) * 8;
+    switch (which) {
+        case 0: {
+            auto k = k_large_fwd1<CWW_NU, CWW_NT>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+            k<<<g1, CWW_NT, s1, st>>>(a);
+            break;
+        }
+        case 1: {
+            auto k = k_large_fwd2<CWW_NU, CWW_NT>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+            k<<<g2, CWW_NT, s2, st>>>(a);
+            break;
+        }
+        case 2: {
+            auto k = k_large_adj2<CWW_NU, CWW_NT>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+            k<<<g2, CWW_NT, s2, st>>>(a);
+            break;
+        }
+        default: {
+            auto k = k_large_adj1<CWW_NU, CWW_NT>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1a);
+            k<<<g1, CWW_NT, s1a, st>>>(a);
+            break;
+        }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
+    const int nt = 256;
+    if (w.kind == 0) {
+        long long smem = (FiltSmem<CWW_NU>::SIZE + (1ll << w.lev)) * 8;
+        auto k = k_wav_coarse<CWW_NU>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<(unsigned)w.nvec, nt, smem, st>>>(w.tab, w.t, w.src, w.ls, w.sv0, w.src_vs, w.dst, w.ld,
+                                              w.dv0, w.dst_vs, w.r0, w.lev, w.inverse, w.vmp);
+    } else {
+        long long tot = (long long)w.nvec << w.lev;
+        int grid = (int)((tot + nt - 1) / nt);
+        if (grid > 148 * 16) grid = 148 * 16;
+        if (w.kind == 1)
+            k_idwt_level<CWW_NU><<<grid, nt, 0, st>>>(w.tab, w.t, w.src, w.src_vs, w.x, w.lx, w.xv0,
+                                                      w.dst, w.dst_vs, w.lev, (int)w.nvec, w.vmp);
+        else
+            k_dwt_level<CWW_NU><<<grid, nt, 0, st>>>(w.tab, w.t, w.src, w.src_vs, w.dst, w.dst_vs,
+                                                     w.y, w.ly, w.yv0, w.lev, (int)w.nvec, w.vmp);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace cww

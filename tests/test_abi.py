@@ -1,0 +1,94 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/cww_b200.h declares, validates specs like the reference
+(fastop.cpp:31-45, wavelet.cpp:31-39) and refuses to compute without a GPU
+(no CPU fallback).  No compute calls here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(REPO, "include", "cww_b200.h")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(cww_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_loads_and_exports_all_symbols():
+    import paper_2106_00554_b200 as cw
+    L = cw._load()
+    names = _declared()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(L, n), n
+    assert b"sm_100a" in L.cww_version()
+
+
+def _desc(**kw):
+    import paper_2106_00554_b200 as cw
+    d = cw._Desc()
+    cw._load().cww_op_desc_init(C.byref(d))
+    for k, v in kw.items():
+        setattr(d, k, v)
+    d.data_dir = cw.DATA_DIR.encode()
+    return d
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(nu=7), 3), (dict(nu=0), 3), (dict(nu=1, boundary=1), 3), (dict(nu=1, family=1, boundary=0), 3),
+    (dict(nu=4, j=2), 3), (dict(nu=2, q=0), 3), (dict(dim=3), 3), (dict(nu=4, j=6, min_level=2), 3),
+    (dict(nu=2, j=5, min_level=6), 3), (dict(family=5), 1), (dict(nu=2, j=14, dim=2), 7),
+])
+def test_spec_validation(kw, status):
+    import paper_2106_00554_b200 as cw
+    L = cw._load()
+    d = _desc(**kw)
+    h = C.c_void_p()
+    assert L.cww_op_create(C.byref(d), C.byref(h)) == status
+    assert L.cww_last_error()
+
+
+def test_no_cpu_fallback():
+    import torch
+    import paper_2106_00554_b200 as cw
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    L = cw._load()
+    d = _desc(nu=2, j=5, q=1)
+    h = C.c_void_p()
+    assert L.cww_op_create(C.byref(d), C.byref(h)) == 5  # CWW_ERR_CUDA
+    assert b"no CUDA device" in L.cww_last_error()
+    with pytest.raises(cw.CwwError):
+        cw.FastOp(cw.WaveletSpec(cw.Family.Daubechies, 2, cw.Boundary.Vmp), 5, 1)
+
+
+def test_python_spec_mirror():
+    import paper_2106_00554_b200 as cw
+    s = cw.parse_wavelet_name("db4", cw.Boundary.Vmp)
+    assert s.nu == 4 and s.min_level() == 3 and s.name() == "db4"
+    assert cw.parse_wavelet_name("sym6", cw.Boundary.Vmp).family == cw.Family.Symlet
+    assert cw.parse_wavelet_name("haar", cw.Boundary.Periodic).nu == 1
+    with pytest.raises(cw.CwwError):
+        cw.parse_wavelet_name("coif3", cw.Boundary.Vmp)
+    with pytest.raises(cw.CwwError):
+        cw.WaveletSpec(cw.Family.Daubechies, 1, cw.Boundary.Vmp).validate()
+
+
+@pytest.mark.parametrize("args", [(0, 1001, 10, 1, 1.0, 1), (1, 1002, 16, 4, 1.0, 1),
+                                  (0, 1003, 14, 4, 0.1, 1), (1, 1004, 6, 4, 0.05, 2),
+                                  (0, 1005, 7, 3, 0.02, 2)])
+def test_synth_matches_oracle(orc, args):
+    """The product's seeded-input generator equals the oracle's test_rng port."""
+    import paper_2106_00554_b200 as cw
+    kind, seed, j, r0, dens, dim = args
+    assert np.array_equal(cw.synth(kind, seed, j, r0, dens, dim), orc.synth(kind, seed, j, r0, dens, dim))
+
+
+def test_header_documents_reference_interfaces():
+    txt = open(HEADER).read()
+    for cite in ("fastop.hpp", "wavelet.hpp", "walsh.hpp", "kernel.hpp"):
+        assert cite in txt

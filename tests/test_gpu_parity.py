@@ -1,0 +1,259 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on
+the same seeded inputs.  Tolerance: relative L2 <= 1e-12 (fp64, BASELINE.json
+north_star); index / permutation / sign tables bit-exact.  At the full
+BASELINE sizes the size-independent properties (adjoint identity, linearity,
+normal operator) are checked, plus one full-size vector against the oracle."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _cw():
+    import paper_2106_00554_b200 as cw
+    return cw
+
+
+def make(fam, nu, bnd, j, q, dim=1, r0=-1, use_idwt=True):
+    cw = _cw()
+    spec = cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd))
+    if nu == 1:
+        return cw.HaarFullRankOp(j, q, 0 if r0 < 0 else r0) if use_idwt else None
+    op = cw.FastOp(spec, j, q, dim)
+    if not use_idwt:
+        return op
+    return cw.ComposedOp(op, None, True, None if r0 < 0 else r0)
+
+
+def gpu(x):
+    import torch
+    return torch.as_tensor(x, dtype=torch.float64, device="cuda")
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+# (family, nu, boundary, j, q, dim, r0) -- small / edge-case coverage
+SMALL = [
+    (0, 2, 1, 2, 1, 1, -1), (0, 2, 1, 3, 1, 1, -1), (0, 2, 1, 3, 2, 1, -1), (0, 3, 1, 3, 1, 1, -1),
+    (0, 4, 1, 3, 1, 1, -1), (0, 5, 1, 4, 1, 1, -1), (0, 6, 1, 4, 2, 1, -1), (0, 2, 1, 5, 1, 1, 3),
+    (0, 4, 1, 6, 2, 1, 4), (0, 3, 1, 7, 2, 1, 4), (0, 6, 1, 8, 3, 1, -1), (1, 4, 1, 9, 1, 1, -1),
+    (1, 5, 1, 10, 2, 1, 5), (0, 2, 0, 2, 1, 1, -1), (0, 3, 0, 5, 2, 1, -1), (0, 4, 0, 6, 1, 1, 3),
+    (1, 6, 0, 7, 3, 1, -1), (0, 2, 0, 9, 1, 1, 0), (0, 4, 1, 10, 1, 1, 4), (0, 2, 1, 12, 1, 1, 3),
+    (0, 3, 1, 13, 2, 1, 4), (0, 6, 0, 11, 2, 1, -1), (0, 1, 0, 0, 0, 1, 0), (0, 1, 0, 1, 1, 1, 0),
+    (0, 1, 0, 5, 0, 1, 0), (0, 1, 0, 10, 1, 1, 1), (0, 1, 0, 8, 2, 1, 3), (0, 1, 0, 13, 1, 1, 2),
+]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
+@pytest.mark.parametrize("use_idwt", [1, 0])
+def test_parity_1d(orc, cuda, case, use_idwt):
+    fam, nu, bnd, j, q, dim, r0 = case
+    if nu == 1 and not use_idwt:
+        pytest.skip("Haar op always composes the IDWT")
+    ref = orc.op(fam, nu, bnd, j, q, dim, r0)
+    op = make(fam, nu, bnd, j, q, dim, r0, bool(use_idwt))
+    B = 3
+    x = np.stack([orc.normals(100 + b, ref.nin) for b in range(B)])
+    y = np.stack([orc.normals(200 + b, ref.nout) for b in range(B)])
+    fx = host(op.forward(gpu(x)))
+    ay = host(op.adjoint(gpu(y)))
+    for b in range(B):
+        assert rel(fx[b], ref.forward(x[b], use_idwt)) <= TOL, b
+        assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL, b
+
+
+TWO_D = [(0, 2, 1, 3, 1, 2, -1), (0, 4, 1, 4, 1, 2, 4), (0, 2, 1, 6, 1, 2, 3), (0, 3, 0, 5, 2, 2, -1),
+         (0, 4, 1, 7, 1, 2, 4), (1, 5, 1, 5, 1, 2, -1), (0, 6, 0, 6, 1, 2, -1)]
+
+
+@pytest.mark.parametrize("case", TWO_D, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
+@pytest.mark.parametrize("use_idwt", [1, 0])
+def test_parity_2d(orc, cuda, case, use_idwt):
+    fam, nu, bnd, j, q, dim, r0 = case
+    ref = orc.op(*case)
+    op = make(fam, nu, bnd, j, q, dim, r0, bool(use_idwt))
+    x = np.stack([orc.normals(300 + b, ref.nin) for b in range(2)])
+    y = np.stack([orc.normals(400 + b, ref.nout) for b in range(2)])
+    fx, ay = host(op.forward(gpu(x))), host(op.adjoint(gpu(y)))
+    for b in range(2):
+        assert rel(fx[b], ref.forward(x[b], use_idwt)) <= TOL
+        assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL
+
+
+# large-M path (two-pass Hadamard with the L2-resident intermediate)
+LARGE = [(0, 4, 1, 14, 1, 1, 4), (0, 2, 1, 15, 2, 1, 3), (0, 4, 1, 16, 2, 1, 4), (0, 3, 0, 14, 1, 1, -1),
+         (1, 6, 1, 15, 1, 1, -1), (0, 1, 0, 14, 1, 1, 1), (0, 5, 1, 17, 1, 1, -1)]
+
+
+@pytest.mark.parametrize("case", LARGE, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
+@pytest.mark.parametrize("use_idwt", [1, 0])
+def test_parity_large(orc, cuda, case, use_idwt):
+    fam, nu, bnd, j, q, dim, r0 = case
+    if nu == 1 and not use_idwt:
+        pytest.skip("Haar op always composes the IDWT")
+    ref = orc.op(*case)
+    op = make(fam, nu, bnd, j, q, dim, r0, bool(use_idwt))
+    x = np.stack([orc.normals(500 + b, ref.nin) for b in range(2)])
+    y = np.stack([orc.normals(600 + b, ref.nout) for b in range(2)])
+    fx, ay = host(op.forward(gpu(x))), host(op.adjoint(gpu(y)))
+    for b in range(2):
+        assert rel(fx[b], ref.forward(x[b], use_idwt)) <= TOL
+        assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL
+
+
+# ---- BASELINE.json configurations ------------------------------------------
+CONFIGS = {  # (family, nu, boundary, j, q, dim, r0), (kind, density)
+    1: ((0, 1, 0, 10, 1, 1, 1), (0, 1.0)),
+    2: ((0, 4, 1, 16, 2, 1, 4), (1, 1.0)),
+    3: ((0, 3, 1, 21, 2, 1, 4), (0, 0.1)),
+    4: ((0, 4, 1, 10, 1, 2, 4), (1, 0.05)),
+    5: ((0, 2, 1, 12, 1, 2, 3), (0, 0.02)),
+}
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_config_against_oracle(orc, cuda, cfg):
+    (fam, nu, bnd, j, q, dim, r0), (kind, dens) = CONFIGS[cfg]
+    ref = orc.op(fam, nu, bnd, j, q, dim, r0)
+    op = make(fam, nu, bnd, j, q, dim, r0)
+    x = orc.synth(kind, 1000 * cfg, j, r0, dens, dim)
+    y = orc.normals(1000 * cfg + 500, ref.nout)
+    assert rel(host(op.forward(gpu(x))), ref.forward(x)) <= TOL
+    assert rel(host(op.adjoint(gpu(y))), ref.adjoint(y)) <= TOL
+
+
+def test_config3_one_vector_against_oracle(orc, cuda):
+    (fam, nu, bnd, j, q, dim, r0), (kind, dens) = CONFIGS[3]
+    ref = orc.op(fam, nu, bnd, j, q, dim, r0)
+    op = make(fam, nu, bnd, j, q, dim, r0)
+    x = orc.synth(kind, 3000, j, r0, dens)
+    assert rel(host(op.forward(gpu(x))), ref.forward(x)) <= TOL
+    y = orc.normals(3500, ref.nout)
+    assert rel(host(op.adjoint(gpu(y))), ref.adjoint(y)) <= TOL
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_config_properties_full_size(cuda, cfg):
+    """Adjoint identity <A x, y> = <x, A* y> and linearity at the full sizes."""
+    import torch
+    cw = _cw()
+    (fam, nu, bnd, j, q, dim, r0), (kind, dens) = CONFIGS[cfg]
+    op = make(fam, nu, bnd, j, q, dim, r0)
+    B = 2 if cfg in (3, 5) else 4
+    x = torch.stack([gpu(cw.synth(kind, 1000 * cfg + b, j, r0, dens, dim)) for b in range(B)])
+    g = torch.Generator(device="cuda").manual_seed(cfg)
+    y = torch.randn((B, op.rows()), generator=g, dtype=torch.float64, device="cuda")
+    Ax, Aty = op.forward(x), op.adjoint(y)
+    lhs = (Ax * y).sum(dim=1)
+    rhs = (x * Aty).sum(dim=1)
+    assert torch.all(torch.abs(lhs - rhs) <= 1e-12 * torch.linalg.norm(Ax, dim=1) * torch.linalg.norm(y, dim=1))
+    A2 = op.forward(2.0 * x[:1] - 3.0 * x[1:2])
+    assert rel(host(A2), host(2.0 * Ax[:1] - 3.0 * Ax[1:2])) <= 1e-13
+    # near-isometry bound ||A x|| <= ||x|| (orthonormal Walsh system, orthogonal W)
+    assert torch.all(torch.linalg.norm(Ax, dim=1) <= torch.linalg.norm(x, dim=1) * (1 + 1e-12))
+
+
+def test_normal_operator_matches_two_calls(cuda):
+    import torch
+    cw = _cw()
+    (fam, nu, bnd, j, q, dim, r0), _ = CONFIGS[5]
+    op = make(fam, nu, bnd, 8, q, dim, r0)
+    x = gpu(cw.synth(0, 5, 8, r0, 0.02, 2))
+    ref = op.adjoint(op.forward(op.adjoint(op.forward(x))))
+    out = op.normal(x.clone(), iters=2)
+    assert rel(host(out), host(ref)) <= 1e-13
+    assert torch.isfinite(out).all()
+
+
+def test_host_pointer_path(orc, cuda):
+    (fam, nu, bnd, j, q, dim, r0), (kind, dens) = CONFIGS[2]
+    ref = orc.op(fam, nu, bnd, 12, q, dim, r0)
+    op = make(fam, nu, bnd, 12, q, dim, r0)
+    x = np.stack([orc.synth(kind, 7 + b, 12, r0, dens) for b in range(3)])
+    fx = op.forward(x)  # numpy in -> the staged host path (cww_forward_host)
+    assert isinstance(fx, np.ndarray)
+    for b in range(3):
+        assert rel(fx[b], ref.forward(x[b])) <= TOL
+    y = orc.normals(9, ref.nout)
+    assert rel(op.adjoint(y), ref.adjoint(y)) <= TOL
+
+
+# ---- primitives: integer tables bit-exact, FWHT, DWT -------------------------
+@pytest.mark.parametrize("bits", [1, 5, 13, 18, 23])
+def test_sequency_perm_bit_exact(orc, cuda, bits):
+    cw = _cw()
+    got = host(cw.sequency_perm(bits)).astype(np.int64)
+    n = np.arange(1 << bits, dtype=np.int64)
+    g = n ^ (n >> 1)
+    expect = np.zeros_like(g)
+    for b in range(bits):
+        expect |= ((g >> b) & 1) << (bits - 1 - b)
+    assert np.array_equal(got, expect)
+    for k in list(range(min(64, 1 << bits))) + [(1 << bits) - 1]:
+        assert got[k] == orc.seq_to_nat(k, bits)
+
+
+def test_walsh_sign_rows_bit_exact(orc, cuda):
+    cw = _cw()
+    for j in (3, 6, 11):
+        ps = list(range(min(1 << j, 40))) + [(1 << j) - 1]
+        got = host(cw.walsh_sign_rows(ps, j))
+        for i, p in enumerate(ps):
+            assert np.array_equal(got[i], orc.sign_row(p, j))
+
+
+@pytest.mark.parametrize("bits", [3, 10, 13, 16])
+def test_fwht(orc, cuda, bits):
+    cw = _cw()
+    v = np.stack([orc.normals(bits + b, 1 << bits) for b in range(2)])
+    s = host(cw.fwht_sequency(gpu(v)))
+    n = host(cw.fwht_natural(gpu(v)))
+    for b in range(2):
+        assert rel(s[b], orc.fwht_sequency(v[b])) <= 1e-14
+        assert rel(n[b], orc.fwht_natural(v[b])) <= 1e-14
+    ones = host(cw.fwht_sequency(gpu(np.ones(8))))
+    assert ones[0] == 8.0 and np.all(ones[1:] == 0.0)
+
+
+@pytest.mark.parametrize("nu,bnd,j,r0,dim", [(2, 1, 7, 3, 1), (4, 1, 9, 4, 1), (3, 0, 8, -1, 1),
+                                             (1, 0, 10, 0, 1), (6, 1, 8, -1, 1), (2, 1, 5, 3, 2),
+                                             (4, 1, 6, 4, 2)])
+def test_dwt(orc, cuda, nu, bnd, j, r0, dim):
+    cw = _cw()
+    spec = cw.WaveletSpec(cw.Family.Daubechies, nu, cw.Boundary(bnd))
+    n = (1 << j) if dim == 1 else (1 << (2 * j))
+    x = orc.normals(77 + nu, n)
+    f = host(cw.dwt_apply(spec, j, gpu(x), False, r0, dim))
+    i = host(cw.dwt_apply(spec, j, gpu(x), True, r0, dim))
+    assert rel(f, orc.dwt(0, nu, bnd, j, x, 0, r0, dim)) <= 1e-14
+    assert rel(i, orc.dwt(0, nu, bnd, j, x, 1, r0, dim)) <= 1e-14
+
+
+def test_kernel_table_matches_oracle(orc, cuda):
+    cw = _cw()
+    for fam in (0, 1):
+        for nu in (2, 3, 4, 5, 6):
+            for bnd in (0, 1):
+                op = cw.FastOp(cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd)), nu + 3, 2)
+                got = op.kernel_table()
+                want = orc.kernel_table(fam, nu, bnd, 2)
+                for g_, w_ in zip(got, want):
+                    assert np.max(np.abs(g_ - w_)) <= 1e-15
+                assert [t[:2] for t in op.edge_terms()] == [t[:2] for t in orc.op(fam, nu, bnd, nu + 3, 2).edge_terms()]
+
+
+def test_dimension_mismatch_raises(cuda):
+    cw = _cw()
+    op = make(0, 2, 1, 5, 1)
+    with pytest.raises(cw.CwwError):
+        op.forward(gpu(np.zeros(33)))
