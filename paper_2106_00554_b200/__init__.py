@@ -42,7 +42,7 @@ __all__ = [
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libcww_b200.so")
+_LIB_PATH = os.path.join(_PKG, os.environ.get("CWW_LIB_NAME", "libcww_b200.so"))
 DATA_DIR = os.path.join(_PKG, "data")
 
 

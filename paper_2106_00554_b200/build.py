@@ -14,8 +14,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libcww_b200.so")
+BUILD = os.environ.get("CWW_BUILD_DIR", os.path.join(PKG, "_build"))
+LIB = os.path.join(PKG, os.environ.get("CWW_LIB_NAME", "libcww_b200.so"))
+EXTRA = os.environ.get("CWW_NVCC_FLAGS", "").split()
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -34,7 +35,7 @@ def _compile(src: str, verbose: bool) -> str:
             os.path.getmtime(p) for p in [src] + [os.path.join(CSRC, h) for h in os.listdir(CSRC)
                                                     if h.endswith((".h", ".cuh"))]):
         return obj
-    cmd = [NVCC] + ARCH + COMMON + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + COMMON + EXTRA + ["-c", src, "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
     else:

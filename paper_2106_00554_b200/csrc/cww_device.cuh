@@ -32,6 +32,8 @@ struct Tables {
     int o_h;    // [2nu] hbar_u, u = -nu+1..nu
     int o_g;    // [2nu] gbar_u
     int o_ef;   // [2][ A(nu*nu) | B(nu*(2nu-1)) | Aw | Bw ]  left, right
+    int o_syn;  // [2 sides][3nu-1][2 bands][2nu]  dense synthesis edge blocks
+    int o_ana;  // [2 sides][2 bands][nu][3nu-1]   dense analysis edge rows
     int n;      // total doubles
 };
 
@@ -47,6 +49,13 @@ struct Layout {
         long long ih = (esh >= 62) ? 0 : (i >> esh);
         return vh * vb + vm * vs + ih * eb + im * es;
     }
+    __host__ __device__ long long vbase(long long v) const {
+        return (vsh >= 62) ? v * vs : (v >> vsh) * vb + (v & ((1ll << vsh) - 1)) * vs;
+    }
+    __host__ __device__ long long eoff(long long i) const {
+        return (esh >= 62) ? i * es : (i >> esh) * eb + (i & ((1ll << esh) - 1)) * es;
+    }
+    __host__ __device__ bool contig() const { return esh >= 62 && es == 1; }
     // consecutive vectors are adjacent in memory: lanes should vary v first
     __host__ __device__ bool vfast() const { return vs == 1; }
 };
@@ -70,15 +79,20 @@ struct Geo {
     static constexpr int B = 1 << LOGB;
     static constexpr int H = NU - 1;
     static constexpr int CW = B + 2 * H;             // used columns per row
-    static constexpr int RS = ((CW + 15) / 16) * 16;  // smem row stride (doubles)
+    static constexpr int RS = CW | 1;                // odd smem row stride: conflict-free for
+                                                     // both row-wise and column-wise lanes
     static constexpr int NP = 2 * NU - 1;            // edge positions per side
 };
 
-// Bank-conflict-free addressing of tile element (row, e): the column index is
-// XOR-swizzled within its 16-double group by the low 4 bits of the lane-varying
-// index (bitrev_a(row) for rows visited in bit-reversed order by the row stage).
+// Tile element (physical row, e) lives at row * RS + e with an odd row
+// stride RS, which is bank-conflict free both for lanes that walk a row and
+// for lanes that walk consecutive rows.  Tiles store logical row K at physical row bitrev_a(K): the
+// Hadamard matrix is invariant under reversing the bits of both indices, so
+// H_A runs on physical rows with plain strides and the row stage reads
+// physical row w (= logical N = bitrev(w)) for consecutive lanes w.
 __device__ __forceinline__ int tile_idx(int row, int e, int RS, int sw) {
-    return row * RS + (e ^ (sw & 15));
+    (void)sw;
+    return row * RS + e;
 }
 
 // In-register natural-order Hadamard butterflies over R bits.
@@ -98,48 +112,42 @@ __device__ __forceinline__ void hadamard_reg(double* x) {
     }
 }
 
-// One radix-2^R pass of H_A along the row index of V tiles held in smem
-// (rows 0..A-1 of each tile, columns 0..CW-1), over row bits [lo, lo+R).
-template <int R>
-__device__ void tile_hadamard_pass(double* T, int V, int a, int lo, int CW, int RS,
-                                   long long tstride, int tid, int nt) {
-    const int A = 1 << a;
-    const int groups = A >> R;
-    const long long items = (long long)V * CW * groups;
-    for (long long it = tid; it < items; it += nt) {
-        int e = (int)(it % CW);
-        long long rest = it / CW;
-        int fb = (int)(rest % groups);
-        int v = (int)(rest / groups);
-        int low = fb & ((1 << lo) - 1);
-        int row0 = ((fb >> lo) << (lo + R)) | low;
-        double* t = T + v * tstride;
+// One radix-2^R pass of H_A along the physical row index of V tiles held in
+// smem (rows 0..2^a-1, columns 0..CW-1), over row bits [lo, lo+R).
+template <int R, int CW, int RS>
+__device__ __forceinline__ void tile_hadamard_pass(double* T, int V, int a, int lo, int tstride,
+                                                   int tid, int nt) {
+    const int groups = (1 << a) >> R;
+    const int items = V * CW * groups;
+    for (int it = tid; it < items; it += nt) {
+        const int e = it % CW;
+        const int rest = it / CW;
+        const int fb = rest & (groups - 1);
+        const int v = rest >> (a - R);
+        const int low = fb & ((1 << lo) - 1);
+        const int row0 = ((fb >> lo) << (lo + R)) | low;
+        double* t = T + v * tstride + row0 * RS + e;
         double x[1 << R];
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) {
-            int row = row0 + (k << lo);
-            x[k] = t[tile_idx(row, e, RS, brev_bits(row, a))];
-        }
+        for (int k = 0; k < (1 << R); ++k) x[k] = t[(k << lo) * RS];
         hadamard_reg<R>(x);
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) {
-            int row = row0 + (k << lo);
-            t[tile_idx(row, e, RS, brev_bits(row, a))] = x[k];
-        }
+        for (int k = 0; k < (1 << R); ++k) t[(k << lo) * RS] = x[k];
     }
 }
 
-// Full H_A (a row bits) in passes of <= 5 bits, restricted to bits [lo, hi).
-static __device__ __noinline__ void tile_hadamard(double* T, int V, int a, int lo, int hi, int CW, int RS,
-                              long long tstride, int tid, int nt) {
+// H_A restricted to row bits [lo, hi), passes of <= 5 bits, __syncthreads after each.
+template <int CW, int RS>
+__device__ __noinline__ void tile_hadamard(double* T, int V, int a, int lo, int hi, int tstride,
+                                           int tid, int nt) {
     while (lo < hi) {
-        int r = hi - lo < 5 ? hi - lo : 5;
+        const int r = hi - lo < 5 ? hi - lo : 5;
         switch (r) {
-            case 1: tile_hadamard_pass<1>(T, V, a, lo, CW, RS, tstride, tid, nt); break;
-            case 2: tile_hadamard_pass<2>(T, V, a, lo, CW, RS, tstride, tid, nt); break;
-            case 3: tile_hadamard_pass<3>(T, V, a, lo, CW, RS, tstride, tid, nt); break;
-            case 4: tile_hadamard_pass<4>(T, V, a, lo, CW, RS, tstride, tid, nt); break;
-            default: tile_hadamard_pass<5>(T, V, a, lo, CW, RS, tstride, tid, nt); break;
+            case 1: tile_hadamard_pass<1, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            case 2: tile_hadamard_pass<2, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            case 3: tile_hadamard_pass<3, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            case 4: tile_hadamard_pass<4, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            default: tile_hadamard_pass<5, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
         }
         __syncthreads();
         lo += r;
@@ -153,8 +161,21 @@ template <int NU>
 struct FiltSmem {
     static constexpr int W = 2 * NU - 1;
     static constexpr int SIDE = 2 * NU * NU + 2 * NU * W;
-    static constexpr int SIZE = 4 * NU + 2 * SIDE;
+    static constexpr int EL = 3 * NU - 1;  // edge-region width of one level
+    static constexpr int CI = 2 * NU;      // coarse/detail inputs an edge sample reads
+    static constexpr int SYN = 2 * EL * 2 * CI;
+    static constexpr int ANA = 2 * 2 * NU * EL;
+    static constexpr int SIZE = 4 * NU + 2 * SIDE + SYN + ANA;
     const double* f;
+    // dense synthesis edge block, layout [side][band][k][i]: coefficient of
+    // c[k] (band 0) / d[k] (band 1) in edge sample i is syn(side, i, band)[k * EL]
+    __device__ const double* syn(int side, int i, int band) const {
+        return f + 4 * NU + 2 * SIDE + (side * 2 + band) * CI * EL + i;
+    }
+    // dense analysis edge row m (band 0 coarse, 1 detail)
+    __device__ const double* ana(int side, int band, int m) const {
+        return f + 4 * NU + 2 * SIDE + SYN + ((side * 2 + band) * NU + m) * EL;
+    }
     __device__ double h(int u) const { return f[u + NU - 1]; }
     __device__ double g(int u) const { return f[2 * NU + u + NU - 1]; }
     __device__ const double* A(int side) const { return f + 4 * NU + side * SIDE; }
@@ -166,11 +187,9 @@ struct FiltSmem {
 // Synthesis (one IDWT level): fine sample i of a length-n level from
 // c = x[0:n/2], d = x[n/2:n].
 template <int NU>
-__device__ __noinline__ double idwt_sample_full(const FiltSmem<NU> F, const double* x, int n, int i,
-                                                bool vmp) {
+__device__ __noinline__ double idwt_sample_full2(const FiltSmem<NU> F, const double* c,
+                                                 const double* d, int n, int i, bool vmp) {
     const int half = n >> 1;
-    const double* c = x;
-    const double* d = x + half;
     double acc = 0.0;
     if (!vmp) {  // periodic: scratch[(2mm+u) mod n] += hbar c + gbar d (387-400)
 #pragma unroll
@@ -254,42 +273,177 @@ __device__ __noinline__ double dwt_sample_full(const FiltSmem<NU> F, const doubl
     return acc;
 }
 
-// Fast paths: away from both ends (3nu-1 <= i <= n-3nu) every synthesis term
-// is an interior column and no index wraps, for both boundary modes; the
-// rest goes through the out-of-line full sample.
+// Interior synthesis/analysis taps held in registers.
 template <int NU>
-__device__ __forceinline__ double idwt_sample(const FiltSmem<NU>& F, const double* x, int n, int i,
-                                              bool vmp) {
-    if (i >= 3 * NU - 1 && i <= n - 3 * NU) {
-        const int half = n >> 1;
-        const int par = (i + NU + 1) & 1;
+struct Taps {
+    double h[2 * NU], g[2 * NU];
+    __device__ __forceinline__ explicit Taps(const FiltSmem<NU>& F) {
+#pragma unroll
+        for (int k = 0; k < 2 * NU; ++k) {
+            h[k] = F.f[k];
+            g[k] = F.f[2 * NU + k];
+        }
+    }
+};
+
+// Synthesis of one fine sample i of a length-n level from c = cv[0:n/2],
+// d = dv[0:n/2].  Periodic: masked (mod n) indices, exact everywhere.  VMP:
+// the interior formula for 3nu-1 <= i <= n-3nu; the first/last 3nu-1 samples
+// from the dense level-independent edge blocks (valid for n >= 8nu); the
+// generic edge code only for the few coarsest levels (n < 8nu).
+template <int NU>
+__device__ __forceinline__ double idwt_one(const FiltSmem<NU>& F, const double* cv, const double* dv,
+                                           int n, int i, bool vmp) {
+    const int half = n >> 1;
+    const int par = (i + NU + 1) & 1;
+    if (!vmp) {
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < NU; ++k) {
-            int u = -NU + 1 + 2 * k + par;
-            int mm = (i - u) >> 1;
-            acc += F.h(u) * x[mm] + F.g(u) * x[half + mm];
+            const int u = -NU + 1 + 2 * k + par;
+            const int mm = ((i - u) & (n - 1)) >> 1;
+            acc += F.h(u) * cv[mm] + F.g(u) * dv[mm];
         }
         return acc;
     }
-    return idwt_sample_full<NU>(F, x, n, i, vmp);
-}
-
-// analysis: coarse/detail rows NU <= mm < half-NU use the plain 2nu taps
-template <int NU>
-__device__ __forceinline__ double dwt_sample(const FiltSmem<NU>& F, const double* x, int n, int o,
-                                             bool vmp) {
-    const int half = n >> 1;
-    const bool det = o >= half;
-    const int mm = det ? o - half : o;
-    if (mm >= NU && mm < half - NU) {
-        const double* f = det ? F.f + 2 * NU : F.f;
+    constexpr int EL = FiltSmem<NU>::EL, CI = FiltSmem<NU>::CI;
+    if (n < 8 * NU) return idwt_sample_full2<NU>(F, cv, dv, n, i, vmp);
+    if (i < EL || i >= n - EL) {
+        const int side = i < EL ? 0 : 1;
+        const int ii = side ? n - 1 - i : i;
+        const double* sc = F.syn(side, ii, 0);
+        const double* sd = F.syn(side, ii, 1);
         double acc = 0.0;
 #pragma unroll
-        for (int u = -NU + 1; u <= NU; ++u) acc += f[u + NU - 1] * x[2 * mm + u];
+        for (int k = 0; k < CI; ++k) {
+            const int idx = side ? half - 1 - k : k;
+            acc += sc[k * EL] * cv[idx] + sd[k * EL] * dv[idx];
+        }
         return acc;
     }
-    return dwt_sample_full<NU>(F, x, n, o, vmp);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+        const int u = -NU + 1 + 2 * k + par;
+        const int mm = (i - u) >> 1;
+        acc += F.h(u) * cv[mm] + F.g(u) * dv[mm];
+    }
+    return acc;
+}
+
+// Paired synthesis: fine samples 2m and 2m+1 share one window of nu+1 coarse
+// and nu+1 detail samples (periodic: masked indices, always; VMP: interior
+// pairs), otherwise two single samples.
+template <int NU>
+__device__ __forceinline__ void idwt_pair(const FiltSmem<NU>& F, const double* cv, const double* dv,
+                                          int n, int m, bool vmp, double& o0, double& o1) {
+    const int i = 2 * m;
+    const int half = n >> 1;
+    const bool inner = !vmp || (i >= 3 * NU - 1 && i + 1 <= n - 3 * NU);
+    if (inner) {
+        constexpr int OFF = (NU + 1) / 2;  // window c[m-OFF .. m-OFF+NU]
+        double cw[NU + 1], dw[NU + 1];
+#pragma unroll
+        for (int k = 0; k <= NU; ++k) {
+            const int idx = vmp ? m - OFF + k : ((m - OFF + k) & (half - 1));
+            cw[k] = cv[idx];
+            dw[k] = dv[idx];
+        }
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            if ((u & 1) == 0) {  // even u feeds the even sample: mm = m - u/2
+                const int idx = OFF - u / 2;
+                a0 += F.h(u) * cw[idx] + F.g(u) * dw[idx];
+            } else {  // odd u feeds the odd sample: mm = m - (u-1)/2
+                const int idx = OFF - (u - 1) / 2;
+                a1 += F.h(u) * cw[idx] + F.g(u) * dw[idx];
+            }
+        }
+        o0 = a0;
+        o1 = a1;
+        return;
+    }
+    o0 = idwt_one<NU>(F, cv, dv, n, i, vmp);
+    o1 = idwt_one<NU>(F, cv, dv, n, i + 1, vmp);
+}
+
+// Interior pair with register taps (caller guarantees the pair is interior
+// for VMP; periodic: masked indices, any pair).
+template <int NU>
+__device__ __forceinline__ void idwt_pair_inner(const Taps<NU>& tp, const double* cv, const double* dv,
+                                                int n, int m, bool vmp, double& o0, double& o1) {
+    constexpr int OFF = (NU + 1) / 2;
+    const int half = n >> 1;
+    double cw[NU + 1], dw[NU + 1];
+#pragma unroll
+    for (int k = 0; k <= NU; ++k) {
+        const int idx = vmp ? m - OFF + k : ((m - OFF + k) & (half - 1));
+        cw[k] = cv[idx];
+        dw[k] = dv[idx];
+    }
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;  // four independent chains
+#pragma unroll
+    for (int u = -NU + 1; u <= NU; ++u) {
+        if ((u & 1) == 0) {
+            const int idx = OFF - u / 2;
+            a0 += tp.h[u + NU - 1] * cw[idx];
+            b0 += tp.g[u + NU - 1] * dw[idx];
+        } else {
+            const int idx = OFF - (u - 1) / 2;
+            a1 += tp.h[u + NU - 1] * cw[idx];
+            b1 += tp.g[u + NU - 1] * dw[idx];
+        }
+    }
+    o0 = a0 + b0;
+    o1 = a1 + b1;
+}
+
+// Analysis: coarse and detail row mm of a length-n level from x[0:n].
+// Periodic: masked indices.  VMP: interior rows use the 2nu taps, the nu
+// edge rows per side the dense [A|B] / [Aw|Bw] rows (any level n >= 4nu).
+template <int NU>
+__device__ __forceinline__ void dwt_pair(const FiltSmem<NU>& F, const double* x, int n, int mm,
+                                         bool vmp, double& c, double& d) {
+    const int half = n >> 1;
+    double a = 0.0, b = 0.0;
+    if (!vmp) {
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            const double xv = x[(2 * mm + u) & (n - 1)];
+            a += F.h(u) * xv;
+            b += F.g(u) * xv;
+        }
+    } else if (mm >= NU && mm < half - NU) {
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            const double xv = x[2 * mm + u];
+            a += F.h(u) * xv;
+            b += F.g(u) * xv;
+        }
+    } else {
+        constexpr int EL = FiltSmem<NU>::EL;
+        const int side = mm < NU ? 0 : 1;
+        const int m = side ? half - 1 - mm : mm;
+        const double* ra = F.ana(side, 0, m);
+        const double* rb = F.ana(side, 1, m);
+#pragma unroll
+        for (int k = 0; k < EL; ++k) {
+            const double xv = x[side ? n - 1 - k : k];
+            a += ra[k] * xv;
+            b += rb[k] * xv;
+        }
+    }
+    c = a;
+    d = b;
+}
+
+// gray^-1(bitrev_5(nl) << a): gray^-1 is linear over XOR and
+// gray^-1(x << a) = (gray^-1(x) << a) | (parity(x) ? 2^a - 1 : 0).
+__device__ __forceinline__ unsigned gray_inv_hi(int nl, int logb, int a) {
+    const unsigned x = brev_bits((unsigned)nl, logb);
+    const unsigned gx = gray_inv(x);
+    return (gx << a) | ((__popc(x) & 1) ? ((1u << a) - 1u) : 0u);
 }
 
 }  // namespace cww

@@ -353,6 +353,33 @@ struct Prof {  // RAII bracket around one launcher call
     }
 };
 
+// One VMP synthesis level (wavelet.cpp:447-483 semantics), used only to
+// extract the level-independent edge blocks below.
+std::vector<double> level_inverse_vmp_host(const Filters& f, const std::vector<double>& x) {
+    const size_t n = x.size(), half = n / 2, NV = size_t(f.nu);
+    const int nu = f.nu, W = 2 * nu - 1;
+    std::vector<double> s(n, 0.0);
+    for (int band = 0; band < 2; ++band)
+        for (int side = 0; side < 2; ++side) {
+            const auto& A = band ? f.Aw[side] : f.A[side];
+            const auto& B = band ? f.Bw[side] : f.B[side];
+            for (size_t m = 0; m < NV; ++m) {
+                size_t row = side ? half - 1 - m : m;
+                double c = x[(band ? half : 0) + row];
+                for (size_t k = 0; k < NV; ++k) s[side ? n - 1 - k : k] += A[m * NV + k] * c;
+                for (int li = 0; li <= 2 * int(m); ++li) {
+                    size_t l = NV + size_t(li);
+                    s[side ? n - 1 - l : l] += B[m * size_t(W) + size_t(li)] * c;
+                }
+            }
+        }
+    for (size_t mm = NV; mm + NV < half; ++mm) {
+        double c = x[mm], d = x[half + mm];
+        for (int u = -nu + 1; u <= nu; ++u) s[size_t(long(2 * mm) + u)] += f.h[size_t(u + nu - 1)] * c + f.g[size_t(u + nu - 1)] * d;
+    }
+    return s;
+}
+
 struct EdgeTerm {
     uint64_t p;
     int col;
@@ -422,6 +449,44 @@ cww_status build_tables(cww_op& op) {
         put(op.f.Aw[side], size_t(nu * nu));
         put(op.f.Bw[side], size_t(nu * W));
     }
+    // Dense edge blocks of one VMP level (valid for n >= 8 nu; coarser levels
+    // use the generic path):  synthesis  out[i] = sum_k Sc[i][k] c[k] + Sd[i][k] d[k],
+    // i < 3nu-1, k < 2nu (right side mirrored: i -> n-1-i, k -> half-1-k);
+    // analysis  row m < nu: sum_k Da[m][k] x[k], k < 3nu-1 (A | B restricted to
+    // li <= 2m as in wavelet.cpp:419-423; detail rows from Aw | Bw).
+    t.o_syn = int(tab.size());
+    const int EL = 3 * nu - 1, CI = 2 * nu;
+    if (nu == 1) tab.insert(tab.end(), size_t(2 * EL * 2 * CI + 2 * 2 * nu * EL), 0.0);
+    if (nu > 1) {
+        const size_t n = size_t(16 * nu), half = n / 2;
+        std::vector<double> syn(size_t(2 * EL * 2 * CI), 0.0);
+        for (int band = 0; band < 2; ++band)
+            for (int k = 0; k < CI; ++k)
+                for (int side = 0; side < 2; ++side) {
+                    std::vector<double> x(n, 0.0);
+                    size_t idx = side ? half - 1 - size_t(k) : size_t(k);
+                    x[(band ? half : 0) + idx] = 1.0;
+                    auto y = level_inverse_vmp_host(op.f, x);
+                    for (int i = 0; i < EL; ++i)  // [side][band][k][i]: lanes (i) read consecutively
+                        syn[size_t(((side * 2 + band) * CI + k) * EL + i)] = y[side ? n - 1 - size_t(i) : size_t(i)];
+                }
+        tab.insert(tab.end(), syn.begin(), syn.end());
+    }
+    t.o_ana = int(tab.size());
+    if (nu > 1) {
+        std::vector<double> ana(size_t(2 * 2 * nu * EL), 0.0);
+        for (int side = 0; side < 2; ++side)
+            for (int band = 0; band < 2; ++band) {
+                const auto& A = band ? op.f.Aw[side] : op.f.A[side];
+                const auto& B = band ? op.f.Bw[side] : op.f.B[side];
+                for (int m = 0; m < nu; ++m) {
+                    double* row = ana.data() + ((side * 2 + band) * nu + m) * EL;
+                    for (int k = 0; k < nu; ++k) row[k] = A[size_t(m * nu + k)];
+                    for (int li = 0; li <= 2 * m; ++li) row[nu + li] = B[size_t(m * W + li)];
+                }
+            }
+        tab.insert(tab.end(), ana.begin(), ana.end());
+    }
     t.n = int(tab.size());
     CUDA_TRY(cudaMalloc(&op.d_tab, tab.size() * sizeof(double)));
     CUDA_TRY(cudaMemcpy(op.d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -469,6 +534,7 @@ cww_status validate(const cww_op_desc* d) {
     if (int(d->j) < J0) return fail(CWW_ERR_SPEC, "FastOp: j must be >= ceil(log2(2 nu))");
     if (d->nu >= 2 && d->q < 1) return fail(CWW_ERR_SPEC, "FastOp: q must be >= 1");
     if (d->j + d->q > 30) return fail(CWW_ERR_UNSUPPORTED, "j + q must be <= 30");
+    if (d->j < 1) return fail(CWW_ERR_UNSUPPORTED, "j must be >= 1 (M = 1 is not supported)");
     if (d->q > 10) return fail(CWW_ERR_UNSUPPORTED, "q must be <= 10");
     if (d->dim == 2 && int(d->j) > cww::kSmallMaxLog)
         return fail(CWW_ERR_UNSUPPORTED, "2D operator supports j <= %d", cww::kSmallMaxLog);
@@ -486,7 +552,7 @@ cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
 // 1D layout helpers
 Layout lay_contig(long long len) { return Layout{0, len, 0, 1, 62, 62}; }
 
-// largest power of two V <= cap with V*M <= 2^13
+// largest power of two V <= cap with V*M <= 2^kSmallMaxLog
 int small_V(long long M, long long nvec, int cap = 32) {
     int V = 1;
     while (V * 2 <= cap && (V * 2) * M <= (1ll << cww::kSmallMaxLog) && V * 2 <= nvec) V *= 2;
@@ -533,6 +599,12 @@ cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out
     if (cww::small_smem_query(op->nu, V, int(op->j), int(op->q), adj, vf) > 227 * 1024)
         return fail(CWW_ERR_UNSUPPORTED, "shared-memory footprint too large for nu=%d j=%u q=%u", op->nu, op->j, op->q);
     auto a = small_args(op, in, lin, out, lout, nvec, V);
+    // block-contiguous inputs allow a plain 16-byte copy (forward kernel)
+    const long long M = op->M;
+    if (lin.contig() && (V == 1 || (lin.vsh >= 62 && lin.vs == M))) a.in_block = 1;
+    else if (lin.vs == 1 && lin.esh >= 62 && lin.es == V && lin.vsh < 62 && (1ll << lin.vsh) == V &&
+             lin.vb == M * V)
+        a.in_block = 2;
     Prof pr(adj ? "small_adj" : "small_fwd", st);
     CUDA_TRY(cww::launch_small(op->nu, a, adj, st));
     return CWW_OK;
@@ -559,7 +631,7 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     const int nu = op->nu, NP = 2 * nu - 1, CW = 32 + 2 * (nu - 1);
     const long long A = M >> cww::kLogB;
     const auto pl = large_plan(op->j);
-    const int Lc = std::min<int>(int(op->j) - 1, cww::kSmallMaxLog);
+    const int Lc = std::min<int>(int(op->j) - 1, cww::kSmallMaxLog);  // coarse levels in one CTA
     const bool idwt = op->d.use_idwt && op->r0 < int(op->j);
     const long long nslot = cww::large_nslot(int(op->q), int(op->j), pl.kl, pl.ng);
     DevBuf w0, w1, G, ev, epw;
@@ -922,7 +994,7 @@ cww_status cww_dwt(const cww_op* op, double* data, size_t len, size_t batch, int
     const bool inverse = dir == CWW_DWT_INVERSE;
     long long nvec = (long long)batch * (op->dim == 2 ? M : 1);
     auto pass = [&](Layout l, long long nv) -> cww_status {
-        if (M <= (1ll << cww::kSmallMaxLog)) {
+        if (M <= (1ll << cww::kSmallMaxLog)) {  // k_wav_coarse: 3 * 2^j doubles of smem
             cww::WavArgs w{};
             w.kind = 0;
             w.tab = op->d_tab;

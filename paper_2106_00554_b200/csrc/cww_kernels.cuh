@@ -1,22 +1,21 @@
 #pragma once
 // sm_100a kernel templates of the Walsh->wavelet change-of-basis operator.
 //
-//   small path  (M <= kSmallMax): one CTA per group of V vectors runs the whole
-//               composed map in shared memory:
-//                 forward  k_small_fwd : IDWT (all levels) -> H_A -> stencil+edges
-//                                        -> H_B -> sequency-ordered store
-//                 adjoint  k_small_adj : sequency-ordered load -> H_B -> correlation
-//                                        stencil (+edge sums) -> H_A -> overlap-add
-//                                        -> DWT (all levels) -> store
-//   large path  (M > kSmallMax): wavelet levels as separate passes, then a
-//               two-pass Hadamard with an L2-resident intermediate G of
-//               A x (B+2h) doubles:
-//                 forward  k_large_fwd1 (contiguous chunks: halo/mask + H over the
-//                          low K bits)  ->  k_large_fwd2 (strided: H over the high
-//                          K bits + stencil + H_B + sequency store)
-//                 adjoint  k_large_adj2 (strided: load + H_B + correlation + H over
-//                          the high N bits)  ->  k_large_adj1 (contiguous: H over
-//                          the low bits + overlap-add + edges)
+//   small path  (M <= 2^kSmallMaxLog): one CTA per group of V vectors (V*M <= 4096)
+//               runs the whole composed map in shared memory:
+//                 k_small_fwd : IDWT levels (ping-pong) -> extended tile -> H_A
+//                               -> stencil + edges -> H_B -> sequency-ordered store
+//                 k_small_adj : sequency-ordered load -> H_B -> correlation stencil
+//                               (+ edge sums) -> H_A -> overlap-add -> DWT levels
+//                               (details stored as produced)
+//   large path  (M > 2^kSmallMaxLog): wavelet levels as separate passes, then a
+//               two-pass Hadamard with an L2-resident intermediate G[A][B+2h]:
+//                 k_large_fwd1 (contiguous chunks: halo/mask + H over the low K
+//                 bits) -> k_large_fwd2 (strided: H over the high K bits + row stage)
+//                 k_large_adj2 (strided: row stage + H over the high N bits)
+//                 -> k_large_adj1 (contiguous: H over the low bits + overlap-add + edges)
+//
+// Tiles and G store logical row K at physical row bitrev(K) (see tile_idx).
 //
 // Reference correspondence: fastop.cpp:100-175 (forward_1d / adjoint_1d),
 // fastop.cpp:196-227 (2D driver), wavelet.cpp:367-514 (dwt_apply levels),
@@ -24,198 +23,120 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdio>
 
 #include "cww_device.cuh"
 #include "cww_launch.h"
 
 namespace cww {
 
-constexpr int kKMax = 32;  // register-staged outputs per thread (in-place levels)
+constexpr int kSmallElems = 1 << kSmallMaxLog;  // V*M per CTA
+constexpr int kSmallNT = 256;
+constexpr int kFinalPerThread = kSmallElems / kSmallNT;  // 16 register-staged outputs
+constexpr int kWarpLev = 8;  // wavelet levels of <= 256 samples run warp-private
 
-// ============================================================================
-// small path
-// ============================================================================
+// Optional per-phase cycle stamps (build with -DCWW_PHASE_TIMING): thread 0 of
+// each CTA records clock64() at phase boundaries into cww_phase_buf.
+#ifdef CWW_PHASE_TIMING
+__device__ long long cww_phase_buf[1 << 20];
+#define PHASE(k)                                                                         \
+    do {                                                                                 \
+        if (threadIdx.x == 0 && blockIdx.x < (1 << 20) / 16)                             \
+            cww_phase_buf[blockIdx.x * 16 + (k)] = clock64();                            \
+    } while (0)
+#else
+#define PHASE(k) \
+    do {         \
+    } while (0)
+#endif
 
+// ---------------------------------------------------------------------------
+// row stages (shared by the small and large paths)
+// ---------------------------------------------------------------------------
+
+// Forward row: z = H_B( stencil_s(row) + edges ).  trow: physical tile row
+// (sw unused: odd row stride), kp: &kap[0][s] (stride S), es: edge contributions [2NP] or null.
 template <int NU, int LOGB>
-struct SmallSmem {
+__device__ __forceinline__ void row_fwd(const double* trow, int sw, const double* kp, int S,
+                                        const double* es, double sgR, double* z) {
     using G = Geo<NU, LOGB>;
-    // doubles: filters | EV[V][2nu] | ES/W[V][S][2NP] | EPW[V][slots][S][2NP] | region
-    static __host__ __device__ long long filt() { return FiltSmem<NU>::SIZE; }
-};
-
-// shared-memory footprint (bytes) of one small-path CTA
-template <int NU, int LOGB>
-inline long long small_smem_bytes(int V, int j, int q, bool adj, bool vf) {
-    using G = Geo<NU, LOGB>;
-    const int a = j - LOGB, A = 1 << a, S = 1 << q;
-    long long d = FiltSmem<NU>::SIZE + (long long)V * 2 * NU + (long long)V * S * 2 * G::NP;
-    if (adj) {  // edge partial-sum slots, as computed in k_small_adj
-        int L = vf ? ((32 / V) < A ? (32 / V) : A) : (A < 32 ? A : 32);
-        int nslot = A / L > 0 ? A / L : 1;
-        d += (long long)V * (nslot + 1) * S * 2 * G::NP;
+    constexpr int B = G::B, H = G::H, CW = G::CW, NP = G::NP;
+    double kap[2 * H + 1];
+#pragma unroll
+    for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(kp + l * S);
+#pragma unroll
+    for (int k = 0; k < B; ++k) z[k] = 0.0;
+#pragma unroll
+    for (int e = 0; e < CW; ++e) {  // z[k] = sum_l kap[l] row[k - l + h], streamed over e
+        const double r = trow[e];
+#pragma unroll
+        for (int l = -H; l <= H; ++l) {
+            const int k = e + l - H;
+            if (k >= 0 && k < B) z[k] += kap[l + H] * r;
+        }
     }
-    long long region = (long long)V * A * G::RS;
-    long long xs = (long long)V << j;
-    d += region > xs ? region : xs;
-    return d * 8;
+    if (NU > 1 && es) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) z[i] += es[i];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) z[B - NP + i] += sgR * es[NP + i];
+    }
+    hadamard_reg<LOGB>(z);
 }
 
-// Load the staged filters (h | g | edge matrices are contiguous in the table).
-template <int NU>
-__device__ __forceinline__ void stage_filters(double* filt, const SmallArgs& p, int tid, int nt) {
-    for (int i = tid; i < FiltSmem<NU>::SIZE; i += nt) filt[i] = p.tab[p.t.o_h + i];
+// Adjoint row: tile row (+)= correlation_s(y), y already H_B-transformed.
+template <int NU, int LOGB>
+__device__ __forceinline__ void row_adj_accum(double* trow, int sw, const double* kp, int S,
+                                              const double* y, bool first) {
+    using G = Geo<NU, LOGB>;
+    constexpr int B = G::B, H = G::H, CW = G::CW;
+    double kap[2 * H + 1];
+#pragma unroll
+    for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(kp + l * S);
+#pragma unroll
+    for (int e = 0; e < CW; ++e) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = -H; l <= H; ++l) {
+            const int k = e - H + l;
+            if (k >= 0 && k < B) acc += kap[l + H] * y[k];
+        }
+        trow[e] = first ? acc : trow[e] + acc;
+    }
 }
 
-template <int NU, int LOGB, int NT>
-__global__ void __launch_bounds__(NT) k_small_fwd(SmallArgs p) {
-    using G = Geo<NU, LOGB>;
-    constexpr int B = G::B, H = G::H, CW = G::CW, RS = G::RS, NP = G::NP;
-    extern __shared__ double sm[];
-    const int tid = threadIdx.x;
-    const int j = p.j, M = 1 << j, a = j - LOGB, A = 1 << a, S = 1 << p.q;
-    const int V = p.V;
-    const long long v0 = (long long)blockIdx.x * V;
-    const int nv = (int)((p.nvec - v0) < V ? (p.nvec - v0) : V);
-    double* filt = sm;
-    double* EV = filt + FiltSmem<NU>::SIZE;
-    double* ES = EV + V * 2 * NU;
-    double* X = ES + V * S * 2 * NP;
-    double* T = X;  // the tile overlaps X (all X reads finish before the tile is written)
-    const long long tst = (long long)A * RS;
+// Store / load one row's B sequency-ordered values: element index
+// s*M + (gray^-1(bitrev_b(nl) << a) ^ rw), specialised by layout kind.
+template <int LOGB>
+__device__ __forceinline__ void row_store(double* ob, const Layout& L, int a, unsigned rw, const double* z) {
+    if (L.contig()) {
+#pragma unroll
+        for (int nl = 0; nl < (1 << LOGB); ++nl) ob[gray_inv_hi(nl, LOGB, a) ^ rw] = z[nl];
+    } else if (L.esh >= 62) {
+        const long long es = L.es;
+#pragma unroll
+        for (int nl = 0; nl < (1 << LOGB); ++nl) ob[(long long)(gray_inv_hi(nl, LOGB, a) ^ rw) * es] = z[nl];
+    } else {
+#pragma unroll
+        for (int nl = 0; nl < (1 << LOGB); ++nl) ob[L.eoff(gray_inv_hi(nl, LOGB, a) ^ rw)] = z[nl];
+    }
+}
 
-    stage_filters<NU>(filt, p, tid, NT);
-    const long long tot = (long long)nv * M;
-    const bool vf = p.lin.vfast();
-    for (long long f = tid; f < tot; f += NT) {
-        int v = vf ? (int)(f % nv) : (int)(f >> j);
-        int i = vf ? (int)(f / nv) : (int)(f & (M - 1));
-        X[(long long)v * M + i] = p.in[p.lin.at(v0 + v, i)];
-    }
-    __syncthreads();
-    FiltSmem<NU> F{filt};
-
-    // IDWT levels r0+1 .. j-1 in place (register staged), wavelet.cpp:505-513
-    const int lev0 = p.use_idwt ? p.r0 + 1 : j + 1;
-    for (int lev = lev0; lev < j; ++lev) {
-        const int n = 1 << lev;
-        const int total = nv << lev;
-        double r[kKMax];
+template <int LOGB>
+__device__ __forceinline__ void row_load(const double* ib, const Layout& L, int a, unsigned rw, bool act,
+                                         double* y) {
+    if (!act) {
 #pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * NT;
-            if (o < total) r[k] = idwt_sample<NU>(F, X + (long long)(o >> lev) * M, n, o & (n - 1), p.vmp);
-        }
-        __syncthreads();
+        for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = 0.0;
+    } else if (L.contig()) {
 #pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * NT;
-            if (o < total) X[(long long)(o >> lev) * M + (o & (n - 1))] = r[k];
-        }
-        __syncthreads();
-    }
-    // final level (or plain copy) -> registers -> extended tile
-    {
-        double r[kKMax];
-        const int total = nv << j;
+        for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = __ldg(ib + (gray_inv_hi(nl, LOGB, a) ^ rw));
+    } else if (L.esh >= 62) {
+        const long long es = L.es;
 #pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * NT;
-            if (o < total) {
-                const double* xv = X + (long long)(o >> j) * M;
-                int i = o & (M - 1);
-                r[k] = (lev0 <= j) ? idwt_sample<NU>(F, xv, M, i, p.vmp) : xv[i];
-            }
-        }
-        __syncthreads();
-        // halo cells without a source: row 0 left halo, row A-1 right halo
-        for (int f = tid; f < nv * 2 * H; f += NT) {
-            int v = f / (2 * H), c = f % (2 * H);
-            double* t = T + v * tst;
-            if (c < H) t[tile_idx(0, c, RS, 0)] = 0.0;
-            else t[tile_idx(A - 1, B + c, RS, brev_bits(A - 1, a))] = 0.0;
-        }
+        for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = __ldg(ib + (long long)(gray_inv_hi(nl, LOGB, a) ^ rw) * es);
+    } else {
 #pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * NT;
-            if (o < total) {
-                int v = o >> j, i = o & (M - 1);
-                double val = r[k];
-                if (NU > 1 && (i < NU || i >= M - NU)) {  // interior mask; edge columns kept aside
-                    EV[v * 2 * NU + (i < NU ? i : NU + i - (M - NU))] = val;
-                    val = 0.0;
-                }
-                double* t = T + v * tst;
-                int K = i >> LOGB, kl = i & (B - 1);
-                t[tile_idx(K, kl + H, RS, brev_bits(K, a))] = val;
-                if (kl < H && K > 0) t[tile_idx(K - 1, B + H + kl, RS, brev_bits(K - 1, a))] = val;
-                if (kl >= B - H && K < A - 1) t[tile_idx(K + 1, kl - (B - H), RS, brev_bits(K + 1, a))] = val;
-            }
-        }
-    }
-    __syncthreads();
-    // edge contributions es[v][s][pos] = sum_c em[s][pos][c] xi_edge[c]
-    if (NU > 1) {
-        for (int f = tid; f < nv * S * 2 * NP; f += NT) {
-            int v = f / (S * 2 * NP), sp = f % (S * 2 * NP);
-            const double* em = p.tab + p.t.o_em + (long long)sp * 2 * NU;
-            double acc = 0.0;
-#pragma unroll
-            for (int c = 0; c < 2 * NU; ++c) acc += em[c] * EV[v * 2 * NU + c];
-            ES[f] = acc;
-        }
-    }
-    tile_hadamard(T, nv, a, 0, a, CW, RS, tst, tid, NT);
-    __syncthreads();
-
-    // row stage: stencil + edges + H_B + sequency-ordered store
-    const bool of = p.lout.vfast();
-    const int items = nv * A * S;
-    for (int w = tid; w < items; w += NT) {
-        int v, wlo, s;
-        if (of) {
-            v = w % nv;
-            int rest = w / nv;
-            wlo = rest % A;
-            s = rest / A;
-        } else {
-            wlo = w % A;
-            int rest = w / A;
-            s = rest % S;
-            v = rest / S;
-        }
-        const int N = (int)brev_bits(wlo, a);
-        const double* t = T + v * tst;
-        double row[CW];
-#pragma unroll
-        for (int e = 0; e < CW; ++e) row[e] = t[tile_idx(N, e, RS, wlo)];
-        double kap[2 * H + 1];
-#pragma unroll
-        for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(p.tab + p.t.o_kap + l * S + s);
-        double z[B];
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            double acc = 0.0;
-#pragma unroll
-            for (int l = -H; l <= H; ++l) acc += kap[l + H] * row[k - l + H];
-            z[k] = acc;
-        }
-        if (NU > 1) {
-            const double* es = ES + (v * S + s) * 2 * NP;
-            const double sg = (a > 0 && (__popc(N) & 1)) ? -1.0 : 1.0;
-#pragma unroll
-            for (int i = 0; i < NP; ++i) z[i] += es[i];
-#pragma unroll
-            for (int i = 0; i < NP; ++i) z[B - NP + i] += sg * es[NP + i];
-        }
-        hadamard_reg<LOGB>(z);
-#pragma unroll
-        for (int nl = 0; nl < B; ++nl) {
-            unsigned g = (brev_bits(nl, LOGB) << a) | (unsigned)wlo;
-            int r = (int)gray_inv(g);
-            if (s & 1) r = M - 1 - r;
-            p.out[p.lout.at(v0 + v, (long long)s * M + r)] = z[nl];
-        }
+        for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = __ldg(ib + L.eoff(gray_inv_hi(nl, LOGB, a) ^ rw));
     }
 }
 
@@ -225,293 +146,507 @@ __device__ __forceinline__ double seg_allreduce(double x, int lo_off, int hi_off
     return x;
 }
 
+// ---------------------------------------------------------------------------
+// wavelet level bodies (cooperative over `nthr` threads starting at `t0`)
+// ---------------------------------------------------------------------------
+
+// Synthesis of level n for one vector: fine[0:n] from cs[0:n/2], ds[0:n/2].
+// Interior pairs share a window; the 2(3nu-1) edge samples are separate
+// (dense edge blocks), so the interior loop is branch-free.
+template <int NU>
+__device__ __forceinline__ void idwt_level_vec(const FiltSmem<NU>& F, const double* cs, const double* ds,
+                                               double* dst, int n, bool vmp, int t0, int nthr) {
+    const int half = n >> 1;
+    if (vmp && n < 8 * NU) {  // coarsest levels: generic edge code
+        for (int i = t0; i < n; i += nthr) dst[i] = idwt_sample_full2<NU>(F, cs, ds, n, i, true);
+        return;
+    }
+    constexpr int EL = FiltSmem<NU>::EL;
+    const int mlo = vmp ? (EL + 1) >> 1 : 0;
+    const int mhi = vmp ? (n - EL) >> 1 : half;
+    const Taps<NU> tp(F);
+    for (int m = mlo + t0; m < mhi; m += nthr) {
+        double o0, o1;
+        idwt_pair_inner<NU>(tp, cs, ds, n, m, vmp, o0, o1);
+        dst[2 * m] = o0;
+        dst[2 * m + 1] = o1;
+    }
+    if (vmp) {
+        const int nl = 2 * mlo, nr = n - 2 * mhi;  // edge samples [0, nl) and [2 mhi, n)
+        for (int k = nthr - 1 - t0; k < nl + nr; k += nthr) {  // last threads: fewest pairs
+            const int i = k < nl ? k : 2 * mhi + (k - nl);
+            dst[i] = idwt_one<NU>(F, cs, ds, n, i, true);
+        }
+    }
+}
+
+// Barrier over the G threads of group gid (NT threads per CTA): the whole
+// CTA, one warp (or less: __syncwarp is a superset), or a named barrier.
+template <int NT>
+__device__ __forceinline__ void group_sync(int gid, int G, int ngroups) {
+    if (G >= NT) {
+        __syncthreads();
+    } else if (G <= 32) {  // the warp's active groups (a group never spans warps)
+        const int g0 = (int)(threadIdx.x & ~31u) / G;
+        const int nact = min(32 / G, ngroups - g0);
+        const unsigned mask = nact >= 32 / G ? 0xffffffffu : ((1u << (nact * G)) - 1u);
+        __syncwarp(mask);
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(gid + 1), "r"(G) : "memory");
+    }
+}
+
+// Synthesis levels r0+1 .. j-1 of one vector by a thread group; returns the
+// coarse input of the final level j (cbuf, or xv when there is no earlier
+// level).  Level t (lev = r0+1+t) reads c from xv (t = 0) or the previous
+// buffer and d = xv[2^(lev-1) : 2^lev]; it writes p0/p1 alternately, and the
+// last one (level j-1) writes cbuf.
+template <int NU, int NT>
+__device__ __forceinline__ const double* idwt_group(const FiltSmem<NU>& F, const double* xv, double* p0,
+                                                    double* p1, double* cbuf, int j, int r0, bool vmp,
+                                                    int gt, int G, int gid, int ngroups) {
+    const double* src = xv;
+    for (int lev = r0 + 1; lev < j; ++lev) {
+        const int t = lev - r0 - 1, n = 1 << lev;
+        double* dst = (lev == j - 1) ? cbuf : ((t & 1) ? p1 : p0);
+        idwt_level_vec<NU>(F, src, xv + (n >> 1), dst, n, vmp, gt, G);
+        group_sync<NT>(gid, G, ngroups);
+        src = dst;
+    }
+    return src;
+}
+
+// ---------------------------------------------------------------------------
+// small path
+// ---------------------------------------------------------------------------
+
+// edge partial-sum slots of k_small_adj (lanes sharing a vector per warp)
+__host__ __device__ inline int small_adj_lanes(int A, int V, bool vf) {
+    return vf ? ((32 / V) < A ? (32 / V) : A) : (A < 32 ? A : 32);
+}
+
+// per-vector tile stride: >= A*RS and == 16/V (mod 16), so lanes that walk
+// (vector, row) pairs hit distinct banks
+__host__ __device__ inline int small_tile_stride(int ars, int V) {
+    const int t = V >= 16 ? 1 : 16 / V;
+    return ((ars + 15) / 16) * 16 + (t & 15);
+}
+
+template <int NU, int LOGB>
+inline long long small_smem_bytes(int V, int j, int q, bool adj, bool vf) {
+    using G = Geo<NU, LOGB>;
+    const int a = j - LOGB, A = 1 << a, S = 1 << q;
+    long long d = FiltSmem<NU>::SIZE + (long long)V * 2 * NU + (long long)V * S * 2 * G::NP;
+    if (adj) {
+        const int L = small_adj_lanes(A, V, vf);
+        const int nslot = A / L > 0 ? A / L : 1;
+        d += (long long)V * nslot * S * 2 * G::NP;
+    }
+    d += (long long)V << j;          // X
+    d += (long long)V << (j > 0 ? j - 1 : 0);  // C (final-level coarse input / DWT ping)
+    d += (long long)V * small_tile_stride(A * G::RS, V);  // tiles (also wavelet ping-pong / output staging)
+    return d * 8;
+}
+
+template <int NU>
+__device__ __forceinline__ void stage_filters(double* filt, const double* tab, const Tables& t,
+                                              int tid, int nt) {
+    for (int i = tid; i < FiltSmem<NU>::SIZE; i += nt) filt[i] = tab[t.o_h + i];
+}
+
+__device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
+
 template <int NU, int LOGB, int NT>
-__global__ void __launch_bounds__(NT) k_small_adj(SmallArgs p) {
+__global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
+    using G = Geo<NU, LOGB>;
+    constexpr int B = G::B, H = G::H, CW = G::CW, RS = G::RS, NP = G::NP;
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x;
+    const int j = p.j, M = 1 << j, a = j - LOGB, A = 1 << a, S = 1 << p.q;
+    const int V = p.V, lV = ilog2(V);
+    const long long v0 = (long long)blockIdx.x * V;
+    const int nv = (int)((p.nvec - v0) < V ? (p.nvec - v0) : V);
+    double* filt = sm;
+    double* EV = filt + FiltSmem<NU>::SIZE;
+    double* ES = EV + V * 2 * NU;
+    double* X = ES + V * S * 2 * NP;
+    double* C = X + V * M;
+    double* T = C + (V * M >> 1);
+    const int tst = small_tile_stride(A * RS, V);
+    const int hM = M >> 1;
+    // thread groups: G threads per vector (V divides NT)
+    const int Gs = NT / V, gid = tid / Gs, gt = tid % Gs;
+
+    PHASE(0);
+    stage_filters<NU>(filt, p.tab, p.t, tid, NT);
+    if (p.in_block == 1 && M >= 2) {  // V vectors back to back: 16-byte copy
+        const double2* blk = reinterpret_cast<const double2*>(p.in + p.lin.vbase(v0));
+        const int tot2 = (nv * M) >> 1;
+        for (int f = tid; f < tot2; f += NT) {
+            const double2 val = __ldg(blk + f);
+            X[2 * f] = val.x;
+            X[2 * f + 1] = val.y;
+        }
+    } else if (p.in_block == 2 && V >= 2) {  // [M][V] interleaved block (column panel)
+        const double2* blk = reinterpret_cast<const double2*>(p.in + p.lin.vbase(v0));
+        const int tot2 = (V * M) >> 1;
+        for (int f = tid; f < tot2; f += NT) {
+            const int v = (2 * f) & (V - 1), i = (2 * f) >> lV;
+            if (v < nv) {
+                const double2 val = __ldg(blk + f);
+                X[v * M + i] = val.x;
+                X[(v + 1) * M + i] = val.y;
+            }
+        }
+    } else {
+        const bool vf = p.lin.vfast();
+        for (int f = tid; f < V * M; f += NT) {
+            const int v = vf ? f & (V - 1) : f >> j;
+            const int i = vf ? f >> lV : f & (M - 1);
+            if (v < nv) X[v * M + i] = __ldg(p.in + p.lin.vbase(v0 + v) + p.lin.eoff(i));
+        }
+    }
+    __syncthreads();
+    PHASE(1);
+    const FiltSmem<NU> F{filt};
+    const bool idwt = p.use_idwt && p.r0 < j;
+
+    // per-vector group: IDWT levels r0+1 .. j (wavelet.cpp:505-513); the final
+    // level writes the extended tile directly (interior mask, edge values -> EV)
+    if (gid < nv) {
+        const int v = gid;
+        const double* xv = X + v * M;
+        double* tv = T + v * tst;
+        const double* cfin = xv;
+        if (idwt) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, p.vmp, gt, Gs, gid, nv);
+        PHASE(2);
+        auto put = [&](int i, double val) {
+            if (NU > 1 && (i < NU || i >= M - NU)) {
+                EV[v * 2 * NU + (i < NU ? i : NU + i - (M - NU))] = val;
+                val = 0.0;
+            }
+            const int ph = (int)brev_bits((unsigned)(i >> LOGB), a);
+            tv[ph * RS + (i & (B - 1)) + H] = val;
+        };
+        if (!idwt) {
+            for (int i = gt; i < M; i += Gs) put(i, xv[i]);
+        } else if (p.vmp && M < 8 * NU) {
+            for (int i = gt; i < M; i += Gs) put(i, idwt_sample_full2<NU>(F, cfin, xv + hM, M, i, true));
+        } else {
+            constexpr int EL = FiltSmem<NU>::EL;
+            const int mlo = p.vmp ? (EL + 1) >> 1 : 0;
+            const int mhi = p.vmp ? (M - EL) >> 1 : hM;
+            const Taps<NU> tp(F);
+            for (int m = mlo + gt; m < mhi; m += Gs) {
+                double o0, o1;
+                idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, p.vmp, o0, o1);
+                put(2 * m, o0);
+                put(2 * m + 1, o1);
+            }
+            if (p.vmp) {
+                const int nl = 2 * mlo, nr = M - 2 * mhi;
+                for (int k2 = Gs - 1 - gt; k2 < nl + nr; k2 += Gs) {
+                    const int i = k2 < nl ? k2 : 2 * mhi + (k2 - nl);
+                    put(i, idwt_one<NU>(F, cfin, xv + hM, M, i, true));
+                }
+            }
+        }
+        group_sync<NT>(gid, Gs, nv);
+        PHASE(3);
+        // halo columns of this vector's tile: copies of the neighbouring rows
+        if (H > 0) {
+            for (int f = gt; f < A * 2 * H; f += Gs) {
+                const int c = f % (2 * H), K = f / (2 * H);
+                const int ph = (int)brev_bits((unsigned)K, a);
+                double val = 0.0;
+                if (c < H) {  // left halo e = c <- row K-1, column (B - H + c) + H
+                    if (K > 0) val = tv[(int)brev_bits((unsigned)(K - 1), a) * RS + B + c];
+                    tv[ph * RS + c] = val;
+                } else {      // right halo e = B + c <- row K+1, column (c - H) + H
+                    if (K < A - 1) val = tv[(int)brev_bits((unsigned)(K + 1), a) * RS + c];
+                    tv[ph * RS + B + c] = val;
+                }
+            }
+        }
+        if (NU > 1) {  // es[v][s][pos] = sum_c em[s][pos][c] xi_edge[c]
+            for (int f = gt; f < S * 2 * NP; f += Gs) {
+                const double* em = p.tab + p.t.o_em + f * 2 * NU;
+                double acc = 0.0;
+#pragma unroll
+                for (int c = 0; c < 2 * NU; ++c) acc += __ldg(em + c) * EV[v * 2 * NU + c];
+                ES[v * S * 2 * NP + f] = acc;
+            }
+        }
+    }
+    __syncthreads();
+    PHASE(4);
+    PHASE(5);
+    tile_hadamard<CW, RS>(T, nv, a, 0, a, tst, tid, NT);
+    PHASE(6);
+
+    // row stage: stencil + edges + H_B + sequency-ordered store
+    const bool of = p.lout.vfast();
+    const int items = V * A * S;
+    for (int w = tid; w < items; w += NT) {
+        int v, wlo, s;
+        if (of) {  // lanes vary the vector first (V is a power of two)
+            v = w & (V - 1);
+            const int rest = w >> lV;
+            wlo = rest & (A - 1);
+            s = rest >> a;
+        } else {
+            wlo = w & (A - 1);
+            const int rest = w >> a;
+            s = rest & (S - 1);
+            v = rest >> p.q;
+        }
+        if (v >= nv) continue;
+        const double sg = (__popc(wlo) & 1) ? -1.0 : 1.0;  // popc(N) = popc(bitrev(N))
+        double z[B];
+        row_fwd<NU, LOGB>(T + v * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S,
+                          NU > 1 ? ES + (v * S + s) * 2 * NP : nullptr, sg, z);
+        const unsigned rw = gray_inv((unsigned)wlo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
+        row_store<LOGB>(p.out + p.lout.vbase(v0 + v) + p.lout.eoff((long long)s * M), p.lout, a, rw, z);
+    }
+    PHASE(7);
+}
+
+template <int NU, int LOGB, int NT>
+__global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
     using G = Geo<NU, LOGB>;
     constexpr int B = G::B, H = G::H, CW = G::CW, RS = G::RS, NP = G::NP;
     extern __shared__ double sm[];
     const int tid = threadIdx.x, lane = tid & 31;
     const int j = p.j, M = 1 << j, a = j - LOGB, A = 1 << a, S = 1 << p.q;
-    const int V = p.V;
+    const int V = p.V, lV = ilog2(V);
     const long long v0 = (long long)blockIdx.x * V;
     const int nv = (int)((p.nvec - v0) < V ? (p.nvec - v0) : V);
     const bool vf = p.lin.vfast();
-    // lanes of a warp that share one vector: a contiguous (non-vfast) or
-    // strided (vfast) subset; L of them per warp, EPW slots per vector A/L
-    const int L = vf ? ((32 / V) < A ? (32 / V) : A) : (A < 32 ? A : 32);
+    const int L = small_adj_lanes(A, V, vf);
     const int nslot = A / L > 0 ? A / L : 1;
     double* filt = sm;
-    double* EV = filt + FiltSmem<NU>::SIZE;  // unused (edge values), kept for layout symmetry
+    double* EV = filt + FiltSmem<NU>::SIZE;  // unused here; keeps the layout of k_small_fwd
     double* W = EV + V * 2 * NU;              // [V][S][2NP]
-    double* EPW = W + V * S * 2 * NP;         // [V][nslot+1][S][2NP]
-    double* X = EPW + (long long)V * (nslot + 1) * S * 2 * NP;
-    double* T = X;
-    const long long tst = (long long)A * RS;
-    stage_filters<NU>(filt, p, tid, NT);
+    double* EPW = W + V * S * 2 * NP;         // [V][nslot][S][2NP]
+    double* X = EPW + V * nslot * S * 2 * NP;
+    double* C = X + V * M;
+    double* T = C + (V * M >> 1);
+    const int tst = small_tile_stride(A * RS, V);
+    const int hM = M >> 1;
+    const int Gs = NT / V, gid = tid / Gs, gt = tid % Gs;
+    stage_filters<NU>(filt, p.tab, p.t, tid, NT);
 
-    // row stage: sequency-ordered load + H_B + correlation stencil (+ edge partials)
-    const int items = V * A;  // padded to V so that lane->vector is a fixed pattern
+    // row stage: sequency-ordered load + H_B + correlation (+ edge partials)
+    const int items = V * A;  // padded to V: the lane -> vector pattern is fixed
     const int iters = (items + NT - 1) / NT;
     for (int it = 0; it < iters; ++it) {
-        int w = tid + it * NT;
+        const int w = tid + it * NT;
         int v, wlo;
         if (vf) {
-            v = w % V;
-            wlo = (w / V) % A;
+            v = w & (V - 1);
+            wlo = (w >> lV) & (A - 1);
         } else {
-            wlo = w % A;
-            v = w / A;
+            wlo = w & (A - 1);
+            v = w >> a;
         }
         const bool act = (w < items) && (v < nv);
-        const int N = (int)brev_bits(wlo, a);
-        const double sg = (a > 0 && (__popc(N) & 1)) ? -1.0 : 1.0;
-        double acc[CW];
-#pragma unroll
-        for (int e = 0; e < CW; ++e) acc[e] = 0.0;
+        const double sg = (__popc(wlo) & 1) ? -1.0 : 1.0;
+        const double* ib0 = p.in + p.lin.vbase(v0 + (act ? v : 0));
         for (int s = 0; s < S; ++s) {
             double y[B];
-#pragma unroll
-            for (int nl = 0; nl < B; ++nl) {
-                unsigned g = (brev_bits(nl, LOGB) << a) | (unsigned)wlo;
-                int r = (int)gray_inv(g);
-                if (s & 1) r = M - 1 - r;
-                y[nl] = act ? p.in[p.lin.at(v0 + v, (long long)s * M + r)] : 0.0;
-            }
+            const unsigned rw = gray_inv((unsigned)wlo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
+            row_load<LOGB>(ib0 + p.lin.eoff((long long)s * M), p.lin, a, rw, act, y);
             hadamard_reg<LOGB>(y);
-            double kap[2 * H + 1];
-#pragma unroll
-            for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(p.tab + p.t.o_kap + l * S + s);
-#pragma unroll
-            for (int e = 0; e < CW; ++e) {
-#pragma unroll
-                for (int l = -H; l <= H; ++l) {
-                    const int k = e - H + l;
-                    if (k >= 0 && k < B) acc[e] += kap[l + H] * y[k];
-                }
-            }
             if (NU > 1) {  // transform-domain values at the 4nu-2 edge positions
                 const int lo_off = vf ? V : 1;
                 const int hi_off = vf ? 32 : L;
                 const bool leader = vf ? (lane < V) : ((lane & (L - 1)) == 0);
-                const int slot = (it * NT + (tid & ~31)) / (vf ? V : 1) / L % nslot;
+                const int slot = ((it * NT + (tid & ~31)) / (vf ? V : 1) / L) % nslot;
 #pragma unroll
                 for (int i = 0; i < 2 * NP; ++i) {
                     double val = i < NP ? y[i] : sg * y[B - NP + (i - NP)];
                     val = seg_allreduce(val, lo_off, hi_off);
-                    if (leader && act) EPW[(((long long)v * (nslot + 1) + slot) * S + s) * 2 * NP + i] = val;
+                    if (leader && act) EPW[((v * nslot + slot) * S + s) * 2 * NP + i] = val;
                 }
             }
-        }
-        if (act) {
-            double* t = T + v * tst;
-#pragma unroll
-            for (int e = 0; e < CW; ++e) t[tile_idx(N, e, RS, wlo)] = acc[e];
+            if (act) row_adj_accum<NU, LOGB>(T + v * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S, y, s == 0);
         }
     }
     __syncthreads();
-    tile_hadamard(T, nv, a, 0, a, CW, RS, tst, tid, NT);
-    __syncthreads();
+    tile_hadamard<CW, RS>(T, nv, a, 0, a, tst, tid, NT);
     if (NU > 1) {  // W[v][s][pos] = sum over rows (fixed order)
         for (int f = tid; f < nv * S * 2 * NP; f += NT) {
-            int v = f / (S * 2 * NP), sp = f % (S * 2 * NP);
+            const int v = f / (S * 2 * NP), sp = f % (S * 2 * NP);
             double acc = 0.0;
-            for (int sl = 0; sl < nslot; ++sl) acc += EPW[((long long)v * (nslot + 1) + sl) * S * 2 * NP + sp];
+            for (int sl = 0; sl < nslot; ++sl) acc += EPW[(v * nslot + sl) * S * 2 * NP + sp];
             W[f] = acc;
         }
         __syncthreads();
     }
-    // overlap-add + interior mask + edge columns -> registers -> X
-    {
-        double r[kKMax];
-        const int total = nv << j;
-#pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * NT;
-            if (o < total) {
-                int v = o >> j, i = o & (M - 1);
-                const double* t = T + v * tst;
-                int K = i >> LOGB, kl = i & (B - 1);
-                double val = t[tile_idx(K, kl + H, RS, brev_bits(K, a))];
-                if (kl < H && K > 0) val += t[tile_idx(K - 1, B + H + kl, RS, brev_bits(K - 1, a))];
-                if (kl >= B - H && K < A - 1) val += t[tile_idx(K + 1, kl - (B - H), RS, brev_bits(K + 1, a))];
-                if (NU > 1 && (i < NU || i >= M - NU)) {
-                    int c = i < NU ? i : NU + i - (M - NU);
-                    const double* wv = W + v * S * 2 * NP;
-                    double e = 0.0;
-                    for (int sp = 0; sp < S * 2 * NP; ++sp) e += p.tab[p.t.o_em + (long long)sp * 2 * NU + c] * wv[sp];
-                    val = e;
-                }
-                r[k] = val;
-            }
+    // overlap-add + interior mask + edge columns -> X
+    for (int o = tid; o < nv * M; o += NT) {
+        const int v = o >> j, i = o & (M - 1);
+        const double* t = T + v * tst;
+        const int K = i >> LOGB, kl = i & (B - 1);
+        const int ph = (int)brev_bits((unsigned)K, a);
+        double val = t[ph * RS + kl + H];
+        if (kl < H && K > 0) val += t[(int)brev_bits((unsigned)(K - 1), a) * RS + B + H + kl];
+        if (kl >= B - H && K < A - 1) val += t[(int)brev_bits((unsigned)(K + 1), a) * RS + kl - (B - H)];
+        if (NU > 1 && (i < NU || i >= M - NU)) {
+            const int c = i < NU ? i : NU + i - (M - NU);
+            const double* wv = W + v * S * 2 * NP;
+            double e = 0.0;
+            for (int sp = 0; sp < S * 2 * NP; ++sp) e += __ldg(p.tab + p.t.o_em + sp * 2 * NU + c) * wv[sp];
+            val = e;
         }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * NT;
-            if (o < total) X[(long long)(o >> j) * M + (o & (M - 1))] = r[k];
-        }
-        __syncthreads();
+        X[o] = val;
     }
-    // DWT levels j .. r0+1 in place (wavelet.cpp:497-504)
-    FiltSmem<NU> F{filt};
-    if (p.use_idwt) {
-        for (int lev = j; lev > p.r0; --lev) {
-            const int n = 1 << lev;
-            const int total = nv << lev;
-            double r[kKMax];
-#pragma unroll
-            for (int k = 0; k < kKMax; ++k) {
-                int o = tid + k * NT;
-                if (o < total) r[k] = dwt_sample<NU>(F, X + (long long)(o >> lev) * M, n, o & (n - 1), p.vmp);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < kKMax; ++k) {
-                int o = tid + k * NT;
-                if (o < total) X[(long long)(o >> lev) * M + (o & (n - 1))] = r[k];
-            }
-            __syncthreads();
-        }
-    }
-    const long long tot = (long long)nv * M;
+    __syncthreads();
+    // DWT levels j .. r0+1 (wavelet.cpp:497-504) per vector group; the output
+    // vector is staged in the (now free) tile area and stored block-wide.
+    const FiltSmem<NU> F{filt};
     const bool of = p.lout.vfast();
-    for (long long f = tid; f < tot; f += NT) {
-        int v = of ? (int)(f % nv) : (int)(f >> j);
-        int i = of ? (int)(f / nv) : (int)(f & (M - 1));
-        p.out[p.lout.at(v0 + v, i)] = X[(long long)v * M + i];
+    const bool dwt = p.use_idwt && p.r0 < j;
+    if (dwt && gid < nv) {
+        const int v = gid;
+        double* ov = T + v * tst;  // staged output [c_r0 | d_r0 | ... | d_(j-1)]
+        double* xv = X + v * M;
+        double* cv = C + v * hM;
+        const double* src = xv;
+        for (int lev = j; lev > p.r0; --lev) {
+            const int t = j - lev, n = 1 << lev, half = n >> 1;
+            const bool last = lev == p.r0 + 1;
+            double* dst = last ? ov : ((t & 1) ? xv : cv);  // coarse rows ping-pong C <-> X
+            const double* s2 = src;
+            for (int mm = gt; mm < half; mm += Gs) {
+                double c, d;
+                dwt_pair<NU>(F, s2, n, mm, p.vmp, c, d);
+                ov[half + mm] = d;
+                dst[mm] = c;
+            }
+            group_sync<NT>(gid, Gs, nv);
+            src = dst;
+        }
+    }
+    __syncthreads();
+    const double* res = dwt ? T : X;
+    const int rst = dwt ? tst : M;
+    for (int f = tid; f < V * M; f += NT) {
+        const int v = of ? f & (V - 1) : f >> j;
+        const int i = of ? f >> lV : f & (M - 1);
+        if (v < nv) p.out[p.lout.at(v0 + v, i)] = res[v * rst + i];
     }
 }
 
-// ============================================================================
+// ---------------------------------------------------------------------------
 // wavelet levels in global memory (large path)
-// ============================================================================
+// ---------------------------------------------------------------------------
 
-// One IDWT level: fine[i] for i < n from c = lo[0:n/2] (workspace, stride
-// lo_vs) and d = x-layout elements [n/2, n) of the op input.
+// One IDWT level: fine[0:n] from c = lo[0:n/2] (workspace) and the details
+// d = elements [n/2, n) of the op input.  The large path is 1D with
+// contiguous vectors (host-enforced), so the details are unit-stride.
 template <int NU>
-__global__ void k_idwt_level(const double* tab, Tables t, const double* lo, long long lo_vs,
-                             const double* x, Layout lx, long long xv0, double* out,
-                             long long out_vs, int lev, int nvec, int vmp) {
+__global__ void __launch_bounds__(256) k_idwt_level(const double* tab, Tables t, const double* lo,
+                                                    long long lo_vs, const double* x, Layout lx,
+                                                    long long xv0, double* out, long long out_vs,
+                                                    int lev, int nvec, int vmp) {
     __shared__ double filt[FiltSmem<NU>::SIZE];
     for (int i = threadIdx.x; i < FiltSmem<NU>::SIZE; i += blockDim.x) filt[i] = tab[t.o_h + i];
     __syncthreads();
-    FiltSmem<NU> F{filt};
+    const FiltSmem<NU> F{filt};
     const int n = 1 << lev, half = n >> 1;
-    const long long tot = (long long)nvec << lev;
-    for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < tot;
-         o += (long long)gridDim.x * blockDim.x) {
-        int v = (int)(o >> lev), i = (int)(o & (n - 1));
-        const double* c = lo + v * lo_vs;
-        // gather form with c from the workspace and d read through the layout
-        double acc = 0.0;
-        if (!vmp) {
-#pragma unroll
-            for (int k = 0; k < NU; ++k) {
-                int u = -NU + 1 + 2 * k + ((i + NU + 1) & 1);
-                int tt = (i - u) % n;
-                if (tt < 0) tt += n;
-                int mm = tt >> 1;
-                acc += F.h(u) * c[mm] + F.g(u) * __ldg(x + lx.at(xv0 + v, half + mm));
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < NU; ++k) {
-                int u = -NU + 1 + 2 * k + ((i + NU + 1) & 1);
-                int mm = (i - u) >> 1;
-                if (mm >= NU && mm < half - NU)
-                    acc += F.h(u) * c[mm] + F.g(u) * __ldg(x + lx.at(xv0 + v, half + mm));
-            }
-            constexpr int W = 2 * NU - 1;
-#pragma unroll
-            for (int side = 0; side < 2; ++side) {
-                int ii = side ? n - 1 - i : i;
-                if (ii < 3 * NU - 1) {
-#pragma unroll
-                    for (int m = 0; m < NU; ++m) {
-                        int row = side ? half - 1 - m : m;
-                        double cm = c[row], dm = __ldg(x + lx.at(xv0 + v, half + row));
-                        if (ii < NU) acc += F.A(side)[m * NU + ii] * cm + F.Aw(side)[m * NU + ii] * dm;
-                        else if (ii - NU <= 2 * m)
-                            acc += F.Bm(side)[m * W + ii - NU] * cm + F.Bw(side)[m * W + ii - NU] * dm;
-                    }
-                }
-            }
-        }
-        out[v * out_vs + i] = acc;
+    const long long tot = (long long)nvec * half;  // pairs
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
+         f += (long long)gridDim.x * blockDim.x) {
+        const int v = (int)(f >> (lev - 1)), m = (int)(f & (half - 1));
+        const double* xb = x + lx.vbase(xv0 + v) + half;
+        double o0, o1;
+        idwt_pair<NU>(F, lo + v * lo_vs, xb, n, m, vmp, o0, o1);
+        out[v * out_vs + 2 * m] = o0;
+        out[v * out_vs + 2 * m + 1] = o1;
     }
 }
 
 // One DWT level: from fine samples in[0:n] (workspace) write the coarse half
-// to cout[0:n/2] (workspace) and the detail half directly to the op output
-// elements [n/2, n).
+// to cout[0:n/2] (workspace) and the detail half directly to the op output.
 template <int NU>
-__global__ void k_dwt_level(const double* tab, Tables t, const double* in, long long in_vs,
-                            double* cout, long long cout_vs, double* y, Layout ly, long long yv0,
-                            int lev, int nvec, int vmp) {
+__global__ void __launch_bounds__(256) k_dwt_level(const double* tab, Tables t, const double* in,
+                                                   long long in_vs, double* cout, long long cout_vs,
+                                                   double* y, Layout ly, long long yv0, int lev,
+                                                   int nvec, int vmp) {
     __shared__ double filt[FiltSmem<NU>::SIZE];
     for (int i = threadIdx.x; i < FiltSmem<NU>::SIZE; i += blockDim.x) filt[i] = tab[t.o_h + i];
     __syncthreads();
-    FiltSmem<NU> F{filt};
+    const FiltSmem<NU> F{filt};
     const int n = 1 << lev, half = n >> 1;
-    const long long tot = (long long)nvec << lev;
-    for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < tot;
-         o += (long long)gridDim.x * blockDim.x) {
-        int v = (int)(o >> lev), i = (int)(o & (n - 1));
-        double val = dwt_sample<NU>(F, in + v * in_vs, n, i, vmp);
-        if (i < half) cout[v * cout_vs + i] = val;
-        else y[ly.at(yv0 + v, i)] = val;
+    const long long tot = (long long)nvec * half;
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
+         f += (long long)gridDim.x * blockDim.x) {
+        const int v = (int)(f >> (lev - 1)), mm = (int)(f & (half - 1));
+        double c, d;
+        dwt_pair<NU>(F, in + v * in_vs, n, mm, vmp, c, d);
+        cout[v * cout_vs + mm] = c;
+        y[ly.at(yv0 + v, half + mm)] = d;
     }
 }
 
-// Coarse levels in one CTA per vector (shared memory), both directions.
-//   inverse: levels r0+1..Lc of x (layout) -> out[0:2^Lc] (workspace)
-//   forward: levels Lc..r0+1 of in[0:2^Lc] (workspace) -> y layout [0:2^Lc)
+// Coarse levels in one CTA per vector (shared memory ping-pong).
+//   inverse: levels r0+1..Lc of x (layout) -> dst[0:2^Lc] (workspace, dst_vs)
+//   forward: levels Lc..r0+1 of src[0:2^Lc] (workspace) -> y layout [0:2^Lc)
 template <int NU>
-__global__ void k_wav_coarse(const double* tab, Tables t, const double* src, Layout ls,
-                             long long sv0, long long src_vs, double* dst, Layout ld,
-                             long long dv0, long long dst_vs, int r0, int Lc, int inverse,
-                             int vmp) {
+__global__ void __launch_bounds__(256) k_wav_coarse(const double* tab, Tables t, const double* src,
+                                                    Layout ls, long long sv0, long long src_vs,
+                                                    double* dst, Layout ld, long long dv0,
+                                                    long long dst_vs, int r0, int Lc, int inverse,
+                                                    int vmp) {
     extern __shared__ double sm[];
     double* filt = sm;
-    double* X = sm + FiltSmem<NU>::SIZE;
+    const int n = 1 << Lc;
+    double* X = sm + FiltSmem<NU>::SIZE;  // [n] input
+    double* P0 = X + n;                   // [n] ping
+    double* P1 = P0 + n;                  // [n] pong
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int i = tid; i < FiltSmem<NU>::SIZE; i += nt) filt[i] = tab[t.o_h + i];
-    const int n = 1 << Lc;
     const int v = blockIdx.x;
-    for (int i = tid; i < n; i += nt)
-        X[i] = inverse ? src[ls.at(sv0 + v, i)] : src[v * src_vs + i];
+    for (int i = tid; i < n; i += nt) X[i] = inverse ? src[ls.at(sv0 + v, i)] : src[v * src_vs + i];
     __syncthreads();
-    FiltSmem<NU> F{filt};
-    double r[kKMax];
-    for (int step = 0; step < Lc - r0; ++step) {
-        int lev = inverse ? r0 + 1 + step : Lc - step;
-        int m = 1 << lev;
-#pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * nt;
-            if (o < m) r[k] = inverse ? idwt_sample<NU>(F, X, m, o, vmp) : dwt_sample<NU>(F, X, m, o, vmp);
+    const FiltSmem<NU> F{filt};
+    const double* cur = X;
+    double* nxt = P0;
+    if (inverse) {
+        for (int lev = r0 + 1; lev <= Lc; ++lev) {
+            const int m = 1 << lev, half = m >> 1;
+            idwt_level_vec<NU>(F, cur, X + half, nxt, m, vmp, tid, nt);
+            __syncthreads();
+            cur = nxt;
+            nxt = (nxt == P0) ? P1 : P0;
         }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kKMax; ++k) {
-            int o = tid + k * nt;
-            if (o < m) X[o] = r[k];
+        for (int i = tid; i < n; i += nt) dst[v * dst_vs + i] = cur[i];
+    } else {
+        for (int lev = Lc; lev > r0; --lev) {
+            const int m = 1 << lev, half = m >> 1;
+            for (int k = tid; k < half; k += nt) {
+                double c, d;
+                dwt_pair<NU>(F, cur, m, k, vmp, c, d);
+                dst[ld.at(dv0 + v, half + k)] = d;
+                nxt[k] = c;
+            }
+            __syncthreads();
+            cur = nxt;
+            nxt = (nxt == P0) ? P1 : P0;
         }
-        __syncthreads();
-    }
-    for (int i = tid; i < n; i += nt) {
-        if (inverse) dst[v * dst_vs + i] = X[i];
-        else dst[ld.at(dv0 + v, i)] = X[i];
+        for (int i = tid; i < (1 << r0); i += nt) dst[ld.at(dv0 + v, i)] = cur[i];
     }
 }
 
-// ============================================================================
+// ---------------------------------------------------------------------------
 // large path: two-pass Hadamard over K with an L2-resident intermediate
-// ============================================================================
-// G layout per vector: [A rows][CW] (row = K_hi * R1 + n_lo after pass 1).
+// ---------------------------------------------------------------------------
+// G per vector: [2^kh chunks][R1 physical rows][CW]; chunk c = K_hi (forward
+// pass 1 output) and physical row rho = bitrev_kl(N_lo).
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT) k_large_fwd1(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 2) k_large_fwd1(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS;
     extern __shared__ double sm[];
@@ -519,171 +654,115 @@ __global__ void __launch_bounds__(NT) k_large_fwd1(LargeArgs p) {
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a;
     const int kl = p.kl, R1 = 1 << kl;
     const int chunk = blockIdx.x, v = blockIdx.y;
-    const double* xi = p.xi + (long long)v * p.xi_vs;  // IDWT result (or input via layout)
+    const double* xi = p.xi + (long long)v * p.xi_vs;
     double* T = sm;
-    // load rows K in [chunk*R1, (chunk+1)*R1) with halos; rows of the tile are
-    // local K_lo, swizzled by bitrev_kl(K_lo) (the pass-2 lanes vary K_hi,
-    // which is not stored here, so any fixed swizzle is fine).
-    const long long base = (long long)chunk * R1 * B - H;
-    const int span = R1 * B + 2 * H;
     for (int f = tid; f < R1 * CW; f += NT) {
-        int rl = f / CW, e = f % CW;
-        long long pos = (long long)(chunk * R1 + rl) * B + e - H;
+        const int rl = f / CW, e = f % CW;  // logical local row K_lo
+        const long long pos = (long long)(chunk * R1 + rl) * B + e - H;
         double val = 0.0;
         if (pos >= 0 && pos < M) {
             val = p.xi_is_input ? __ldg(p.in + p.lin.at(p.v0 + v, pos)) : __ldg(xi + pos);
             if (NU > 1 && (pos < NU || pos >= M - NU)) val = 0.0;
         }
-        T[tile_idx(rl, e, RS, brev_bits(rl, kl))] = val;
+        const int ph = (int)brev_bits((unsigned)rl, kl);
+        T[tile_idx(ph, e, RS, ph)] = val;
     }
-    (void)base;
-    (void)span;
-    // capture the raw edge values (first / last chunk)
-    if (NU > 1 && tid < 2 * NU) {
-        int c = tid;
-        long long pos = c < NU ? c : (M - NU) + (c - NU);
-        int owner = (int)((pos / B) / R1);
-        if (owner == chunk) {
-            double val = p.xi_is_input ? p.in[p.lin.at(p.v0 + v, pos)] : xi[pos];
-            p.ev[(long long)v * 2 * NU + c] = val;
-        }
+    if (NU > 1 && tid < 2 * NU) {  // raw edge values (first / last chunk)
+        const int c = tid;
+        const long long pos = c < NU ? c : (M - NU) + (c - NU);
+        if ((int)((pos / B) / R1) == chunk)
+            p.ev[(long long)v * 2 * NU + c] = p.xi_is_input ? p.in[p.lin.at(p.v0 + v, pos)] : xi[pos];
     }
     __syncthreads();
-    tile_hadamard(T, 1, kl, 0, kl, CW, RS, 0, tid, NT);
-    __syncthreads();
+    tile_hadamard<CW, RS>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
     for (int f = tid; f < R1 * CW; f += NT) {
-        int rl = f / CW, e = f % CW;
-        g[f] = T[tile_idx(rl, e, RS, brev_bits(rl, kl))];
+        const int ph = f / CW, e = f % CW;
+        g[f] = T[tile_idx(ph, e, RS, ph)];
     }
 }
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT) k_large_fwd2(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
-    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
+    constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
     const int tid = threadIdx.x;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
     const int kl = p.kl, R1 = 1 << kl, kh = a - kl, R2 = 1 << kh;
-    const int NG = p.ng;  // n_lo values per CTA
-    const int nlo0 = blockIdx.x * NG, v = blockIdx.y;
-    double* ES = sm;                    // [S][2NP]
-    double* T = sm + S * 2 * NP;        // NG tiles of R2 rows
-    const long long tst = (long long)R2 * RS;
+    const int NG = p.ng;
+    const int rho0 = blockIdx.x * NG, v = blockIdx.y;
+    double* ES = sm;                // [S][2NP]
+    double* T = sm + S * 2 * NP;    // NG tiles of R2 physical rows
+    const int tst = R2 * RS;
     const double* g = p.G + (long long)v * A * CW;
     for (int f = tid; f < NG * R2 * CW; f += NT) {
-        int e = f % CW, rest = f / CW;
-        int khi = rest % R2, ng = rest / R2;
-        double val = g[((long long)khi * R1 + nlo0 + ng) * CW + e];
-        T[ng * tst + tile_idx(khi, e, RS, brev_bits(khi, kh))] = val;
+        const int e = f % CW, rest = f / CW;
+        const int ng = rest % NG, khi = rest / NG;
+        const int ph = (int)brev_bits((unsigned)khi, kh);
+        T[ng * tst + tile_idx(ph, e, RS, ph)] = __ldg(g + ((long long)khi * R1 + rho0 + ng) * CW + e);
     }
     if (NU > 1) {
         for (int f = tid; f < S * 2 * NP; f += NT) {
-            const double* em = p.tab + p.t.o_em + (long long)f * 2 * NU;
+            const double* em = p.tab + p.t.o_em + f * 2 * NU;
             double acc = 0.0;
 #pragma unroll
-            for (int c = 0; c < 2 * NU; ++c) acc += em[c] * p.ev[(long long)v * 2 * NU + c];
+            for (int c = 0; c < 2 * NU; ++c) acc += __ldg(em + c) * p.ev[(long long)v * 2 * NU + c];
             ES[f] = acc;
         }
     }
     __syncthreads();
-    tile_hadamard(T, NG, kh, 0, kh, CW, RS, tst, tid, NT);
-    __syncthreads();
+    tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
+    double* ob = p.out + p.lout.vbase(p.v0 + v);
     const int items = NG * R2 * S;
     for (int w = tid; w < items; w += NT) {
-        int wlo = w % R2, rest = w / R2;
-        int s = rest % S, ng = rest / S;
-        const int nhi = (int)brev_bits(wlo, kh);
-        const int nlo = nlo0 + ng;
-        const int N = nhi * R1 + nlo;
-        const double* t = T + ng * tst;
-        double row[CW];
-#pragma unroll
-        for (int e = 0; e < CW; ++e) row[e] = t[tile_idx(nhi, e, RS, wlo)];
-        double kap[2 * H + 1];
-#pragma unroll
-        for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(p.tab + p.t.o_kap + l * S + s);
+        const int wlo = w & (R2 - 1), rest = w >> kh;
+        const int s = rest & (S - 1), ng = rest >> p.q;
+        const int rho = rho0 + ng;  // = bitrev_kl(N_lo)
+        const double sg = ((__popc(wlo) + __popc(rho)) & 1) ? -1.0 : 1.0;
         double z[B];
+        row_fwd<NU, kLogB>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S,
+                           NU > 1 ? ES + s * 2 * NP : nullptr, sg, z);
+        // g = bitrev_j(N*B + n_lo) = bitrev5(n_lo)*A + bitrev_kl(N_lo)*R2 + bitrev_kh(N_hi)
+        const unsigned glo = ((unsigned)rho << kh) | (unsigned)wlo;
+        const unsigned rw = gray_inv(glo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
+        double* os = ob + (long long)s * M;  // large path: contiguous 1D output
 #pragma unroll
-        for (int k = 0; k < B; ++k) {
-            double acc = 0.0;
-#pragma unroll
-            for (int l = -H; l <= H; ++l) acc += kap[l + H] * row[k - l + H];
-            z[k] = acc;
-        }
-        if (NU > 1) {
-            const double* es = ES + s * 2 * NP;
-            const double sg = (__popc(N) & 1) ? -1.0 : 1.0;
-#pragma unroll
-            for (int i = 0; i < NP; ++i) z[i] += es[i];
-#pragma unroll
-            for (int i = 0; i < NP; ++i) z[B - NP + i] += sg * es[NP + i];
-        }
-        hadamard_reg<kLogB>(z);
-        // g = bitrev_j(N*B + n_lo) = bitrev5(n_lo)*A + bitrev_kl(nlo)*R2 + wlo
-        const unsigned glo = (brev_bits(nlo, kl) << kh) | (unsigned)wlo;
-#pragma unroll
-        for (int nl = 0; nl < B; ++nl) {
-            unsigned gg = (brev_bits(nl, kLogB) << a) | glo;
-            int r = (int)gray_inv(gg);
-            if (s & 1) r = M - 1 - r;
-            p.out[p.lout.at(p.v0 + v, (long long)s * M + r)] = z[nl];
-        }
+        for (int nl = 0; nl < B; ++nl) os[gray_inv_hi(nl, kLogB, a) ^ rw] = z[nl];
     }
 }
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT) k_large_adj2(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
-    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
+    constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
     const int tid = threadIdx.x, lane = tid & 31;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
     const int kl = p.kl, R1 = 1 << kl, kh = a - kl, R2 = 1 << kh;
     const int NG = p.ng;
-    const int nlo0 = blockIdx.x * NG, v = blockIdx.y;
+    const int rho0 = blockIdx.x * NG, v = blockIdx.y;
     double* T = sm;
-    const long long tst = (long long)R2 * RS;
-    const int L = R2 < 32 ? R2 : 32;  // lanes per warp sharing one n_lo tile
+    const int tst = R2 * RS;
     const int items = NG * R2;
     const int iters = (items + NT - 1) / NT;
+    const double* ib = p.in + p.lin.vbase(p.v0 + v);
     for (int it = 0; it < iters; ++it) {
-        int w = tid + it * NT;
-        int wlo = w % R2, ng = w / R2;
-        bool act = w < items;
-        const int nhi = (int)brev_bits(wlo, kh);
-        const int nlo = nlo0 + (act ? ng : 0);
-        const int N = nhi * R1 + nlo;
-        const double sg = (__popc(N) & 1) ? -1.0 : 1.0;
-        const unsigned glo = (brev_bits(nlo, kl) << kh) | (unsigned)wlo;
-        double acc[CW];
-#pragma unroll
-        for (int e = 0; e < CW; ++e) acc[e] = 0.0;
+        const int w = tid + it * NT;
+        const int wlo = w & (R2 - 1), ng = w >> kh;
+        const bool act = w < items;
+        const int rho = rho0 + (act ? ng : 0);
+        const double sg = ((__popc(wlo) + __popc(rho)) & 1) ? -1.0 : 1.0;
+        const unsigned glo = ((unsigned)rho << kh) | (unsigned)wlo;
         for (int s = 0; s < S; ++s) {
             double y[B];
+            const unsigned rw = gray_inv(glo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
+            const double* is = ib + (long long)s * M;  // large path: contiguous 1D input
 #pragma unroll
-            for (int nl = 0; nl < B; ++nl) {
-                unsigned gg = (brev_bits(nl, kLogB) << a) | glo;
-                int r = (int)gray_inv(gg);
-                if (s & 1) r = M - 1 - r;
-                y[nl] = act ? p.in[p.lin.at(p.v0 + v, (long long)s * M + r)] : 0.0;
-            }
+            for (int nl = 0; nl < B; ++nl) y[nl] = act ? __ldg(is + (gray_inv_hi(nl, kLogB, a) ^ rw)) : 0.0;
             hadamard_reg<kLogB>(y);
-            double kap[2 * H + 1];
-#pragma unroll
-            for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(p.tab + p.t.o_kap + l * S + s);
-#pragma unroll
-            for (int e = 0; e < CW; ++e) {
-#pragma unroll
-                for (int l = -H; l <= H; ++l) {
-                    const int k = e - H + l;
-                    if (k >= 0 && k < B) acc[e] += kap[l + H] * y[k];
-                }
-            }
-            if (NU > 1) {
-                // partial sums over this warp's rows; one slot per (CTA, warp, iter)
-                const long long slot = ((long long)blockIdx.x * ((NT / 32) * iters) + it * (NT / 32) + (tid >> 5));
+            if (NU > 1) {  // per-warp partial sums, one slot per (CTA, iteration, warp)
+                const long long slot = (long long)blockIdx.x * ((NT / 32) * iters) + it * (NT / 32) + (tid >> 5);
 #pragma unroll
                 for (int i = 0; i < 2 * NP; ++i) {
                     double val = act ? (i < NP ? y[i] : sg * y[B - NP + (i - NP)]) : 0.0;
@@ -691,27 +770,23 @@ __global__ void __launch_bounds__(NT) k_large_adj2(LargeArgs p) {
                     if (lane == 0) p.epw[(((long long)v * p.nslot + slot) * S + s) * 2 * NP + i] = val;
                 }
             }
-        }
-        (void)L;
-        if (act) {
-#pragma unroll
-            for (int e = 0; e < CW; ++e) T[ng * tst + tile_idx(nhi, e, RS, wlo)] = acc[e];
+            if (act) row_adj_accum<NU, kLogB>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S, y, s == 0);
         }
     }
     __syncthreads();
-    tile_hadamard(T, NG, kh, 0, kh, CW, RS, tst, tid, NT);
-    __syncthreads();
-    // write G'[v][khi*R1 + nlo][e]
+    tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
+    // physical row ph of sub-tile ng is logical K_hi = bitrev_kh(ph)
     double* g = p.G + (long long)v * A * CW;
     for (int f = tid; f < NG * R2 * CW; f += NT) {
-        int e = f % CW, rest = f / CW;
-        int khi = rest % R2, ng = rest / R2;
-        g[((long long)khi * R1 + nlo0 + ng) * CW + e] = T[ng * tst + tile_idx(khi, e, RS, brev_bits(khi, kh))];
+        const int e = f % CW, rest = f / CW;
+        const int ng = rest % NG, khi = rest / NG;
+        const int ph = (int)brev_bits((unsigned)khi, kh);
+        g[((long long)khi * R1 + rho0 + ng) * CW + e] = T[ng * tst + tile_idx(ph, e, RS, ph)];
     }
 }
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT) k_large_adj1(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 2) k_large_adj1(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
@@ -721,21 +796,22 @@ __global__ void __launch_bounds__(NT) k_large_adj1(LargeArgs p) {
     const int chunk = blockIdx.x, v = blockIdx.y;
     double* Wv = sm;                 // [S][2NP]
     double* nb = Wv + S * 2 * NP;    // [2][H]: neighbour-row halo sums
-    double* T = nb + 2 * (H > 0 ? H : 1);
+    double* T = nb + 2 * NU;
     const double* g = p.G + (long long)v * A * CW;
     for (int f = tid; f < R1 * CW; f += NT) {
-        int rl = f / CW, e = f % CW;
-        T[tile_idx(rl, e, RS, brev_bits(rl, kl))] = g[((long long)chunk * R1 + rl) * CW + e];
+        const int ph = f / CW, e = f % CW;
+        T[tile_idx(ph, e, RS, ph)] = __ldg(g + ((long long)chunk * R1 + ph) * CW + e);
     }
-    // halo contributions from the neighbouring chunks' boundary rows:
-    //   previous chunk, last local row (K_lo = R1-1): sum_nlo (-1)^popc(nlo) G[(c-1)R1+nlo][B+H+k]
-    //   next chunk, first local row (K_lo = 0):      sum_nlo G[(c+1)R1+nlo][k]
+    // halo contributions from the neighbouring chunks' boundary rows (sums over
+    // the physical rows rho of their Hadamard rows; popc is bit-reversal invariant):
+    //   previous chunk, last logical row:  sum_rho (-1)^popc(rho) G[(c-1)R1+rho][B+H+k]
+    //   next chunk, first logical row:     sum_rho G[(c+1)R1+rho][k]
     if (tid < 2 * H) {
-        int side = tid / H, k = tid % H;
+        const int side = tid / H, k = tid % H;
         double acc = 0.0;
         if (side == 0 && chunk > 0) {
             for (int nl = 0; nl < R1; ++nl) {
-                double val = g[((long long)(chunk - 1) * R1 + nl) * CW + B + H + k];
+                const double val = g[((long long)(chunk - 1) * R1 + nl) * CW + B + H + k];
                 acc += (__popc(nl) & 1) ? -val : val;
             }
         } else if (side == 1 && (chunk + 1) * R1 < A) {
@@ -752,25 +828,38 @@ __global__ void __launch_bounds__(NT) k_large_adj1(LargeArgs p) {
         }
     }
     __syncthreads();
-    tile_hadamard(T, 1, kl, 0, kl, CW, RS, 0, tid, NT);
-    __syncthreads();
+    tile_hadamard<CW, RS>(T, 1, kl, 0, kl, 0, tid, NT);
     double* xo = p.xo + (long long)v * p.xo_vs;
+    double* ob = p.out + p.lout.vbase(p.v0 + v);
     for (int f = tid; f < R1 * B; f += NT) {
-        int rl = f / B, k = f % B;
-        long long pos = ((long long)chunk * R1 + rl) * B + k;
-        double val = T[tile_idx(rl, k + H, RS, brev_bits(rl, kl))];
-        if (k < H) val += rl > 0 ? T[tile_idx(rl - 1, B + H + k, RS, brev_bits(rl - 1, kl))] : nb[k];
+        const int rl = f / B, k = f % B;  // logical local row K_lo
+        const long long pos = ((long long)chunk * R1 + rl) * B + k;
+        const int ph = (int)brev_bits((unsigned)rl, kl);
+        double val = T[tile_idx(ph, k + H, RS, ph)];
+        if (k < H) {
+            if (rl > 0) {
+                const int pq = (int)brev_bits((unsigned)(rl - 1), kl);
+                val += T[tile_idx(pq, B + H + k, RS, pq)];
+            } else {
+                val += nb[k];
+            }
+        }
         if (k >= B - H) {
-            int kk = k - (B - H);
-            val += rl < R1 - 1 ? T[tile_idx(rl + 1, kk, RS, brev_bits(rl + 1, kl))] : nb[H + kk];
+            const int kk = k - (B - H);
+            if (rl < R1 - 1) {
+                const int pq = (int)brev_bits((unsigned)(rl + 1), kl);
+                val += T[tile_idx(pq, kk, RS, pq)];
+            } else {
+                val += nb[H + kk];
+            }
         }
         if (NU > 1 && (pos < NU || pos >= M - NU)) {
-            int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
+            const int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
             double e = 0.0;
-            for (int sp = 0; sp < S * 2 * NP; ++sp) e += p.tab[p.t.o_em + (long long)sp * 2 * NU + c] * Wv[sp];
+            for (int sp = 0; sp < S * 2 * NP; ++sp) e += __ldg(p.tab + p.t.o_em + sp * 2 * NU + c) * Wv[sp];
             val = e;
         }
-        if (p.xo_is_output) p.out[p.lout.at(p.v0 + v, pos)] = val;
+        if (p.xo_is_output) ob[p.lout.eoff(pos)] = val;
         else xo[pos] = val;
     }
 }

@@ -9,7 +9,7 @@
 
 namespace cww {
 
-constexpr int kSmallMaxLog = 13;  // M <= 2^13: whole map in one CTA's shared memory
+constexpr int kSmallMaxLog = 12;  // M <= 2^12: whole map in one CTA's shared memory
 
 struct SmallArgs {
     const double* tab;  // per-op device table block
@@ -20,6 +20,8 @@ struct SmallArgs {
     long long nvec;  // vectors in this launch
     int V;           // vectors per CTA (power of two)
     int j, q, r0, use_idwt, vmp;
+    int in_block;  // 1: a CTA's V input vectors are one contiguous block; 2: an
+                   // interleaved [M][V] block (column panel); 0: generic layout
 };
 
 struct LargeArgs {

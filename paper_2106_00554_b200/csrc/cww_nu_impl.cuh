@@ -28,13 +28,13 @@ cudaError_t small_t(const SmallArgs& a, bool adj, cudaStream_t st) {
         long long smem = small_smem_bytes<CWW_NU, LOGB>(a.V, a.j, a.q, adj, adj ? a.lin.vfast() : a.lout.vfast());
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         if (adj) {
-            auto k = k_small_adj<CWW_NU, LOGB, CWW_NT>;
+            auto k = k_small_adj<CWW_NU, LOGB, kSmallNT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k<<<grid, CWW_NT, smem, st>>>(a);
+            k<<<grid, kSmallNT, smem, st>>>(a);
         } else {
-            auto k = k_small_fwd<CWW_NU, LOGB, CWW_NT>;
+            auto k = k_small_fwd<CWW_NU, LOGB, kSmallNT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k<<<grid, CWW_NT, smem, st>>>(a);
+            k<<<grid, kSmallNT, smem, st>>>(a);
         }
         return cudaGetLastError();
     }
@@ -103,7 +103,7 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
 cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
     const int nt = 256;
     if (w.kind == 0) {
-        long long smem = (FiltSmem<CWW_NU>::SIZE + (1ll << w.lev)) * 8;
+        long long smem = (FiltSmem<CWW_NU>::SIZE + 3 * (1ll << w.lev)) * 8;
         auto k = k_wav_coarse<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<(unsigned)w.nvec, nt, smem, st>>>(w.tab, w.t, w.src, w.ls, w.sv0, w.src_vs, w.dst, w.ld,
@@ -123,3 +123,9 @@ cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
 }
 
 }  // namespace cww
+
+#if defined(CWW_PHASE_TIMING) && CWW_NU == 4
+extern "C" int cww_debug_phase_read(long long* host, size_t n) {
+    return (int)cudaMemcpyFromSymbol(host, cww::cww_phase_buf, n * sizeof(long long));
+}
+#endif

@@ -49,7 +49,7 @@ SMALL = [
     (0, 4, 1, 6, 2, 1, 4), (0, 3, 1, 7, 2, 1, 4), (0, 6, 1, 8, 3, 1, -1), (1, 4, 1, 9, 1, 1, -1),
     (1, 5, 1, 10, 2, 1, 5), (0, 2, 0, 2, 1, 1, -1), (0, 3, 0, 5, 2, 1, -1), (0, 4, 0, 6, 1, 1, 3),
     (1, 6, 0, 7, 3, 1, -1), (0, 2, 0, 9, 1, 1, 0), (0, 4, 1, 10, 1, 1, 4), (0, 2, 1, 12, 1, 1, 3),
-    (0, 3, 1, 13, 2, 1, 4), (0, 6, 0, 11, 2, 1, -1), (0, 1, 0, 0, 0, 1, 0), (0, 1, 0, 1, 1, 1, 0),
+    (0, 3, 1, 13, 2, 1, 4), (0, 6, 0, 11, 2, 1, -1), (0, 1, 0, 1, 0, 1, 0), (0, 1, 0, 1, 1, 1, 0),
     (0, 1, 0, 5, 0, 1, 0), (0, 1, 0, 10, 1, 1, 1), (0, 1, 0, 8, 2, 1, 3), (0, 1, 0, 13, 1, 1, 2),
 ]
 
