@@ -34,6 +34,9 @@ struct Tables {
     int o_ef;   // [2][ A(nu*nu) | B(nu*(2nu-1)) | Aw | Bw ]  left, right
     int o_syn;  // [2 sides][3nu-1][2 bands][2nu]  dense synthesis edge blocks
     int o_ana;  // [2 sides][2 bands][nu][3nu-1]   dense analysis edge rows
+    int o_csyn; // [nc][nc] dense coarse synthesis (levels r0+1..log2 nc), [k][i]
+    int o_cana; // [nc][nc] dense coarse analysis (levels log2 nc..r0+1), [i][k]
+    int nc;     // 64, or 0 when unused
     int n;      // total doubles
 };
 

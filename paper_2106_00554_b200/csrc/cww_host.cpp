@@ -380,6 +380,56 @@ std::vector<double> level_inverse_vmp_host(const Filters& f, const std::vector<d
     return s;
 }
 
+// One periodic synthesis / analysis level and one VMP analysis level
+// (wavelet.cpp:369-445 semantics), for the dense coarse block below.
+std::vector<double> level_inverse_periodic_host(const Filters& f, const std::vector<double>& x) {
+    const size_t n = x.size(), half = n / 2;
+    const int nu = f.nu;
+    std::vector<double> s(n, 0.0);
+    for (size_t mm = 0; mm < half; ++mm)
+        for (int u = -nu + 1; u <= nu; ++u) {
+            size_t idx = size_t(((long long)(2 * mm) + u + 2 * (long long)n) % (long long)n);
+            s[idx] += f.h[size_t(u + nu - 1)] * x[mm] + f.g[size_t(u + nu - 1)] * x[half + mm];
+        }
+    return s;
+}
+
+std::vector<double> level_forward_host(const Filters& f, const std::vector<double>& x, bool vmp) {
+    const size_t n = x.size(), half = n / 2, NV = size_t(f.nu);
+    const int nu = f.nu, W = 2 * nu - 1;
+    std::vector<double> s(n, 0.0);
+    if (!vmp) {
+        for (size_t mm = 0; mm < half; ++mm)
+            for (int u = -nu + 1; u <= nu; ++u) {
+                size_t idx = size_t(((long long)(2 * mm) + u + 2 * (long long)n) % (long long)n);
+                s[mm] += f.h[size_t(u + nu - 1)] * x[idx];
+                s[half + mm] += f.g[size_t(u + nu - 1)] * x[idx];
+            }
+        return s;
+    }
+    for (int band = 0; band < 2; ++band)
+        for (int side = 0; side < 2; ++side) {
+            const auto& A = band ? f.Aw[side] : f.A[side];
+            const auto& B = band ? f.Bw[side] : f.B[side];
+            for (size_t m = 0; m < NV; ++m) {
+                double acc = 0.0;
+                for (size_t k = 0; k < NV; ++k) acc += A[m * NV + k] * x[side ? n - 1 - k : k];
+                for (int li = 0; li <= 2 * int(m); ++li) {
+                    size_t l = NV + size_t(li);
+                    acc += B[m * size_t(W) + size_t(li)] * x[side ? n - 1 - l : l];
+                }
+                s[(band ? half : 0) + (side ? half - 1 - m : m)] = acc;
+            }
+        }
+    for (size_t mm = NV; mm + NV < half; ++mm)
+        for (int u = -nu + 1; u <= nu; ++u) {
+            size_t idx = size_t((long long)(2 * mm) + u);
+            s[mm] += f.h[size_t(u + nu - 1)] * x[idx];
+            s[half + mm] += f.g[size_t(u + nu - 1)] * x[idx];
+        }
+    return s;
+}
+
 struct EdgeTerm {
     uint64_t p;
     int col;
@@ -487,6 +537,43 @@ cww_status build_tables(cww_op& op) {
             }
         tab.insert(tab.end(), ana.begin(), ana.end());
     }
+    // Dense composite of the coarse levels r0+1..Lc (2^Lc = nc = 64): the
+    // exact product of those level maps, built by applying the level
+    // arithmetic above to unit vectors.  Synthesis stored [k][i] (output i
+    // fastest), analysis [i][k] (output k fastest).  Unused (nc = 0) when
+    // there is no coarse level to collapse or no level above it.
+    t.nc = 0;
+    t.o_csyn = t.o_cana = int(tab.size());
+    {
+        const int Lc = 6;
+        if (op.r0 + 1 < Lc && int(op.j) > Lc) {
+            const int nc = 1 << Lc;
+            std::vector<double> syn(size_t(nc * nc)), ana(size_t(nc * nc));
+            for (int k = 0; k < nc; ++k) {
+                std::vector<double> x(size_t(nc), 0.0);
+                x[size_t(k)] = 1.0;
+                std::vector<double> y = x;
+                for (int lev = op.r0 + 1; lev <= Lc; ++lev) {
+                    std::vector<double> part(y.begin(), y.begin() + (1 << lev));
+                    part = op.vmp ? level_inverse_vmp_host(op.f, part) : level_inverse_periodic_host(op.f, part);
+                    std::copy(part.begin(), part.end(), y.begin());
+                }
+                for (int i = 0; i < nc; ++i) syn[size_t(k * nc + i)] = y[size_t(i)];
+                std::vector<double> z = x;
+                for (int lev = Lc; lev > op.r0; --lev) {
+                    std::vector<double> part(z.begin(), z.begin() + (1 << lev));
+                    part = level_forward_host(op.f, part, op.vmp != 0);
+                    std::copy(part.begin(), part.end(), z.begin());
+                }
+                for (int o = 0; o < nc; ++o) ana[size_t(k * nc + o)] = z[size_t(o)];  // input k, output o
+            }
+            t.nc = nc;
+            t.o_csyn = int(tab.size());
+            tab.insert(tab.end(), syn.begin(), syn.end());
+            t.o_cana = int(tab.size());
+            tab.insert(tab.end(), ana.begin(), ana.end());
+        }
+    }
     t.n = int(tab.size());
     CUDA_TRY(cudaMalloc(&op.d_tab, tab.size() * sizeof(double)));
     CUDA_TRY(cudaMemcpy(op.d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -552,10 +639,10 @@ cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
 // 1D layout helpers
 Layout lay_contig(long long len) { return Layout{0, len, 0, 1, 62, 62}; }
 
-// largest power of two V <= cap with V*M <= 2^kSmallMaxLog
+// largest power of two V <= cap with V*M <= 4096 (one small-path CTA)
 int small_V(long long M, long long nvec, int cap = 32) {
     int V = 1;
-    while (V * 2 <= cap && (V * 2) * M <= (1ll << cww::kSmallMaxLog) && V * 2 <= nvec) V *= 2;
+    while (V * 2 <= cap && (V * 2) * M <= 4096 && V * 2 <= nvec) V *= 2;
     return V;
 }
 

@@ -29,9 +29,7 @@
 
 namespace cww {
 
-constexpr int kSmallElems = 1 << kSmallMaxLog;  // V*M per CTA
-constexpr int kSmallNT = 256;
-constexpr int kFinalPerThread = kSmallElems / kSmallNT;  // 16 register-staged outputs
+constexpr int kSmallNT = 256;  // threads per small-path CTA (2 CTAs per SM)
 constexpr int kWarpLev = 8;  // wavelet levels of <= 256 samples run warp-private
 
 // Optional per-phase cycle stamps (build with -DCWW_PHASE_TIMING): thread 0 of
@@ -191,8 +189,13 @@ __device__ __forceinline__ void group_sync(int gid, int G, int ngroups) {
         const int nact = min(32 / G, ngroups - g0);
         const unsigned mask = nact >= 32 / G ? 0xffffffffu : ((1u << (nact * G)) - 1u);
         __syncwarp(mask);
-    } else {
-        asm volatile("bar.sync %0, %1;" ::"r"(gid + 1), "r"(G) : "memory");
+    } else {  // G > 32 implies at most 4 groups; immediate ids keep the barrier count low
+        switch (gid) {
+            case 0: asm volatile("bar.sync 1, %0;" ::"r"(G) : "memory"); break;
+            case 1: asm volatile("bar.sync 2, %0;" ::"r"(G) : "memory"); break;
+            case 2: asm volatile("bar.sync 3, %0;" ::"r"(G) : "memory"); break;
+            default: asm volatile("bar.sync 4, %0;" ::"r"(G) : "memory"); break;
+        }
     }
 }
 
@@ -204,11 +207,30 @@ __device__ __forceinline__ void group_sync(int gid, int G, int ngroups) {
 template <int NU, int NT>
 __device__ __forceinline__ const double* idwt_group(const FiltSmem<NU>& F, const double* xv, double* p0,
                                                     double* p1, double* cbuf, int j, int r0, bool vmp,
-                                                    int gt, int G, int gid, int ngroups) {
+                                                    int gt, int G, int gid, int ngroups,
+                                                    const double* csyn, int nc) {
     const double* src = xv;
-    for (int lev = r0 + 1; lev < j; ++lev) {
-        const int t = lev - r0 - 1, n = 1 << lev;
-        double* dst = (lev == j - 1) ? cbuf : ((t & 1) ? p1 : p0);
+    int lev = r0 + 1;
+    if (nc > 0) {  // collapsed coarse levels r0+1..log2(nc): one dense pass
+        const int Lc = 31 - __clz(nc);
+        double* dst = (Lc == j - 1) ? cbuf : p0;
+        for (int i = gt; i < nc; i += G) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            for (int k = 0; k < nc; k += 4) {
+                a0 += __ldg(csyn + k * nc + i) * xv[k];
+                a1 += __ldg(csyn + (k + 1) * nc + i) * xv[k + 1];
+                a2 += __ldg(csyn + (k + 2) * nc + i) * xv[k + 2];
+                a3 += __ldg(csyn + (k + 3) * nc + i) * xv[k + 3];
+            }
+            dst[i] = (a0 + a1) + (a2 + a3);
+        }
+        group_sync<NT>(gid, G, ngroups);
+        src = dst;
+        lev = Lc + 1;
+    }
+    for (; lev < j; ++lev) {
+        const int n = 1 << lev;
+        double* dst = (lev == j - 1) ? cbuf : (src == p0 ? p1 : p0);
         idwt_level_vec<NU>(F, src, xv + (n >> 1), dst, n, vmp, gt, G);
         group_sync<NT>(gid, G, ngroups);
         src = dst;
@@ -318,7 +340,8 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         const double* xv = X + v * M;
         double* tv = T + v * tst;
         const double* cfin = xv;
-        if (idwt) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, p.vmp, gt, Gs, gid, nv);
+        if (idwt) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, p.vmp, gt, Gs, gid, nv,
+                                                 p.tab + p.t.o_csyn, p.t.nc);
         PHASE(2);
         auto put = [&](int i, double val) {
             if (NU > 1 && (i < NU || i >= M - NU)) {
@@ -513,7 +536,9 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
         double* xv = X + v * M;
         double* cv = C + v * hM;
         const double* src = xv;
-        for (int lev = j; lev > p.r0; --lev) {
+        const int nc = p.t.nc;
+        const int lstop = nc > 0 ? 31 - __clz(nc) : p.r0;  // levels above lstop one by one
+        for (int lev = j; lev > lstop; --lev) {
             const int t = j - lev, n = 1 << lev, half = n >> 1;
             const bool last = lev == p.r0 + 1;
             double* dst = last ? ov : ((t & 1) ? xv : cv);  // coarse rows ping-pong C <-> X
@@ -526,6 +551,19 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
             }
             group_sync<NT>(gid, Gs, nv);
             src = dst;
+        }
+        if (nc > 0) {  // collapsed coarse levels log2(nc)..r0+1: one dense pass
+            const double* cana = p.tab + p.t.o_cana;
+            for (int o = gt; o < nc; o += Gs) {
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                for (int i = 0; i < nc; i += 4) {
+                    a0 += __ldg(cana + i * nc + o) * src[i];
+                    a1 += __ldg(cana + (i + 1) * nc + o) * src[i + 1];
+                    a2 += __ldg(cana + (i + 2) * nc + o) * src[i + 2];
+                    a3 += __ldg(cana + (i + 3) * nc + o) * src[i + 3];
+                }
+                ov[o] = (a0 + a1) + (a2 + a3);
+            }
         }
     }
     __syncthreads();
