@@ -92,3 +92,37 @@ def test_header_documents_reference_interfaces():
     txt = open(HEADER).read()
     for cite in ("fastop.hpp", "wavelet.hpp", "walsh.hpp", "kernel.hpp"):
         assert cite in txt
+
+
+def test_c_and_cpp_headers_compile_and_link(tmp_path):
+    """A C caller (cww_b200.h) and a reference-style C++ caller
+    (cww_b200.hpp: LinearOp / FastOp / ComposedOp over spans) build and link
+    against the in-tree library."""
+    import shutil
+    import subprocess
+    import paper_2106_00554_b200 as cw
+    lib = cw.library_path()
+    c_src = tmp_path / "c_caller.c"
+    c_src.write_text('#include "cww_b200.h"\n#include <stdio.h>\nint main(void){cww_op_desc d; '
+                     'cww_op_desc_init(&d); cww_op* h=0; cww_status s=cww_op_create(&d,&h); '
+                     'printf("%d %s\\n",(int)s,cww_last_error()); return 0;}\n')
+    cpp_src = tmp_path / "cpp_caller.cpp"
+    cpp_src.write_text('#include "cww_b200.hpp"\n#include <vector>\nint main(){ try { '
+                       'cww_b200::WaveletSpec s{cww_b200::Family::Daubechies, 4, cww_b200::Boundary::Vmp};'
+                       ' cww_b200::FastOp op(s, 6, 2); cww_b200::ComposedOp c(op, true, 4);'
+                       ' std::vector<double> x(c.cols()), y(c.rows()); c.forward(x, y); }'
+                       ' catch (const cww_b200::CwwError& e) { return e.status == CWW_ERR_CUDA ? 0 : 1; }'
+                       ' return 0; }\n')
+    inc = os.path.join(REPO, "include")
+    libdir = os.path.dirname(lib)
+    gcc, gxx = shutil.which("gcc"), shutil.which("g++")
+    r = subprocess.run([gcc, "-std=c11", "-I", inc, str(c_src), "-o", str(tmp_path / "c_caller"),
+                        lib, f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([gxx, "-std=c++20", "-I", inc, str(cpp_src), "-o", str(tmp_path / "cpp_caller"),
+                        lib, f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(tmp_path / "c_caller")], capture_output=True, text=True)
+    assert out.returncode == 0
+    run = subprocess.run([str(tmp_path / "cpp_caller")], capture_output=True, text=True)
+    assert run.returncode == 0, run.stdout + run.stderr
