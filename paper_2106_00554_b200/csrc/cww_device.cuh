@@ -139,12 +139,13 @@ __device__ __forceinline__ void tile_hadamard_pass(double* T, int V, int a, int 
     }
 }
 
-// H_A restricted to row bits [lo, hi), passes of <= 5 bits, __syncthreads after each.
-template <int CW, int RS>
+// H_A restricted to row bits [lo, hi), passes of <= MAXR bits (registers:
+// 2^MAXR doubles per thread), __syncthreads after each.
+template <int CW, int RS, int MAXR = 5>
 __device__ __noinline__ void tile_hadamard(double* T, int V, int a, int lo, int hi, int tstride,
                                            int tid, int nt) {
     while (lo < hi) {
-        const int r = hi - lo < 5 ? hi - lo : 5;
+        const int r = hi - lo < MAXR ? hi - lo : MAXR;
         switch (r) {
             case 1: tile_hadamard_pass<1, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
             case 2: tile_hadamard_pass<2, CW, RS>(T, V, a, lo, tstride, tid, nt); break;

@@ -755,6 +755,9 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     w.r0 = op->r0;
     w.vmp = op->vmp;
 
+    a.r0 = op->r0;
+    a.use_idwt = op->d.use_idwt;
+    a.vmp = op->vmp;
     if (!adj) {
         const double* xi = nullptr;
         if (idwt) {

@@ -30,6 +30,7 @@
 namespace cww {
 
 constexpr int kSmallNT = 256;  // threads per small-path CTA (2 CTAs per SM)
+constexpr int kNc = 64;        // dense coarse wavelet block (levels r0+1..6)
 constexpr int kWarpLev = 8;  // wavelet levels of <= 256 samples run warp-private
 
 // Optional per-phase cycle stamps (build with -DCWW_PHASE_TIMING): thread 0 of
@@ -138,6 +139,75 @@ __device__ __forceinline__ void row_load(const double* ib, const Layout& L, int 
     }
 }
 
+// Deterministic segmented transpose-reduce.  The lanes that differ only in
+// the bits `segbits` form one segment (e.g. the lanes sharing a vector).  Each
+// lane holds R values; afterwards the segment's sums are spread over its lanes:
+// v[0..cnt) of a lane with leader == true hold the sums of the original values
+// base*cnt .. base*cnt+cnt-1.  Each step over one segment bit halves the values
+// a lane keeps (R/2 + R/4 + ... shuffles instead of R per bit).
+template <int R, unsigned SEG>
+__device__ __forceinline__ int seg_transpose_reduce(double* v, int lane, int& cnt, bool& leader) {
+    int n = R, base = 0;
+    unsigned rem = 0;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        if (!(SEG & (unsigned)off)) continue;
+        if (n > 1) {
+            const bool upper = (lane & off) != 0;
+            n >>= 1;
+#pragma unroll
+            for (int i = 0; i < R / 2; ++i) {
+                if (i < n) {
+                    const double send = upper ? v[i] : v[i + n];
+                    const double keep = upper ? v[i + n] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
+            }
+            base = (base << 1) | (upper ? 1 : 0);
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+            rem |= (unsigned)off;
+        }
+    }
+    cnt = n;
+    leader = (lane & rem) == 0;
+    return base;
+}
+
+// Reduce the edge values ev[R] over a lane segment and store the sums
+// dst[idx] (idx < nval) from the leader lanes; SEG must be compile-time so
+// every register index is static.
+template <int R, unsigned SEG>
+__device__ __forceinline__ void seg_reduce_store(double* ev, int lane, int nval, bool live, double* dst) {
+    int cnt;
+    bool leader;
+    const int base = seg_transpose_reduce<R, SEG>(ev, lane, cnt, leader);
+    if (leader && live) {
+#pragma unroll
+        for (int k2 = 0; k2 < R; ++k2) {
+            const int idx = base * cnt + k2;
+            if (k2 < cnt && idx < nval) dst[idx] = ev[k2];
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void seg_reduce_store_rt(double* ev, int lane, unsigned seg, int nval, bool live,
+                                                    double* dst) {
+    switch (seg) {
+        case 31u: seg_reduce_store<R, 31u>(ev, lane, nval, live, dst); break;
+        case 30u: seg_reduce_store<R, 30u>(ev, lane, nval, live, dst); break;
+        case 28u: seg_reduce_store<R, 28u>(ev, lane, nval, live, dst); break;
+        case 24u: seg_reduce_store<R, 24u>(ev, lane, nval, live, dst); break;
+        case 16u: seg_reduce_store<R, 16u>(ev, lane, nval, live, dst); break;
+        case 15u: seg_reduce_store<R, 15u>(ev, lane, nval, live, dst); break;
+        case 7u: seg_reduce_store<R, 7u>(ev, lane, nval, live, dst); break;
+        case 3u: seg_reduce_store<R, 3u>(ev, lane, nval, live, dst); break;
+        case 1u: seg_reduce_store<R, 1u>(ev, lane, nval, live, dst); break;
+        default: seg_reduce_store<R, 0u>(ev, lane, nval, live, dst); break;
+    }
+}
+
 // Warp all-reduce over the lanes that share a vector (deterministic butterfly).
 __device__ __forceinline__ double seg_allreduce(double x, int lo_off, int hi_off) {
     for (int off = lo_off; off < hi_off; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
@@ -214,13 +284,14 @@ __device__ __forceinline__ const double* idwt_group(const FiltSmem<NU>& F, const
     if (nc > 0) {  // collapsed coarse levels r0+1..log2(nc): one dense pass
         const int Lc = 31 - __clz(nc);
         double* dst = (Lc == j - 1) ? cbuf : p0;
-        for (int i = gt; i < nc; i += G) {
+        for (int i = gt; i < kNc; i += G) {  // nc == kNc (64) whenever enabled
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            for (int k = 0; k < nc; k += 4) {
-                a0 += __ldg(csyn + k * nc + i) * xv[k];
-                a1 += __ldg(csyn + (k + 1) * nc + i) * xv[k + 1];
-                a2 += __ldg(csyn + (k + 2) * nc + i) * xv[k + 2];
-                a3 += __ldg(csyn + (k + 3) * nc + i) * xv[k + 3];
+#pragma unroll 16
+            for (int k = 0; k < kNc; k += 4) {
+                a0 += __ldg(csyn + k * kNc + i) * xv[k];
+                a1 += __ldg(csyn + (k + 1) * kNc + i) * xv[k + 1];
+                a2 += __ldg(csyn + (k + 2) * kNc + i) * xv[k + 2];
+                a3 += __ldg(csyn + (k + 3) * kNc + i) * xv[k + 3];
             }
             dst[i] = (a0 + a1) + (a2 + a3);
         }
@@ -481,16 +552,18 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
             row_load<LOGB>(ib0 + p.lin.eoff((long long)s * M), p.lin, a, rw, act, y);
             hadamard_reg<LOGB>(y);
             if (NU > 1) {  // transform-domain values at the 4nu-2 edge positions
-                const int lo_off = vf ? V : 1;
-                const int hi_off = vf ? 32 : L;
-                const bool leader = vf ? (lane < V) : ((lane & (L - 1)) == 0);
                 const int slot = ((it * NT + (tid & ~31)) / (vf ? V : 1) / L) % nslot;
+                constexpr int R = 2 * NP <= 16 ? 16 : 32;
+                double ev[R];
 #pragma unroll
-                for (int i = 0; i < 2 * NP; ++i) {
-                    double val = i < NP ? y[i] : sg * y[B - NP + (i - NP)];
-                    val = seg_allreduce(val, lo_off, hi_off);
-                    if (leader && act) EPW[((v * nslot + slot) * S + s) * 2 * NP + i] = val;
-                }
+                for (int i = 0; i < R; ++i)
+                    ev[i] = (act && i < 2 * NP) ? (i < NP ? y[i] : sg * y[B - NP + (i - NP)]) : 0.0;
+                const unsigned segbits = vf ? (31u & ~(unsigned)(V - 1)) : (unsigned)(L - 1);
+                // v is uniform over a segment; a segment is live iff its warp starts
+                // inside the padded item range and its vector exists
+                const bool live = v < nv && (it * NT + (tid & ~31)) < items;
+                seg_reduce_store_rt<R>(ev, lane, segbits, 2 * NP, live,
+                                       EPW + ((v * nslot + slot) * S + s) * 2 * NP);
             }
             if (act) row_adj_accum<NU, LOGB>(T + v * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S, y, s == 0);
         }
@@ -554,13 +627,14 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
         }
         if (nc > 0) {  // collapsed coarse levels log2(nc)..r0+1: one dense pass
             const double* cana = p.tab + p.t.o_cana;
-            for (int o = gt; o < nc; o += Gs) {
+            for (int o = gt; o < kNc; o += Gs) {
                 double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                for (int i = 0; i < nc; i += 4) {
-                    a0 += __ldg(cana + i * nc + o) * src[i];
-                    a1 += __ldg(cana + (i + 1) * nc + o) * src[i + 1];
-                    a2 += __ldg(cana + (i + 2) * nc + o) * src[i + 2];
-                    a3 += __ldg(cana + (i + 3) * nc + o) * src[i + 3];
+#pragma unroll 16
+                for (int i = 0; i < kNc; i += 4) {
+                    a0 += __ldg(cana + i * kNc + o) * src[i];
+                    a1 += __ldg(cana + (i + 1) * kNc + o) * src[i + 1];
+                    a2 += __ldg(cana + (i + 2) * kNc + o) * src[i + 2];
+                    a3 += __ldg(cana + (i + 3) * kNc + o) * src[i + 3];
                 }
                 ov[o] = (a0 + a1) + (a2 + a3);
             }
@@ -678,13 +752,105 @@ __global__ void __launch_bounds__(256) k_wav_coarse(const double* tab, Tables t,
 }
 
 // ---------------------------------------------------------------------------
+// windowed multilevel synthesis (large path forward: every chunk builds its
+// own pyramid of level windows straight from x, coarse to fine)
+// ---------------------------------------------------------------------------
+
+// Coarse-index range [clo, chi) of level n/2 that the synthesis of fine
+// samples [lo, hi) of level n reads (interior taps; VMP edge samples read the
+// first/last 2nu coarse entries).  Periodic windows may start below 0 / end
+// past n/2: they are read modulo n/2.
+template <int NU>
+__device__ __forceinline__ void idwt_need(int n, int lo, int hi, bool vmp, int& clo, int& chi) {
+    const int half = n >> 1;
+    clo = (lo - NU) >> 1;                    // floor((lo - nu) / 2)
+    chi = ((hi - 1 + NU - 1) >> 1) + 1;      // floor((hi - 1 + nu - 1) / 2) + 1
+    if (vmp) {
+        constexpr int EL = FiltSmem<NU>::EL, CI = FiltSmem<NU>::CI;
+        if (n < 8 * NU) {  // generic coarse levels: whole level
+            clo = 0;
+            chi = half;
+            return;
+        }
+        if (clo < 0) clo = 0;
+        if (chi > half) chi = half;
+        if (lo < EL && chi < CI) chi = CI;
+        if (hi > n - EL && clo > half - CI) clo = half - CI;
+    } else if (chi - clo >= half) {  // the window wraps onto itself: whole level
+        clo = 0;
+        chi = half;
+    }
+}
+
+// Fine samples [lo, hi) of level n from windows cw = c[clo .. chi), dw =
+// d[clo .. chi) (same range; periodic: entries taken modulo n/2), written to
+// out[i - lo] (or, when put != nullptr, handed to put(i, value)).
+template <int NU, class Put>
+__device__ __forceinline__ void idwt_window(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* cw,
+                                            const double* dw, int clo, int n, int lo, int hi, bool vmp,
+                                            int t0, int nthr, Put&& put) {
+    const double* cv = cw - clo;  // absolute (logical) coarse index
+    const double* dv = dw - clo;
+    if (vmp && n < 8 * NU) {
+        for (int i = lo + t0; i < hi; i += nthr) put(i, idwt_sample_full2<NU>(F, cv, dv, n, i, true));
+        return;
+    }
+    constexpr int EL = FiltSmem<NU>::EL;
+    int mlo = (lo + 1) >> 1, mhi = hi >> 1;  // pairs (2m, 2m+1) fully inside [lo, hi)
+    if (vmp) {
+        mlo = max(mlo, (EL + 1) >> 1);
+        mhi = min(mhi, (n - EL) >> 1);
+    }
+    for (int m = mlo + t0; m < mhi; m += nthr) {
+        constexpr int OFF = (NU + 1) / 2;
+        double c[NU + 1], d[NU + 1];
+#pragma unroll
+        for (int k = 0; k <= NU; ++k) {
+            c[k] = cv[m - OFF + k];
+            d[k] = dv[m - OFF + k];
+        }
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            if ((u & 1) == 0) {
+                a0 += tp.h[u + NU - 1] * c[OFF - u / 2];
+                b0 += tp.g[u + NU - 1] * d[OFF - u / 2];
+            } else {
+                a1 += tp.h[u + NU - 1] * c[OFF - (u - 1) / 2];
+                b1 += tp.g[u + NU - 1] * d[OFF - (u - 1) / 2];
+            }
+        }
+        put(2 * m, a0 + b0);
+        put(2 * m + 1, a1 + b1);
+    }
+    // the rest of [lo, hi): partial pairs at the window ends and VMP edge samples
+    const int nl = 2 * mlo - lo, nr = hi - 2 * mhi;
+    for (int k = nthr - 1 - t0; k < nl + nr; k += nthr) {
+        const int i = k < nl ? lo + k : 2 * mhi + (k - nl);
+        if (!vmp) {
+            const int par = (i + NU + 1) & 1;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < NU; ++q) {
+                const int u = -NU + 1 + 2 * q + par;
+                const int mm = (i - u) >> 1;  // logical index, inside the window
+                acc += tp.h[u + NU - 1] * cv[mm] + tp.g[u + NU - 1] * dv[mm];
+            }
+            put(i, acc);
+        } else {
+            put(i, idwt_one<NU>(F, cv, dv, n, i, true));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // large path: two-pass Hadamard over K with an L2-resident intermediate
 // ---------------------------------------------------------------------------
 // G per vector: [2^kh chunks][R1 physical rows][CW]; chunk c = K_hi (forward
 // pass 1 output) and physical row rho = bitrev_kl(N_lo).
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT, 2) k_large_fwd1(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS;
     extern __shared__ double sm[];
@@ -712,7 +878,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd1(LargeArgs p) {
             p.ev[(long long)v * 2 * NU + c] = p.xi_is_input ? p.in[p.lin.at(p.v0 + v, pos)] : xi[pos];
     }
     __syncthreads();
-    tile_hadamard<CW, RS>(T, 1, kl, 0, kl, 0, tid, NT);
+    tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
     for (int f = tid; f < R1 * CW; f += NT) {
         const int ph = f / CW, e = f % CW;
@@ -800,13 +966,13 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
             for (int nl = 0; nl < B; ++nl) y[nl] = act ? __ldg(is + (gray_inv_hi(nl, kLogB, a) ^ rw)) : 0.0;
             hadamard_reg<kLogB>(y);
             if (NU > 1) {  // per-warp partial sums, one slot per (CTA, iteration, warp)
-                const long long slot = (long long)blockIdx.x * ((NT / 32) * iters) + it * (NT / 32) + (tid >> 5);
+                constexpr int R = 2 * NP <= 16 ? 16 : 32;
+                double ev[R];
 #pragma unroll
-                for (int i = 0; i < 2 * NP; ++i) {
-                    double val = act ? (i < NP ? y[i] : sg * y[B - NP + (i - NP)]) : 0.0;
-                    val = seg_allreduce(val, 1, 32);
-                    if (lane == 0) p.epw[(((long long)v * p.nslot + slot) * S + s) * 2 * NP + i] = val;
-                }
+                for (int i = 0; i < R; ++i)
+                    ev[i] = (act && i < 2 * NP) ? (i < NP ? y[i] : sg * y[B - NP + (i - NP)]) : 0.0;
+                const long long slot = (long long)blockIdx.x * ((NT / 32) * iters) + it * (NT / 32) + (tid >> 5);
+                seg_reduce_store<R, 31u>(ev, lane, 2 * NP, true, p.epw + (((long long)v * p.nslot + slot) * S + s) * 2 * NP);
             }
             if (act) row_adj_accum<NU, kLogB>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S, y, s == 0);
         }
@@ -824,7 +990,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 }
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT, 2) k_large_adj1(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
@@ -866,7 +1032,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj1(LargeArgs p) {
         }
     }
     __syncthreads();
-    tile_hadamard<CW, RS>(T, 1, kl, 0, kl, 0, tid, NT);
+    tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* xo = p.xo + (long long)v * p.xo_vs;
     double* ob = p.out + p.lout.vbase(p.v0 + v);
     for (int f = tid; f < R1 * B; f += NT) {

@@ -28,6 +28,7 @@ struct LargeArgs {
     const double* tab;
     Tables t;
     int j, q, kl, ng;  // kl: low K bits handled by the contiguous pass; ng: n_lo per CTA
+    int r0, use_idwt, vmp;
     long long nvec;
     long long v0;      // global index of the first vector (for the I/O layouts)
     // forward pass 1 source: xi workspace (xi_vs per vector) or the op input
