@@ -403,6 +403,40 @@ __device__ __forceinline__ void idwt_pair_inner(const Taps<NU>& tp, const double
     o1 = a1 + b1;
 }
 
+// Two interior pairs (samples 2m .. 2m+3) from one window of nu+2 coarse and
+// nu+2 detail samples (periodic: masked indices).
+template <int NU>
+__device__ __forceinline__ void idwt_quad_inner(const Taps<NU>& tp, const double* cv, const double* dv,
+                                                int n, int m, bool vmp, double* o) {
+    constexpr int OFF = (NU + 1) / 2;
+    const int half = n >> 1;
+    double cw[NU + 2], dw[NU + 2];
+#pragma unroll
+    for (int k = 0; k <= NU + 1; ++k) {
+        const int idx = vmp ? m - OFF + k : ((m - OFF + k) & (half - 1));
+        cw[k] = cv[idx];
+        dw[k] = dv[idx];
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {  // pair m + p: window shifted by p
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            if ((u & 1) == 0) {
+                const int idx = OFF - u / 2 + p;
+                a0 += tp.h[u + NU - 1] * cw[idx];
+                b0 += tp.g[u + NU - 1] * dw[idx];
+            } else {
+                const int idx = OFF - (u - 1) / 2 + p;
+                a1 += tp.h[u + NU - 1] * cw[idx];
+                b1 += tp.g[u + NU - 1] * dw[idx];
+            }
+        }
+        o[2 * p] = a0 + b0;
+        o[2 * p + 1] = a1 + b1;
+    }
+}
+
 // Analysis: coarse and detail row mm of a length-n level from x[0:n].
 // Periodic: masked indices.  VMP: interior rows use the 2nu taps, the nu
 // edge rows per side the dense [A|B] / [Aw|Bw] rows (any level n >= 4nu).

@@ -545,8 +545,12 @@ cww_status build_tables(cww_op& op) {
     t.nc = 0;
     t.o_csyn = t.o_cana = int(tab.size());
     {
+        // Disabled: streaming the 32 KB matrix per vector through L1 costs more
+        // than the coarse levels it replaces (the kernels are L1-bound); kept
+        // for experiments (set CWW_DENSE_COARSE=1).
         const int Lc = 6;
-        if (op.r0 + 1 < Lc && int(op.j) > Lc) {
+        const char* dc = std::getenv("CWW_DENSE_COARSE");
+        if (dc && dc[0] == '1' && op.r0 + 1 < Lc && int(op.j) > Lc) {
             const int nc = 1 << Lc;
             std::vector<double> syn(size_t(nc * nc)), ana(size_t(nc * nc));
             for (int k = 0; k < nc; ++k) {

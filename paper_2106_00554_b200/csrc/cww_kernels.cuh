@@ -61,7 +61,7 @@ __device__ __forceinline__ void row_fwd(const double* trow, int sw, const double
     constexpr int B = G::B, H = G::H, CW = G::CW, NP = G::NP;
     double kap[2 * H + 1];
 #pragma unroll
-    for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(kp + l * S);
+    for (int l = 0; l <= 2 * H; ++l) kap[l] = kp[l * S];
 #pragma unroll
     for (int k = 0; k < B; ++k) z[k] = 0.0;
 #pragma unroll
@@ -90,7 +90,7 @@ __device__ __forceinline__ void row_adj_accum(double* trow, int sw, const double
     constexpr int B = G::B, H = G::H, CW = G::CW;
     double kap[2 * H + 1];
 #pragma unroll
-    for (int l = 0; l <= 2 * H; ++l) kap[l] = __ldg(kp + l * S);
+    for (int l = 0; l <= 2 * H; ++l) kap[l] = kp[l * S];
 #pragma unroll
     for (int e = 0; e < CW; ++e) {
         double acc = 0.0;
@@ -233,7 +233,19 @@ __device__ __forceinline__ void idwt_level_vec(const FiltSmem<NU>& F, const doub
     const int mlo = vmp ? (EL + 1) >> 1 : 0;
     const int mhi = vmp ? (n - EL) >> 1 : half;
     const Taps<NU> tp(F);
-    for (int m = mlo + t0; m < mhi; m += nthr) {
+    // two adjacent pairs (four samples) per thread share one window of nu+2
+    const int nq = (mhi - mlo) >> 1;
+    for (int qi = t0; qi < nq; qi += nthr) {
+        const int m = mlo + 2 * qi;
+        double o[4];
+        idwt_quad_inner<NU>(tp, cs, ds, n, m, vmp, o);
+        dst[2 * m] = o[0];
+        dst[2 * m + 1] = o[1];
+        dst[2 * m + 2] = o[2];
+        dst[2 * m + 3] = o[3];
+    }
+    if (((mhi - mlo) & 1) && t0 == 0) {
+        const int m = mhi - 1;
         double o0, o1;
         idwt_pair_inner<NU>(tp, cs, ds, n, m, vmp, o0, o1);
         dst[2 * m] = o0;
@@ -325,11 +337,25 @@ __host__ __device__ inline int small_tile_stride(int ars, int V) {
     return ((ars + 15) / 16) * 16 + (t & 15);
 }
 
+// shared copy of kap[2h+1][S] and the edge matrix em[S][2NP][2nu]
+__host__ __device__ inline int small_ke_size(int nu, int S) {
+    return (2 * nu - 1) * S + S * 2 * (2 * nu - 1) * 2 * nu;
+}
+
+template <int NU>
+__device__ __forceinline__ void stage_ke(double* ke, const double* tab, const Tables& t, int S, int tid,
+                                         int nt) {
+    const int nk = (2 * NU - 1) * S, ne = S * 2 * (2 * NU - 1) * 2 * NU;
+    for (int i = tid; i < nk; i += nt) ke[i] = tab[t.o_kap + i];
+    for (int i = tid; i < ne; i += nt) ke[nk + i] = tab[t.o_em + i];
+}
+
 template <int NU, int LOGB>
 inline long long small_smem_bytes(int V, int j, int q, bool adj, bool vf) {
     using G = Geo<NU, LOGB>;
     const int a = j - LOGB, A = 1 << a, S = 1 << q;
-    long long d = FiltSmem<NU>::SIZE + (long long)V * 2 * NU + (long long)V * S * 2 * G::NP;
+    long long d = FiltSmem<NU>::SIZE + small_ke_size(NU, S) + (long long)V * 2 * NU +
+                  (long long)V * S * 2 * G::NP;
     if (adj) {
         const int L = small_adj_lanes(A, V, vf);
         const int nslot = A / L > 0 ? A / L : 1;
@@ -360,18 +386,22 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
     const long long v0 = (long long)blockIdx.x * V;
     const int nv = (int)((p.nvec - v0) < V ? (p.nvec - v0) : V);
     double* filt = sm;
-    double* EV = filt + FiltSmem<NU>::SIZE;
+    double* KE = filt + FiltSmem<NU>::SIZE;  // kap | em
+    double* EV = KE + small_ke_size(NU, S);
     double* ES = EV + V * 2 * NU;
     double* X = ES + V * S * 2 * NP;
     double* C = X + V * M;
     double* T = C + (V * M >> 1);
     const int tst = small_tile_stride(A * RS, V);
     const int hM = M >> 1;
+    const double* KAP = KE;
+    const double* EM = KE + (2 * NU - 1) * S;
     // thread groups: G threads per vector (V divides NT)
     const int Gs = NT / V, gid = tid / Gs, gt = tid % Gs;
 
     PHASE(0);
     stage_filters<NU>(filt, p.tab, p.t, tid, NT);
+    stage_ke<NU>(KE, p.tab, p.t, S, tid, NT);
     if (p.in_block == 1 && M >= 2) {  // V vectors back to back: 16-byte copy
         const double2* blk = reinterpret_cast<const double2*>(p.in + p.lin.vbase(v0));
         const int tot2 = (nv * M) >> 1;
@@ -464,10 +494,10 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         }
         if (NU > 1) {  // es[v][s][pos] = sum_c em[s][pos][c] xi_edge[c]
             for (int f = gt; f < S * 2 * NP; f += Gs) {
-                const double* em = p.tab + p.t.o_em + f * 2 * NU;
+                const double* em = EM + f * 2 * NU;
                 double acc = 0.0;
 #pragma unroll
-                for (int c = 0; c < 2 * NU; ++c) acc += __ldg(em + c) * EV[v * 2 * NU + c];
+                for (int c = 0; c < 2 * NU; ++c) acc += em[c] * EV[v * 2 * NU + c];
                 ES[v * S * 2 * NP + f] = acc;
             }
         }
@@ -497,7 +527,7 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         if (v >= nv) continue;
         const double sg = (__popc(wlo) & 1) ? -1.0 : 1.0;  // popc(N) = popc(bitrev(N))
         double z[B];
-        row_fwd<NU, LOGB>(T + v * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S,
+        row_fwd<NU, LOGB>(T + v * tst + wlo * RS, wlo, KAP + s, S,
                           NU > 1 ? ES + (v * S + s) * 2 * NP : nullptr, sg, z);
         const unsigned rw = gray_inv((unsigned)wlo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
         row_store<LOGB>(p.out + p.lout.vbase(v0 + v) + p.lout.eoff((long long)s * M), p.lout, a, rw, z);
@@ -519,8 +549,11 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
     const int L = small_adj_lanes(A, V, vf);
     const int nslot = A / L > 0 ? A / L : 1;
     double* filt = sm;
-    double* EV = filt + FiltSmem<NU>::SIZE;  // unused here; keeps the layout of k_small_fwd
+    double* KE = filt + FiltSmem<NU>::SIZE;  // kap | em
+    double* EV = KE + small_ke_size(NU, S);  // unused here; keeps the layout of k_small_fwd
     double* W = EV + V * 2 * NU;              // [V][S][2NP]
+    const double* KAP = KE;
+    const double* EM = KE + (2 * NU - 1) * S;
     double* EPW = W + V * S * 2 * NP;         // [V][nslot][S][2NP]
     double* X = EPW + V * nslot * S * 2 * NP;
     double* C = X + V * M;
@@ -528,7 +561,10 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
     const int tst = small_tile_stride(A * RS, V);
     const int hM = M >> 1;
     const int Gs = NT / V, gid = tid / Gs, gt = tid % Gs;
+    PHASE(0);
     stage_filters<NU>(filt, p.tab, p.t, tid, NT);
+    stage_ke<NU>(KE, p.tab, p.t, S, tid, NT);
+    __syncthreads();
 
     // row stage: sequency-ordered load + H_B + correlation (+ edge partials)
     const int items = V * A;  // padded to V: the lane -> vector pattern is fixed
@@ -565,11 +601,13 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
                 seg_reduce_store_rt<R>(ev, lane, segbits, 2 * NP, live,
                                        EPW + ((v * nslot + slot) * S + s) * 2 * NP);
             }
-            if (act) row_adj_accum<NU, LOGB>(T + v * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S, y, s == 0);
+            if (act) row_adj_accum<NU, LOGB>(T + v * tst + wlo * RS, wlo, KAP + s, S, y, s == 0);
         }
     }
     __syncthreads();
+    PHASE(1);
     tile_hadamard<CW, RS>(T, nv, a, 0, a, tst, tid, NT);
+    PHASE(2);
     if (NU > 1) {  // W[v][s][pos] = sum over rows (fixed order)
         for (int f = tid; f < nv * S * 2 * NP; f += NT) {
             const int v = f / (S * 2 * NP), sp = f % (S * 2 * NP);
@@ -591,13 +629,22 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
         if (NU > 1 && (i < NU || i >= M - NU)) {
             const int c = i < NU ? i : NU + i - (M - NU);
             const double* wv = W + v * S * 2 * NP;
-            double e = 0.0;
-            for (int sp = 0; sp < S * 2 * NP; ++sp) e += __ldg(p.tab + p.t.o_em + sp * 2 * NU + c) * wv[sp];
-            val = e;
+            double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+            const int nsp = S * 2 * NP;  // multiple of 2; four independent chains
+            int sp = 0;
+            for (; sp + 4 <= nsp; sp += 4) {
+                e0 += EM[sp * 2 * NU + c] * wv[sp];
+                e1 += EM[(sp + 1) * 2 * NU + c] * wv[sp + 1];
+                e2 += EM[(sp + 2) * 2 * NU + c] * wv[sp + 2];
+                e3 += EM[(sp + 3) * 2 * NU + c] * wv[sp + 3];
+            }
+            for (; sp < nsp; ++sp) e0 += EM[sp * 2 * NU + c] * wv[sp];
+            val = (e0 + e1) + (e2 + e3);
         }
         X[o] = val;
     }
     __syncthreads();
+    PHASE(3);
     // DWT levels j .. r0+1 (wavelet.cpp:497-504) per vector group; the output
     // vector is staged in the (now free) tile area and stored block-wide.
     const FiltSmem<NU> F{filt};
@@ -641,6 +688,7 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
         }
     }
     __syncthreads();
+    PHASE(4);
     const double* res = dwt ? T : X;
     const int rst = dwt ? tst : M;
     for (int f = tid; f < V * M; f += NT) {
@@ -648,6 +696,8 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
         const int i = of ? f >> lV : f & (M - 1);
         if (v < nv) p.out[p.lout.at(v0 + v, i)] = res[v * rst + i];
     }
+    __syncthreads();
+    PHASE(5);
 }
 
 // ---------------------------------------------------------------------------
@@ -1059,9 +1109,18 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
         }
         if (NU > 1 && (pos < NU || pos >= M - NU)) {
             const int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
-            double e = 0.0;
-            for (int sp = 0; sp < S * 2 * NP; ++sp) e += __ldg(p.tab + p.t.o_em + sp * 2 * NU + c) * Wv[sp];
-            val = e;
+            const double* em = p.tab + p.t.o_em + c;
+            double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+            const int nsp = S * 2 * NP;
+            int sp = 0;
+            for (; sp + 4 <= nsp; sp += 4) {
+                e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
+                e1 += __ldg(em + (sp + 1) * 2 * NU) * Wv[sp + 1];
+                e2 += __ldg(em + (sp + 2) * 2 * NU) * Wv[sp + 2];
+                e3 += __ldg(em + (sp + 3) * 2 * NU) * Wv[sp + 3];
+            }
+            for (; sp < nsp; ++sp) e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
+            val = (e0 + e1) + (e2 + e3);
         }
         if (p.xo_is_output) ob[p.lout.eoff(pos)] = val;
         else xo[pos] = val;
