@@ -476,6 +476,67 @@ __device__ __forceinline__ void dwt_pair(const FiltSmem<NU>& F, const double* x,
     d = b;
 }
 
+// Asynchronous 8-byte global -> shared copy (LDGSTS): many loads in flight
+// per thread without register staging.
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ---- window geometry of the multilevel (pyramid) wavelet kernels ------------
+// Index ranges [lo, hi).  Periodic ranges are LOGICAL (may start below 0 or end
+// past the level length; entries are read modulo the length): periodic
+// synthesis and analysis are translation-equivariant, so a window never needs
+// to be clipped or collapsed.  VMP ranges are physical (clipped).
+struct Win {
+    int lo, hi;
+};
+
+// Coarse/detail window (level n/2) read by the synthesis of fine samples f of
+// level n (wavelet.cpp:447-483 in gather form).  VMP: the first/last 3nu-1
+// fine samples read coarse entries [0, 2nu) / [n/2-2nu, n/2) (dense edge
+// blocks); levels n < 8nu use the generic edge code on the whole level.
+__host__ __device__ inline Win syn_need(int nu, int n, Win f, bool vmp) {
+    const int half = n >> 1;
+    Win c{(f.lo - nu) >> 1, ((f.hi + nu - 2) >> 1) + 1};
+    if (!vmp) return c;
+    if (n < 8 * nu) return Win{0, half};
+    const int EL = 3 * nu - 1, CI = 2 * nu;
+    if (c.lo < 0) c.lo = 0;
+    if (c.hi > half) c.hi = half;
+    if (f.lo < EL) {
+        c.lo = 0;
+        if (c.hi < CI) c.hi = CI;
+    }
+    if (f.hi > n - EL) {
+        c.hi = half;
+        if (c.lo > half - CI) c.lo = half - CI;
+    }
+    return c;
+}
+
+// Fine window (level n) read by the analysis of coarse/detail rows r of a
+// length-n level (wavelet.cpp:369-385, 403-445).  VMP edge rows (the first /
+// last nu) read the first / last 3nu-1 fine samples.
+__host__ __device__ inline Win ana_need(int nu, int n, Win r, bool vmp) {
+    const int half = n >> 1;
+    Win w{2 * r.lo - nu + 1, 2 * r.hi + nu - 1};
+    if (!vmp) return w;
+    const int EL = 3 * nu - 1;
+    if (w.lo < 0) w.lo = 0;
+    if (w.hi > n) w.hi = n;
+    if (r.lo < nu) {
+        w.lo = 0;
+        if (w.hi < EL) w.hi = EL;
+    }
+    if (r.hi > half - nu) {
+        w.hi = n;
+        if (w.lo > n - EL) w.lo = n - EL;
+    }
+    return w;
+}
+
 // gray^-1(bitrev_5(nl) << a): gray^-1 is linear over XOR and
 // gray^-1(x << a) = (gray^-1(x) << a) | (parity(x) ? 2^a - 1 : 0).
 __device__ __forceinline__ unsigned gray_inv_hi(int nl, int logb, int a) {

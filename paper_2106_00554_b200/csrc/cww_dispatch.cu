@@ -13,7 +13,8 @@ namespace cww {
     cudaError_t launch_small_nu##N(const SmallArgs&, bool, cudaStream_t);           \
     long long small_smem_nu##N(int, int, int, bool, bool);                                \
     cudaError_t launch_large_nu##N(int, const LargeArgs&, cudaStream_t);            \
-    cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);
+    cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);                    \
+    cudaError_t launch_pyr_nu##N(bool, const PyrArgs&, cudaStream_t);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6)
 #undef DECL
 
@@ -55,13 +56,20 @@ cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st) {
     return cudaErrorInvalidValue;
 }
 
-long long large_nslot(int q, int j, int kl, int ng) {
-    (void)q;
+cudaError_t launch_pyr(int nu, bool analysis, const PyrArgs& a, cudaStream_t st) {
+#define C(N) launch_pyr_nu##N(analysis, a, st)
+    SWITCH_NU(nu, C)
+#undef C
+    return cudaErrorInvalidValue;
+}
+
+long long large_nslot(int nu, int q, int j, int kl, int ng) {
     const int nt = 256;
     const int kh = (j - kLogB) - kl, R1 = 1 << kl, R2 = 1 << kh;
+    if (large_cta_red(nu, q)) return R1 / ng;  // one slot per adj2 CTA
     int items = ng * R2;
     int iters = (items + nt - 1) / nt;
-    return (long long)(R1 / ng) * (nt / 32) * iters;
+    return (long long)(R1 / ng) * (nt / 32) * iters;  // one slot per (CTA, iteration, warp)
 }
 
 

@@ -701,6 +701,25 @@ cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out
     return CWW_OK;
 }
 
+// chunk (log2 fine samples per CTA) of the synthesis / analysis pyramids
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : dflt;
+}
+const int kPyrSynLog = env_int("CWW_PYR_SYN_LOG", 12);
+const int kPyrAnaLog = env_int("CWW_PYR_ANA_LOG", 11);
+const int kPyrSynBot = env_int("CWW_PYR_SYN_BOT", 10);  // coarse levels <= this: separate kernel
+
+cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
+    cww::PyrArgs y{};
+    y.tab = op->d_tab;
+    y.t = op->tabs;
+    y.nvec = nvec;
+    y.vmp = op->vmp;
+    y.r0 = op->r0;
+    return y;
+}
+
 // ---- large path (1D, M > 2^13) ----
 struct LargePlan {
     int kl, ng;
@@ -722,9 +741,8 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     const int nu = op->nu, NP = 2 * nu - 1, CW = 32 + 2 * (nu - 1);
     const long long A = M >> cww::kLogB;
     const auto pl = large_plan(op->j);
-    const int Lc = std::min<int>(int(op->j) - 1, cww::kSmallMaxLog);  // coarse levels in one CTA
     const bool idwt = op->d.use_idwt && op->r0 < int(op->j);
-    const long long nslot = cww::large_nslot(int(op->q), int(op->j), pl.kl, pl.ng);
+    const long long nslot = cww::large_nslot(nu, int(op->q), int(op->j), pl.kl, pl.ng);
     DevBuf w0, w1, G, ev, epw;
     CUDA_TRY(G.alloc(size_t(nvec * A * CW), st));
     CUDA_TRY(ev.alloc(size_t(nvec * 2 * nu), st));
@@ -749,15 +767,9 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     a.ev = ev.p;
     a.epw = epw.p;
     a.nslot = nslot;
+    a.cta_red = cww::large_cta_red(nu, int(op->q)) ? 1 : 0;
     a.out = out;
     a.lout = lout;
-
-    cww::WavArgs w{};
-    w.tab = op->d_tab;
-    w.t = op->tabs;
-    w.nvec = nvec;
-    w.r0 = op->r0;
-    w.vmp = op->vmp;
 
     a.r0 = op->r0;
     a.use_idwt = op->d.use_idwt;
@@ -765,42 +777,42 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     if (!adj) {
         const double* xi = nullptr;
         if (idwt) {
-            // coarse levels r0+1..Lc in shared memory, then one pass per fine level
-            int lc = std::max(Lc, op->r0);
-            w.kind = 0;
-            w.lev = lc;
-            w.inverse = 1;
-            w.src = in;
-            w.ls = lin;
-            w.sv0 = 0;
-            w.dst = w0.p;
-            w.dst_vs = M;
-            {
-                Prof pr("wav_coarse", st);
-                CUDA_TRY(cww::launch_wav(nu, w, st));
+            // all synthesis levels r0+1..j in one launch (per-CTA window cones)
+            cww::PyrArgs y = pyr_args(op, nvec);
+            y.top = int(op->j);
+            y.bot = std::max(op->r0, std::min(kPyrSynBot, int(op->j) - 1));
+            y.cb = std::min(int(op->j), kPyrSynLog);
+            y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum);
+            y.x = in;
+            y.lx = lin;
+            y.src_is_x = 1;
+            if (y.bot > op->r0) {  // coarse levels r0+1..bot: one CTA per vector
+                cww::WavArgs w{};
+                w.tab = op->d_tab;
+                w.t = op->tabs;
+                w.nvec = nvec;
+                w.r0 = op->r0;
+                w.vmp = op->vmp;
+                w.kind = 0;
+                w.lev = y.bot;
+                w.inverse = 1;
+                w.src = in;
+                w.ls = lin;
+                w.dst = w1.p;
+                w.dst_vs = 1ll << y.bot;
+                {
+                    Prof pr("wav_coarse", st);
+                    CUDA_TRY(cww::launch_wav(nu, w, st));
+                }
+                y.src_is_x = 0;
+                y.src = w1.p;
+                y.src_vs = 1ll << y.bot;
             }
-            double* cur = w0.p;
-            double* nxt = w1.p;
-            for (int lev = lc + 1; lev <= int(op->j); ++lev) {
-                cww::WavArgs l{};
-                l.kind = 1;
-                l.tab = op->d_tab;
-                l.t = op->tabs;
-                l.nvec = nvec;
-                l.lev = lev;
-                l.vmp = op->vmp;
-                l.src = cur;
-                l.src_vs = M;
-                l.x = in;
-                l.lx = lin;
-                l.xv0 = 0;
-                l.dst = nxt;
-                l.dst_vs = M;
-                Prof pr("idwt_level", st);
-                CUDA_TRY(cww::launch_wav(nu, l, st));
-                std::swap(cur, nxt);
-            }
-            xi = cur;
+            y.out = w0.p;
+            y.out_vs = M;
+            Prof pr("idwt_pyr", st);
+            CUDA_TRY(cww::launch_pyr(nu, false, y, st));
+            xi = w0.p;
         }
         a.xi = xi;
         a.xi_vs = M;
@@ -828,38 +840,46 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
         CUDA_TRY(cww::launch_large(nu, 3, a, st));
     }
     if (!idwt) return CWW_OK;
-    int lc = std::max(Lc, op->r0);
-    double* cur = w0.p;
-    double* nxt = w1.p;
-    for (int lev = int(op->j); lev > lc; --lev) {
-        cww::WavArgs l{};
-        l.kind = 2;
-        l.tab = op->d_tab;
-        l.t = op->tabs;
-        l.nvec = nvec;
-        l.lev = lev;
-        l.vmp = op->vmp;
-        l.src = cur;
-        l.src_vs = M;
-        l.dst = nxt;
-        l.dst_vs = M;
-        l.y = out;
-        l.ly = lout;
-        l.yv0 = 0;
-        Prof pr("dwt_level", st);
-        CUDA_TRY(cww::launch_wav(nu, l, st));
-        std::swap(cur, nxt);
+    // analysis: pyramids of up to d steps (halo ~ (2nu-2) 2^d <= chunk/8); the
+    // last one finishes the coarse levels in its last CTA per vector
+    unsigned* cnt = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cnt), size_t(nvec) * sizeof(unsigned), st));
+    struct CntFree {
+        unsigned* p;
+        cudaStream_t s;
+        ~CntFree() { cudaFreeAsync(p, s); }
+    } cnt_free{cnt, st};
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(nvec) * sizeof(unsigned), st));
+    int T = int(op->j);
+    const double* src = w0.p;
+    double* sink[2] = {w1.p, w0.p};
+    for (int it = 0;; ++it) {
+        const int cb = std::min(T, kPyrAnaLog);
+        int d = 1;
+        while (d + 1 <= T - op->r0 && (2 * nu - 2) * ((1 << (d + 1)) - 1) <= (1 << cb) / 8) ++d;
+        const int bot = std::max({op->r0, T - d, T - cb});
+        const bool tail = bot > op->r0 && bot <= cww::kSmallMaxLog;
+        cww::PyrArgs y = pyr_args(op, nvec);
+        y.top = T;
+        y.bot = bot;
+        y.cb = cb;
+        y.tail = tail ? 1 : 0;
+        y.wmax = cww::pyr_wmax_ana(nu, T, bot, cb, op->vmp != 0);
+        y.src = src;
+        y.src_vs = M;
+        y.y = out;
+        y.ly = lout;
+        y.cws = bot == op->r0 ? nullptr : sink[it & 1];
+        y.cws_vs = M;
+        y.cnt = cnt;
+        {
+            Prof pr("dwt_pyr", st);
+            CUDA_TRY(cww::launch_pyr(nu, true, y, st));
+        }
+        if (bot == op->r0 || tail) break;
+        T = bot;
+        src = y.cws;
     }
-    w.kind = 0;
-    w.lev = lc;
-    w.inverse = 0;
-    w.src = cur;
-    w.src_vs = M;
-    w.dst = out;
-    w.ld = lout;
-    w.dv0 = 0;
-    Prof pr("wav_coarse", st);
-    CUDA_TRY(cww::launch_wav(nu, w, st));
     return CWW_OK;
 }
 

@@ -177,8 +177,9 @@ __device__ __forceinline__ int seg_transpose_reduce(double* v, int lane, int& cn
 // Reduce the edge values ev[R] over a lane segment and store the sums
 // dst[idx] (idx < nval) from the leader lanes; SEG must be compile-time so
 // every register index is static.
-template <int R, unsigned SEG>
-__device__ __forceinline__ void seg_reduce_store(double* ev, int lane, int nval, bool live, double* dst) {
+template <int R, unsigned SEG, bool ACC = false>
+__device__ __forceinline__ void seg_reduce_store(double* ev, int lane, int nval, bool live, double* dst,
+                                                 bool acc = false) {
     int cnt;
     bool leader;
     const int base = seg_transpose_reduce<R, SEG>(ev, lane, cnt, leader);
@@ -186,7 +187,10 @@ __device__ __forceinline__ void seg_reduce_store(double* ev, int lane, int nval,
 #pragma unroll
         for (int k2 = 0; k2 < R; ++k2) {
             const int idx = base * cnt + k2;
-            if (k2 < cnt && idx < nval) dst[idx] = ev[k2];
+            if (k2 < cnt && idx < nval) {
+                if (ACC && acc) dst[idx] += ev[k2];
+                else dst[idx] = ev[k2];
+            }
         }
     }
 }
@@ -806,32 +810,6 @@ __global__ void __launch_bounds__(256) k_wav_coarse(const double* tab, Tables t,
 // own pyramid of level windows straight from x, coarse to fine)
 // ---------------------------------------------------------------------------
 
-// Coarse-index range [clo, chi) of level n/2 that the synthesis of fine
-// samples [lo, hi) of level n reads (interior taps; VMP edge samples read the
-// first/last 2nu coarse entries).  Periodic windows may start below 0 / end
-// past n/2: they are read modulo n/2.
-template <int NU>
-__device__ __forceinline__ void idwt_need(int n, int lo, int hi, bool vmp, int& clo, int& chi) {
-    const int half = n >> 1;
-    clo = (lo - NU) >> 1;                    // floor((lo - nu) / 2)
-    chi = ((hi - 1 + NU - 1) >> 1) + 1;      // floor((hi - 1 + nu - 1) / 2) + 1
-    if (vmp) {
-        constexpr int EL = FiltSmem<NU>::EL, CI = FiltSmem<NU>::CI;
-        if (n < 8 * NU) {  // generic coarse levels: whole level
-            clo = 0;
-            chi = half;
-            return;
-        }
-        if (clo < 0) clo = 0;
-        if (chi > half) chi = half;
-        if (lo < EL && chi < CI) chi = CI;
-        if (hi > n - EL && clo > half - CI) clo = half - CI;
-    } else if (chi - clo >= half) {  // the window wraps onto itself: whole level
-        clo = 0;
-        chi = half;
-    }
-}
-
 // Fine samples [lo, hi) of level n from windows cw = c[clo .. chi), dw =
 // d[clo .. chi) (same range; periodic: entries taken modulo n/2), written to
 // out[i - lo] (or, when put != nullptr, handed to put(i, value)).
@@ -884,13 +862,243 @@ __device__ __forceinline__ void idwt_window(const FiltSmem<NU>& F, const Taps<NU
             for (int q = 0; q < NU; ++q) {
                 const int u = -NU + 1 + 2 * q + par;
                 const int mm = (i - u) >> 1;  // logical index, inside the window
-                acc += tp.h[u + NU - 1] * cv[mm] + tp.g[u + NU - 1] * dv[mm];
+                acc += F.h(u) * cv[mm] + F.g(u) * dv[mm];  // runtime tap index: smem, not registers
             }
             put(i, acc);
         } else {
             put(i, idwt_one<NU>(F, cv, dv, n, i, true));
         }
     }
+}
+
+// Analysis rows mm of a length-n level from a window addressed by LOGICAL
+// fine index (x = window - window.lo): periodic rows need no masking.
+template <int NU>
+__device__ __forceinline__ void dwt_pair_log(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* x,
+                                             int n, int mm, bool vmp, double& c, double& d) {
+    const int half = n >> 1;
+    if (!vmp || (mm >= NU && mm < half - NU)) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            const double xv = x[2 * mm + u];
+            if (u & 1) {
+                a1 += tp.h[u + NU - 1] * xv;
+                b1 += tp.g[u + NU - 1] * xv;
+            } else {
+                a0 += tp.h[u + NU - 1] * xv;
+                b0 += tp.g[u + NU - 1] * xv;
+            }
+        }
+        c = a0 + a1;
+        d = b0 + b1;
+        return;
+    }
+    constexpr int EL = FiltSmem<NU>::EL;
+    const int side = mm < NU ? 0 : 1;
+    const int m = side ? half - 1 - mm : mm;
+    const double* ra = F.ana(side, 0, m);
+    const double* rb = F.ana(side, 1, m);
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k < EL; ++k) {
+        const double xv = x[side ? n - 1 - k : k];
+        a += ra[k] * xv;
+        b += rb[k] * xv;
+    }
+    c = a;
+    d = b;
+}
+
+// ---------------------------------------------------------------------------
+// large path: multilevel wavelet pyramids (one launch for many levels)
+// ---------------------------------------------------------------------------
+// Synthesis: CTA (c, v) produces the fine samples [c*2^cb, (c+1)*2^cb) of
+// level `top` for vector v.  It derives its cone of windows down to level
+// `bot` (syn_need), loads the level-bot coarse window and each level's detail
+// window, and synthesises upward in shared memory; only the top level is
+// written.  The cone shrinks geometrically, so the redundant work at the
+// coarse levels is a few samples per CTA and no inter-CTA exchange is needed.
+template <int NU, int NT>
+__global__ void __launch_bounds__(NT) k_idwt_pyr(PyrArgs p) {
+    extern __shared__ double sm[];
+    constexpr int FS = FiltSmem<NU>::SIZE;
+    double* filt = sm;
+    int* wlo = reinterpret_cast<int*>(sm + FS);
+    int* whi = wlo + 32;
+    int* doff = wlo + 64;
+    double* P = sm + FS + 48;
+    double* Q = P + p.wmax;
+    double* D = Q + p.wmax;  // every level's detail window, prefetched at once
+    const int tid = threadIdx.x, lane = tid & 31, c = blockIdx.x, v = blockIdx.y;
+    const bool vmp = p.vmp != 0;
+    for (int i = tid; i < FS; i += NT) filt[i] = p.tab[p.t.o_h + i];
+    if (tid == 0) {
+        Win f{c << p.cb, (c + 1) << p.cb};
+        for (int lev = p.top; lev >= p.bot; --lev) {
+            wlo[lev] = f.lo;
+            whi[lev] = f.hi;
+            if (lev > p.bot) {
+                f = syn_need(NU, 1 << lev, f, vmp);
+                if (f.hi - f.lo > p.wmax) __trap();
+            }
+        }
+        int off = 0;
+        for (int lev = p.bot + 1; lev <= p.top; ++lev) {
+            doff[lev] = off;
+            off += whi[lev - 1] - wlo[lev - 1];
+        }
+        if (off > p.dsum) __trap();
+    }
+    __syncthreads();
+    const double* xb = p.x + p.lx.vbase(p.xv0 + v);
+    const double* cs = p.src_is_x ? xb : p.src + v * p.src_vs;
+    {
+        const int lo = wlo[p.bot], w = whi[p.bot] - lo, hb = 1 << p.bot;
+        for (int t = tid; t < w; t += NT) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
+    }
+    for (int lev = p.bot + 1; lev <= p.top; ++lev) {  // details of level lev (half = 2^(lev-1))
+        const int lo = wlo[lev - 1], w = whi[lev - 1] - lo, hf = 1 << (lev - 1);
+        const double* ds = xb + hf;
+        double* dd = D + doff[lev];
+        for (int t = tid; t < w; t += NT) cp_async8(dd + t, ds + (vmp ? lo + t : ((lo + t) & (hf - 1))));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const FiltSmem<NU> F{filt};
+    const Taps<NU> tp(F);
+    double* ob = p.out + v * p.out_vs;
+    bool warp_mode = false;
+    for (int lev = p.bot + 1; lev <= p.top; ++lev) {
+        const int n = 1 << lev;
+        const int clo = wlo[lev - 1], lo = wlo[lev], hi = whi[lev];
+        const double* dw = D + doff[lev];
+        if (lev < p.top && hi - lo <= 64) {  // small level: one warp, no CTA barrier
+            warp_mode = true;
+            if (tid < 32) {
+                double* q = Q - lo;
+                idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32,
+                                [&](int i, double val) { q[i] = val; });
+                __syncwarp();
+            }
+        } else {
+            if (warp_mode) __syncthreads();
+            warp_mode = false;
+            if (lev < p.top) {
+                double* q = Q - lo;
+                idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, tid, NT,
+                                [&](int i, double val) { q[i] = val; });
+                __syncthreads();
+            } else {
+                idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, tid, NT,
+                                [&](int i, double val) { ob[i] = val; });
+            }
+        }
+        double* t0 = P;
+        P = Q;
+        Q = t0;
+    }
+}
+
+// Analysis: CTA (c, v) owns rows [c, c+1) * 2^(s-1-lognc) of every step s =
+// top..bot+1 (input length 2^s).  It loads the fine window its cone needs
+// (ana_need; the halo grows ~ (2nu-2) 2^(top-bot), chosen by the host to stay
+// ~10% of the chunk), computes the coarse rows of the cone level by level in
+// shared memory and writes its own detail rows and its own level-bot coarse
+// rows (workspace, or the output when bot = r0).  With `tail`, the last CTA of
+// each vector to finish (atomic ticket) runs the remaining coarse levels
+// bot..r0+1 on the whole level-bot vector, so the coarse transform needs no
+// extra launch.
+template <int NU, int NT>
+__global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
+    extern __shared__ double sm[];
+    constexpr int FS = FiltSmem<NU>::SIZE;
+    double* filt = sm;
+    int* rlo = reinterpret_cast<int*>(sm + FS);
+    int* rhi = rlo + 32;
+    int* xlo = rlo + 64;
+    int* xhi = rlo + 96;
+    double* buf = sm + FS + 64;
+    __shared__ unsigned s_last;
+    const int tid = threadIdx.x, c = blockIdx.x, v = blockIdx.y;
+    const bool vmp = p.vmp != 0;
+    const int lnc = p.top - p.cb;  // log2(chunks per vector)
+    for (int i = tid; i < FS; i += NT) filt[i] = p.tab[p.t.o_h + i];
+    if (tid == 0) {
+        Win r{c << (p.bot - lnc), (c + 1) << (p.bot - lnc)};
+        for (int s = p.bot + 1; s <= p.top; ++s) {
+            const Win w = ana_need(NU, 1 << s, r, vmp);
+            rlo[s] = r.lo;
+            rhi[s] = r.hi;
+            xlo[s] = w.lo;
+            xhi[s] = w.hi;
+            if (w.hi - w.lo > p.wmax) __trap();
+            r = w;
+        }
+    }
+    __syncthreads();
+    double* X = buf;
+    double* Y = buf + p.wmax;
+    {
+        const double* src = p.src + v * p.src_vs;
+        const int lo = xlo[p.top], w = xhi[p.top] - lo, n = 1 << p.top;
+        for (int t = tid; t < w; t += NT) cp_async8(X + t, src + (vmp ? lo + t : ((lo + t) & (n - 1))));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const FiltSmem<NU> F{filt};
+    const Taps<NU> tp(F);
+    for (int s = p.top; s > p.bot; --s) {
+        const int n = 1 << s, half = n >> 1;
+        const int lo = rlo[s], hi = rhi[s];
+        const int plo = c << (s - 1 - lnc), phi = (c + 1) << (s - 1 - lnc);
+        const double* xv = X - xlo[s];
+        double* yv = Y - lo;
+        const bool last = s == p.bot + 1;
+        for (int mm = lo + tid; mm < hi; mm += NT) {
+            double cc, dd;
+            dwt_pair_log<NU>(F, tp, xv, n, mm, vmp, cc, dd);
+            if (!last) yv[mm] = cc;
+            if (mm >= plo && mm < phi) {
+                p.y[p.ly.at(p.yv0 + v, half + mm)] = dd;
+                if (last) {
+                    if (p.cws) p.cws[v * p.cws_vs + mm] = cc;
+                    else p.y[p.ly.at(p.yv0 + v, mm)] = cc;
+                }
+            }
+        }
+        __syncthreads();
+        double* t0 = X;
+        X = Y;
+        Y = t0;
+    }
+    if (!p.tail) return;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(p.cnt + v, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int n0 = 1 << p.bot;
+    double* cur = buf;
+    double* nxt = buf + n0;
+    for (int i = tid; i < n0; i += NT) cur[i] = __ldcg(p.cws + v * p.cws_vs + i);
+    __syncthreads();
+    for (int lev = p.bot; lev > p.r0; --lev) {
+        const int m = 1 << lev, half = m >> 1;
+        for (int k = tid; k < half; k += NT) {
+            double cc, dd;
+            dwt_pair<NU>(F, cur, m, k, vmp, cc, dd);
+            p.y[p.ly.at(p.yv0 + v, half + k)] = dd;
+            nxt[k] = cc;
+        }
+        __syncthreads();
+        double* t0 = cur;
+        cur = nxt;
+        nxt = t0;
+    }
+    for (int i = tid; i < (1 << p.r0); i += NT) p.y[p.ly.at(p.yv0 + v, i)] = cur[i];
+    if (tid == 0) p.cnt[v] = 0u;  // ticket ready for the next launch
 }
 
 // ---------------------------------------------------------------------------
@@ -913,13 +1121,12 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     for (int f = tid; f < R1 * CW; f += NT) {
         const int rl = f / CW, e = f % CW;  // logical local row K_lo
         const long long pos = (long long)(chunk * R1 + rl) * B + e - H;
-        double val = 0.0;
-        if (pos >= 0 && pos < M) {
-            val = p.xi_is_input ? __ldg(p.in + p.lin.at(p.v0 + v, pos)) : __ldg(xi + pos);
-            if (NU > 1 && (pos < NU || pos >= M - NU)) val = 0.0;
-        }
         const int ph = (int)brev_bits((unsigned)rl, kl);
-        T[tile_idx(ph, e, RS, ph)] = val;
+        double* dst = T + tile_idx(ph, e, RS, ph);
+        if (pos >= 0 && pos < M && !(NU > 1 && (pos < NU || pos >= M - NU)))
+            cp_async8(dst, p.xi_is_input ? p.in + p.lin.at(p.v0 + v, pos) : xi + pos);
+        else
+            *dst = 0.0;  // outside the vector, or an edge position (edge terms)
     }
     if (NU > 1 && tid < 2 * NU) {  // raw edge values (first / last chunk)
         const int c = tid;
@@ -927,6 +1134,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
         if ((int)((pos / B) / R1) == chunk)
             p.ev[(long long)v * 2 * NU + c] = p.xi_is_input ? p.in[p.lin.at(p.v0 + v, pos)] : xi[pos];
     }
+    cp_async_wait_all();
     __syncthreads();
     tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
@@ -954,7 +1162,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
         const int e = f % CW, rest = f / CW;
         const int ng = rest % NG, khi = rest / NG;
         const int ph = (int)brev_bits((unsigned)khi, kh);
-        T[ng * tst + tile_idx(ph, e, RS, ph)] = __ldg(g + ((long long)khi * R1 + rho0 + ng) * CW + e);
+        cp_async8(T + ng * tst + tile_idx(ph, e, RS, ph), g + ((long long)khi * R1 + rho0 + ng) * CW + e);
     }
     if (NU > 1) {
         for (int f = tid; f < S * 2 * NP; f += NT) {
@@ -965,6 +1173,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
             ES[f] = acc;
         }
     }
+    cp_async_wait_all();
     __syncthreads();
     tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
     double* ob = p.out + p.lout.vbase(p.v0 + v);
@@ -1000,6 +1209,8 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
     const int tst = R2 * RS;
     const int items = NG * R2;
     const int iters = (items + NT - 1) / NT;
+    const int FE = S * 2 * NP;                     // edge sums per vector
+    double* red = sm + NG * tst;                   // [NT/32 warps][FE]
     const double* ib = p.in + p.lin.vbase(p.v0 + v);
     for (int it = 0; it < iters; ++it) {
         const int w = tid + it * NT;
@@ -1021,13 +1232,25 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 #pragma unroll
                 for (int i = 0; i < R; ++i)
                     ev[i] = (act && i < 2 * NP) ? (i < NP ? y[i] : sg * y[B - NP + (i - NP)]) : 0.0;
-                const long long slot = (long long)blockIdx.x * ((NT / 32) * iters) + it * (NT / 32) + (tid >> 5);
-                seg_reduce_store<R, 31u>(ev, lane, 2 * NP, true, p.epw + (((long long)v * p.nslot + slot) * S + s) * 2 * NP);
+                if (p.cta_red) {
+                    seg_reduce_store<R, 31u, true>(ev, lane, 2 * NP, true, red + (tid >> 5) * FE + s * 2 * NP, it > 0);
+                } else {
+                    const long long slot = (long long)blockIdx.x * ((NT / 32) * iters) + it * (NT / 32) + (tid >> 5);
+                    seg_reduce_store<R, 31u>(ev, lane, 2 * NP, true, p.epw + (((long long)v * p.nslot + slot) * S + s) * 2 * NP);
+                }
             }
             if (act) row_adj_accum<NU, kLogB>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S, y, s == 0);
         }
     }
     __syncthreads();
+    if (NU > 1 && p.cta_red) {  // one slot per CTA: the warps' sums in a fixed order
+        for (int f = tid; f < FE; f += NT) {
+            double acc = 0.0;
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) acc += red[w * FE + f];
+            p.epw[((long long)v * p.nslot + blockIdx.x) * FE + f] = acc;
+        }
+    }
     tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
     // physical row ph of sub-tile ng is logical K_hi = bitrev_kh(ph)
     double* g = p.G + (long long)v * A * CW;
@@ -1048,38 +1271,75 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
     const int kl = p.kl, R1 = 1 << kl;
     const int chunk = blockIdx.x, v = blockIdx.y;
+    const int FE = S * 2 * NP;
     double* Wv = sm;                 // [S][2NP]
-    double* nb = Wv + S * 2 * NP;    // [2][H]: neighbour-row halo sums
+    double* nb = Wv + FE;            // [2][H]: neighbour-row halo sums
     double* T = nb + 2 * NU;
+    double* red = T + R1 * RS;       // reduction scratch: [NT/32][2H] and [NT/FE][FE]
     const double* g = p.G + (long long)v * A * CW;
     for (int f = tid; f < R1 * CW; f += NT) {
         const int ph = f / CW, e = f % CW;
-        T[tile_idx(ph, e, RS, ph)] = __ldg(g + ((long long)chunk * R1 + ph) * CW + e);
+        cp_async8(T + tile_idx(ph, e, RS, ph), g + ((long long)chunk * R1 + ph) * CW + e);
     }
     // halo contributions from the neighbouring chunks' boundary rows (sums over
     // the physical rows rho of their Hadamard rows; popc is bit-reversal invariant):
     //   previous chunk, last logical row:  sum_rho (-1)^popc(rho) G[(c-1)R1+rho][B+H+k]
     //   next chunk, first logical row:     sum_rho G[(c+1)R1+rho][k]
-    if (tid < 2 * H) {
-        const int side = tid / H, k = tid % H;
-        double acc = 0.0;
-        if (side == 0 && chunk > 0) {
-            for (int nl = 0; nl < R1; ++nl) {
-                const double val = g[((long long)(chunk - 1) * R1 + nl) * CW + B + H + k];
-                acc += (__popc(nl) & 1) ? -val : val;
+    // one row per thread, then a fixed-order warp/CTA reduction
+    if (NU > 1) {
+        double hs[2 * H > 0 ? 2 * H : 1];
+        const bool prev = chunk > 0, next = (chunk + 1) * R1 < A;
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+            double a0 = 0.0, a1 = 0.0;
+            for (int nl = tid; nl < R1; nl += NT) {
+                if (prev) {
+                    const double val = __ldg(g + ((long long)(chunk - 1) * R1 + nl) * CW + B + H + k);
+                    a0 += (__popc(nl) & 1) ? -val : val;
+                }
+                if (next) a1 += __ldg(g + ((long long)(chunk + 1) * R1 + nl) * CW + k);
             }
-        } else if (side == 1 && (chunk + 1) * R1 < A) {
-            for (int nl = 0; nl < R1; ++nl) acc += g[((long long)(chunk + 1) * R1 + nl) * CW + k];
+            hs[k] = a0;
+            hs[H + k] = a1;
         }
-        nb[side * H + k] = acc;
+#pragma unroll
+        for (int k = 0; k < 2 * H; ++k)
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) hs[k] += __shfl_xor_sync(0xffffffffu, hs[k], off);
+        if ((tid & 31) == 0) {
+#pragma unroll
+            for (int k = 0; k < 2 * H; ++k) red[(tid >> 5) * 2 * H + k] = hs[k];
+        }
     }
     const bool has_edge = NU > 1 && (chunk == 0 || (chunk + 1) * R1 >= A);
-    if (has_edge) {
-        for (int f = tid; f < S * 2 * NP; f += NT) {
-            double acc = 0.0;
-            for (long long sl = 0; sl < p.nslot; ++sl) acc += p.epw[((long long)v * p.nslot + sl) * S * 2 * NP + f];
-            Wv[f] = acc;
+    double* red2 = red + (NT / 32) * 2 * NU;
+    const int nr = FE <= NT ? NT / FE : 1;  // slot lanes per edge sum
+    for (int idx = tid; has_edge && idx < nr * FE; idx += NT) {
+        const int f = idx % FE, r = idx / FE;
+        const double* e0 = p.epw + (long long)v * p.nslot * FE + f;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        long long sl = r;
+        for (; sl + 3 * nr < p.nslot; sl += 4 * nr) {
+            a0 += e0[sl * FE];
+            a1 += e0[(sl + nr) * FE];
+            a2 += e0[(sl + 2 * nr) * FE];
+            a3 += e0[(sl + 3 * nr) * FE];
         }
+        for (; sl < p.nslot; sl += nr) a0 += e0[sl * FE];
+        red2[r * FE + f] = (a0 + a1) + (a2 + a3);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (NU > 1 && tid < 2 * H) {
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) acc += red[w * 2 * H + tid];
+        nb[tid] = acc;
+    }
+    for (int f = tid; has_edge && f < FE; f += NT) {
+        double acc = 0.0;
+        for (int r = 0; r < nr; ++r) acc += red2[r * FE + f];
+        Wv[f] = acc;
     }
     __syncthreads();
     tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);

@@ -43,6 +43,7 @@ struct LargeArgs {
     // adjoint edge partial sums: [nvec][nslot][S][2(2nu-1)]
     double* epw;
     long long nslot;
+    int cta_red;  // 1: adj2 reduces its warps' edge sums in smem (one slot per CTA)
     // outputs
     double* out;
     Layout lout;
@@ -74,10 +75,74 @@ struct WavArgs {
     long long yv0;
 };
 
+// Multilevel wavelet pyramids (large path).  Synthesis: levels bot+1..top,
+// coarse c_bot from src (or the op input x when src_is_x), details from x, top
+// level to out.  Analysis: steps top..bot+1 from src (fine level top), details
+// to y, coarse c_bot to cws (or y when cws == nullptr); tail: the last CTA per
+// vector runs levels bot..r0+1 (cnt: one zeroed ticket per vector).
+struct PyrArgs {
+    const double* tab;
+    Tables t;
+    long long nvec;
+    int vmp, top, bot, cb, r0, tail;
+    int wmax;  // window buffer length (doubles), from pyr_wmax_*
+    int dsum;  // synthesis: total detail-window length over all levels
+    const double* x;
+    Layout lx;
+    long long xv0;
+    const double* src;
+    long long src_vs;
+    int src_is_x;
+    double* out;
+    long long out_vs;
+    double* y;
+    Layout ly;
+    long long yv0;
+    double* cws;
+    long long cws_vs;
+    unsigned* cnt;
+};
+
+cudaError_t launch_pyr(int nu, bool analysis, const PyrArgs& a, cudaStream_t st);
+
+// Largest window (over all CTAs and levels) of a synthesis pyramid producing
+// chunks of 2^cb samples of level top from level bot.
+// Also returns the largest total detail-window length of one CTA (dsum).
+inline int pyr_wmax_syn(int nu, int top, int bot, int cb, bool vmp, int* dsum) {
+    int wm = 1, ds = 1;
+    for (long long c = 0; c < (1ll << (top - cb)); ++c) {
+        Win f{int(c << cb), int((c + 1) << cb)};
+        int sum = 0;
+        for (int lev = top; lev > bot; --lev) {
+            f = syn_need(nu, 1 << lev, f, vmp);
+            if (f.hi - f.lo > wm) wm = f.hi - f.lo;
+            sum += f.hi - f.lo;
+        }
+        if (sum > ds) ds = sum;
+    }
+    *dsum = ds;
+    return wm;
+}
+
+// Same for an analysis pyramid (steps top..bot+1, chunks of 2^cb at level top).
+inline int pyr_wmax_ana(int nu, int top, int bot, int cb, bool vmp) {
+    int wm = 1;
+    const int lnc = top - cb;
+    for (long long c = 0; c < (1ll << lnc); ++c) {
+        Win r{int(c << (bot - lnc)), int((c + 1) << (bot - lnc))};
+        for (int s = bot + 1; s <= top; ++s) {
+            r = ana_need(nu, 1 << s, r, vmp);
+            if (r.hi - r.lo > wm) wm = r.hi - r.lo;
+        }
+    }
+    return wm;
+}
 cudaError_t launch_small(int nu, const SmallArgs& a, bool adj, cudaStream_t st);
 long long small_smem_query(int nu, int V, int j, int q, bool adj, bool vf);
 cudaError_t launch_large(int nu, int which, const LargeArgs& a, cudaStream_t st);
-long long large_nslot(int q, int j, int kl, int ng);
+long long large_nslot(int nu, int q, int j, int kl, int ng);
+// adj2 keeps per-warp edge sums in smem when they are small (<= 256 values)
+inline bool large_cta_red(int nu, int q) { return (2 * (2 * nu - 1)) << q <= 256; }
 cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st);
 cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, double* scratch,
                         cudaStream_t st);

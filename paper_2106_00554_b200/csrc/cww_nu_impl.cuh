@@ -70,7 +70,9 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
     dim3 g1(1u << kh, (unsigned)a.nvec), g2((unsigned)(R1 / a.ng), (unsigned)a.nvec);
     long long s1 = ((long long)R1 * Gm::RS) * 8;
     long long s2 = ((long long)a.ng * R2 * Gm::RS + S * 2 * Gm::NP) * 8;
-    long long s1a = s1 + (S * 2 * Gm::NP + 2 * CWW_NU) * 8;
+    const long long FE = (long long)S * 2 * Gm::NP;
+    long long s1a = s1 + (FE + 2 * CWW_NU + (CWW_NT / 32) * 2 * CWW_NU + (FE > CWW_NT ? FE : CWW_NT)) * 8;
+    long long s2a = s2 + (a.cta_red ? (CWW_NT / 32) * FE * 8 : 0);
     switch (which) {
         case 0: {
             auto k = k_large_fwd1<CWW_NU, CWW_NT>;
@@ -86,8 +88,8 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
         }
         case 2: {
             auto k = k_large_adj2<CWW_NU, CWW_NT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-            k<<<g2, CWW_NT, s2, st>>>(a);
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2a);
+            k<<<g2, CWW_NT, s2a, st>>>(a);
             break;
         }
         default: {
@@ -96,6 +98,27 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
             k<<<g1, CWW_NT, s1a, st>>>(a);
             break;
         }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t st) {
+    dim3 g(1u << (a.top - a.cb), (unsigned)a.nvec);
+    constexpr long long FS = FiltSmem<CWW_NU>::SIZE;
+    if (analysis) {
+        long long nb = 2ll * a.wmax;
+        if (a.tail && nb < (2ll << a.bot)) nb = 2ll << a.bot;
+        const long long smem = (FS + 64 + nb) * 8;
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+        auto k = k_dwt_pyr<CWW_NU, CWW_NT>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<g, CWW_NT, smem, st>>>(a);
+    } else {
+        const long long smem = (FS + 48 + 2ll * a.wmax + a.dsum) * 8;
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+        auto k = k_idwt_pyr<CWW_NU, CWW_NT>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<g, CWW_NT, smem, st>>>(a);
     }
     return cudaGetLastError();
 }
