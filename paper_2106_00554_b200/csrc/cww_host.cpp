@@ -707,7 +707,7 @@ int env_int(const char* name, int dflt) {
     return e && *e ? std::atoi(e) : dflt;
 }
 const int kPyrSynLog = env_int("CWW_PYR_SYN_LOG", 12);
-const int kPyrAnaLog = env_int("CWW_PYR_ANA_LOG", 11);
+const int kPyrAnaLog = env_int("CWW_PYR_ANA_LOG", 12);
 const int kPyrSynBot = env_int("CWW_PYR_SYN_BOT", 10);  // coarse levels <= this: separate kernel
 
 cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
@@ -722,7 +722,7 @@ cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
 
 // ---- large path (1D, M > 2^13) ----
 struct LargePlan {
-    int kl, ng;
+    int kl, ng, ng_adj;  // ng: fwd2 sub-tiles per CTA; ng_adj: adj2 (one row per thread)
 };
 LargePlan large_plan(unsigned j) {
     int a = int(j) - cww::kLogB;
@@ -731,7 +731,9 @@ LargePlan large_plan(unsigned j) {
     int kh = a - kl;
     int ng = 1;
     while (ng * (1 << kh) < 128 && ng * 2 <= (1 << kl)) ng *= 2;
-    return {kl, ng};
+    int ng_adj = 1;  // adj2 runs one tile row per thread: fill the CTA
+    while (ng_adj * (1 << kh) < 256 && ng_adj * 2 <= (1 << kl)) ng_adj *= 2;
+    return {kl, ng, ng_adj};
 }
 
 cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
@@ -742,7 +744,7 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     const long long A = M >> cww::kLogB;
     const auto pl = large_plan(op->j);
     const bool idwt = op->d.use_idwt && op->r0 < int(op->j);
-    const long long nslot = cww::large_nslot(nu, int(op->q), int(op->j), pl.kl, pl.ng);
+    const long long nslot = cww::large_nslot(nu, int(op->q), int(op->j), pl.kl, pl.ng_adj);
     DevBuf w0, w1, G, ev, epw;
     CUDA_TRY(G.alloc(size_t(nvec * A * CW), st));
     CUDA_TRY(ev.alloc(size_t(nvec * 2 * nu), st));
@@ -827,6 +829,7 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
         }
         return CWW_OK;
     }
+    a.ng = pl.ng_adj;
     // adjoint
     {
         Prof pr("large_adj2", st);

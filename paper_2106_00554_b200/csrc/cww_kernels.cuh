@@ -829,7 +829,7 @@ __device__ __forceinline__ void idwt_window(const FiltSmem<NU>& F, const Taps<NU
         mlo = max(mlo, (EL + 1) >> 1);
         mhi = min(mhi, (n - EL) >> 1);
     }
-    for (int m = mlo + t0; m < mhi; m += nthr) {
+    auto pair = [&](int m, double& o0, double& o1) {
         constexpr int OFF = (NU + 1) / 2;
         double c[NU + 1], d[NU + 1];
 #pragma unroll
@@ -848,8 +848,14 @@ __device__ __forceinline__ void idwt_window(const FiltSmem<NU>& F, const Taps<NU
                 b1 += tp.g[u + NU - 1] * d[OFF - (u - 1) / 2];
             }
         }
-        put(2 * m, a0 + b0);
-        put(2 * m + 1, a1 + b1);
+        o0 = a0 + b0;
+        o1 = a1 + b1;
+    };
+    for (int m = mlo + t0; m < mhi; m += nthr) {
+        double o0, o1;
+        pair(m, o0, o1);
+        put(2 * m, o0);
+        put(2 * m + 1, o1);
     }
     // the rest of [lo, hi): partial pairs at the window ends and VMP edge samples
     const int nl = 2 * mlo - lo, nr = hi - 2 * mhi;
@@ -1048,6 +1054,7 @@ __global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
     __syncthreads();
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
+    double* yb = p.y + p.ly.vbase(p.yv0 + v);  // large path: contiguous 1D output
     for (int s = p.top; s > p.bot; --s) {
         const int n = 1 << s, half = n >> 1;
         const int lo = rlo[s], hi = rhi[s];
@@ -1055,17 +1062,20 @@ __global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
         const double* xv = X - xlo[s];
         double* yv = Y - lo;
         const bool last = s == p.bot + 1;
-        for (int mm = lo + tid; mm < hi; mm += NT) {
-            double cc, dd;
-            dwt_pair_log<NU>(F, tp, xv, n, mm, vmp, cc, dd);
+        auto row = [&](int mm, double cc, double dd) {
             if (!last) yv[mm] = cc;
             if (mm >= plo && mm < phi) {
-                p.y[p.ly.at(p.yv0 + v, half + mm)] = dd;
+                yb[half + mm] = dd;
                 if (last) {
                     if (p.cws) p.cws[v * p.cws_vs + mm] = cc;
-                    else p.y[p.ly.at(p.yv0 + v, mm)] = cc;
+                    else yb[mm] = cc;
                 }
             }
+        };
+        for (int mm = lo + tid; mm < hi; mm += NT) {
+            double c0, d0;
+            dwt_pair_log<NU>(F, tp, xv, n, mm, vmp, c0, d0);
+            row(mm, c0, d0);
         }
         __syncthreads();
         double* t0 = X;
@@ -1089,7 +1099,7 @@ __global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
         for (int k = tid; k < half; k += NT) {
             double cc, dd;
             dwt_pair<NU>(F, cur, m, k, vmp, cc, dd);
-            p.y[p.ly.at(p.yv0 + v, half + k)] = dd;
+            yb[half + k] = dd;
             nxt[k] = cc;
         }
         __syncthreads();
@@ -1097,7 +1107,7 @@ __global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
         cur = nxt;
         nxt = t0;
     }
-    for (int i = tid; i < (1 << p.r0); i += NT) p.y[p.ly.at(p.yv0 + v, i)] = cur[i];
+    for (int i = tid; i < (1 << p.r0); i += NT) yb[i] = cur[i];
     if (tid == 0) p.cnt[v] = 0u;  // ticket ready for the next launch
 }
 
@@ -1152,7 +1162,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
     const int tid = threadIdx.x;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
     const int kl = p.kl, R1 = 1 << kl, kh = a - kl, R2 = 1 << kh;
-    const int NG = p.ng;
+    const int NG = p.ng, lng = 31 - __clz(NG);
     const int rho0 = blockIdx.x * NG, v = blockIdx.y;
     double* ES = sm;                // [S][2NP]
     double* T = sm + S * 2 * NP;    // NG tiles of R2 physical rows
@@ -1160,7 +1170,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
     const double* g = p.G + (long long)v * A * CW;
     for (int f = tid; f < NG * R2 * CW; f += NT) {
         const int e = f % CW, rest = f / CW;
-        const int ng = rest % NG, khi = rest / NG;
+        const int ng = rest & (NG - 1), khi = rest >> lng;  // NG = 2^lng
         const int ph = (int)brev_bits((unsigned)khi, kh);
         cp_async8(T + ng * tst + tile_idx(ph, e, RS, ph), g + ((long long)khi * R1 + rho0 + ng) * CW + e);
     }
@@ -1203,7 +1213,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
     const int tid = threadIdx.x, lane = tid & 31;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
     const int kl = p.kl, R1 = 1 << kl, kh = a - kl, R2 = 1 << kh;
-    const int NG = p.ng;
+    const int NG = p.ng, lng = 31 - __clz(NG);
     const int rho0 = blockIdx.x * NG, v = blockIdx.y;
     double* T = sm;
     const int tst = R2 * RS;
@@ -1256,7 +1266,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
     double* g = p.G + (long long)v * A * CW;
     for (int f = tid; f < NG * R2 * CW; f += NT) {
         const int e = f % CW, rest = f / CW;
-        const int ng = rest % NG, khi = rest / NG;
+        const int ng = rest & (NG - 1), khi = rest >> lng;  // NG = 2^lng
         const int ph = (int)brev_bits((unsigned)khi, kh);
         g[((long long)khi * R1 + rho0 + ng) * CW + e] = T[ng * tst + tile_idx(ph, e, RS, ph)];
     }
@@ -1345,12 +1355,14 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* xo = p.xo + (long long)v * p.xo_vs;
     double* ob = p.out + p.lout.vbase(p.v0 + v);
-    for (int f = tid; f < R1 * B; f += NT) {
-        const int rl = f / B, k = f % B;  // logical local row K_lo
+    static_assert(B == 32, "one tile row per warp");
+    const int lane = tid & 31;
+    for (int rl = tid >> 5; rl < R1; rl += NT / 32) {  // logical local row K_lo, lane = column
+        const int k = lane;
         const long long pos = ((long long)chunk * R1 + rl) * B + k;
         const int ph = (int)brev_bits((unsigned)rl, kl);
         double val = T[tile_idx(ph, k + H, RS, ph)];
-        if (k < H) {
+        if (k < H) {  // overlap-add of the previous row's right halo
             if (rl > 0) {
                 const int pq = (int)brev_bits((unsigned)(rl - 1), kl);
                 val += T[tile_idx(pq, B + H + k, RS, pq)];
@@ -1358,7 +1370,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
                 val += nb[k];
             }
         }
-        if (k >= B - H) {
+        if (k >= B - H) {  // and of the next row's left halo
             const int kk = k - (B - H);
             if (rl < R1 - 1) {
                 const int pq = (int)brev_bits((unsigned)(rl + 1), kl);
@@ -1367,7 +1379,8 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
                 val += nb[H + kk];
             }
         }
-        if (NU > 1 && (pos < NU || pos >= M - NU)) {
+        const long long rpos = pos - k;  // warp-uniform: does this row hold an edge position?
+        if (NU > 1 && (rpos < NU || rpos + B > M - NU) && (pos < NU || pos >= M - NU)) {
             const int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
             const double* em = p.tab + p.t.o_em + c;
             double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
