@@ -701,14 +701,15 @@ cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out
     return CWW_OK;
 }
 
-// chunk (log2 fine samples per CTA) of the synthesis / analysis pyramids
+// Wavelet pyramid plan (tuning knobs overridable from the environment)
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e && *e ? std::atoi(e) : dflt;
 }
-const int kPyrSynLog = env_int("CWW_PYR_SYN_LOG", 12);
-const int kPyrAnaLog = env_int("CWW_PYR_ANA_LOG", 12);
 const int kPyrSynBot = env_int("CWW_PYR_SYN_BOT", 10);  // coarse levels <= this: separate kernel
+const int kWpyrLog = env_int("CWW_WPYR_LOG", 9);       // warp pyramid: 2^9 fine samples per warp
+const int kWpyrLevels = env_int("CWW_WPYR_LEVELS", 0);  // synthesis levels per launch (0: 6 if j <= 17, else 4)
+const int kWpyrAnaLevels = env_int("CWW_WPYR_ANA_LEVELS", 3);  // analysis steps per launch
 
 cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     cww::PyrArgs y{};
@@ -779,16 +780,13 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     if (!adj) {
         const double* xi = nullptr;
         if (idwt) {
-            // all synthesis levels r0+1..j in one launch (per-CTA window cones)
-            cww::PyrArgs y = pyr_args(op, nvec);
-            y.top = int(op->j);
-            y.bot = std::max(op->r0, std::min(kPyrSynBot, int(op->j) - 1));
-            y.cb = std::min(int(op->j), kPyrSynLog);
-            y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum);
-            y.x = in;
-            y.lx = lin;
-            y.src_is_x = 1;
-            if (y.bot > op->r0) {  // coarse levels r0+1..bot: one CTA per vector
+            // coarse levels r0+1..bot in one CTA per vector, then the fine
+            // levels in chained warp pyramids of <= kWpyrLevels levels
+            const int j = int(op->j);
+            int bot = std::max(op->r0, std::min(kPyrSynBot, j - 1));
+            const double* src = nullptr;  // level-bot coarse vector (nullptr: the op input)
+            long long src_vs = 0;
+            if (bot > op->r0) {
                 cww::WavArgs w{};
                 w.tab = op->d_tab;
                 w.t = op->tabs;
@@ -796,25 +794,45 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
                 w.r0 = op->r0;
                 w.vmp = op->vmp;
                 w.kind = 0;
-                w.lev = y.bot;
+                w.lev = bot;
                 w.inverse = 1;
                 w.src = in;
                 w.ls = lin;
                 w.dst = w1.p;
-                w.dst_vs = 1ll << y.bot;
+                w.dst_vs = 1ll << bot;
                 {
                     Prof pr("wav_coarse", st);
                     CUDA_TRY(cww::launch_wav(nu, w, st));
                 }
-                y.src_is_x = 0;
-                y.src = w1.p;
-                y.src_vs = 1ll << y.bot;
+                src = w1.p;
+                src_vs = 1ll << bot;
             }
-            y.out = w0.p;
-            y.out_vs = M;
-            Prof pr("idwt_pyr", st);
-            CUDA_TRY(cww::launch_pyr(nu, false, y, st));
-            xi = w0.p;
+            double* bufs[2] = {w0.p, w1.p};
+            int ob = 0;
+            while (bot < j) {
+                const int top = std::min(j, bot + (kWpyrLevels > 0 ? kWpyrLevels : (j <= 17 ? 6 : 4)));
+                cww::PyrArgs y = pyr_args(op, nvec);
+                y.top = top;
+                y.bot = bot;
+                y.cb = std::min(top, kWpyrLog);
+                y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum);
+                y.x = in;
+                y.lx = lin;
+                y.src_is_x = src ? 0 : 1;
+                y.src = src;
+                y.src_vs = src_vs;
+                ob = (src == w0.p) ? 1 : 0;  // never overwrite the level being read
+                y.out = bufs[ob];
+                y.out_vs = M;
+                {
+                    Prof pr("idwt_pyr", st);
+                    CUDA_TRY(cww::launch_pyr(nu, false, y, st));
+                }
+                src = bufs[ob];
+                src_vs = M;
+                bot = top;
+            }
+            xi = src;
         }
         a.xi = xi;
         a.xi_vs = M;
@@ -843,8 +861,9 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
         CUDA_TRY(cww::launch_large(nu, 3, a, st));
     }
     if (!idwt) return CWW_OK;
-    // analysis: pyramids of up to d steps (halo ~ (2nu-2) 2^d <= chunk/8); the
-    // last one finishes the coarse levels in its last CTA per vector
+    // analysis: chained warp pyramids of <= kWpyrAnaLevels steps (halo ~
+    // (2nu-2) 2^d per 2^kWpyrLog-row chunk); the launch that reaches level
+    // <= kPyrSynBot finishes the coarse levels in its last CTA per vector
     unsigned* cnt = nullptr;
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cnt), size_t(nvec) * sizeof(unsigned), st));
     struct CntFree {
@@ -857,11 +876,9 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     const double* src = w0.p;
     double* sink[2] = {w1.p, w0.p};
     for (int it = 0;; ++it) {
-        const int cb = std::min(T, kPyrAnaLog);
-        int d = 1;
-        while (d + 1 <= T - op->r0 && (2 * nu - 2) * ((1 << (d + 1)) - 1) <= (1 << cb) / 8) ++d;
-        const int bot = std::max({op->r0, T - d, T - cb});
-        const bool tail = bot > op->r0 && bot <= cww::kSmallMaxLog;
+        const int cb = std::min(T, kWpyrLog);
+        const int bot = std::max({op->r0, T - kWpyrAnaLevels, T - cb});
+        const bool tail = bot > op->r0 && bot <= std::max(kPyrSynBot, op->r0);
         cww::PyrArgs y = pyr_args(op, nvec);
         y.top = T;
         y.bot = bot;

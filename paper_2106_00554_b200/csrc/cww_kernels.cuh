@@ -919,27 +919,29 @@ __device__ __forceinline__ void dwt_pair_log(const FiltSmem<NU>& F, const Taps<N
 // ---------------------------------------------------------------------------
 // large path: multilevel wavelet pyramids (one launch for many levels)
 // ---------------------------------------------------------------------------
-// Synthesis: CTA (c, v) produces the fine samples [c*2^cb, (c+1)*2^cb) of
-// level `top` for vector v.  It derives its cone of windows down to level
-// `bot` (syn_need), loads the level-bot coarse window and each level's detail
-// window, and synthesises upward in shared memory; only the top level is
-// written.  The cone shrinks geometrically, so the redundant work at the
-// coarse levels is a few samples per CTA and no inter-CTA exchange is needed.
-template <int NU, int NT>
-__global__ void __launch_bounds__(NT) k_idwt_pyr(PyrArgs p) {
+// Warp-granular synthesis pyramid: every WARP owns one chunk of 2^cb fine
+// samples of level `top` and runs its own cone (windows, prefetch, levels)
+// with __syncwarp only -- no CTA barrier after the filter staging, so the
+// warps of a CTA (and of the other resident CTAs) overlap their load,
+// compute and store phases freely.
+template <int NU>
+__global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
     extern __shared__ double sm[];
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
-    int* wlo = reinterpret_cast<int*>(sm + FS);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int per = 48 + 2 * p.wmax + p.dsum;
+    double* wb = sm + FS + wid * per;
+    int* wlo = reinterpret_cast<int*>(wb);
     int* whi = wlo + 32;
     int* doff = wlo + 64;
-    double* P = sm + FS + 48;
+    double* P = wb + 48;
     double* Q = P + p.wmax;
-    double* D = Q + p.wmax;  // every level's detail window, prefetched at once
-    const int tid = threadIdx.x, lane = tid & 31, c = blockIdx.x, v = blockIdx.y;
+    double* D = Q + p.wmax;
+    const int c = blockIdx.x * nw + wid, v = blockIdx.y;
     const bool vmp = p.vmp != 0;
-    for (int i = tid; i < FS; i += NT) filt[i] = p.tab[p.t.o_h + i];
-    if (tid == 0) {
+    for (int i = tid; i < FS; i += blockDim.x) filt[i] = p.tab[p.t.o_h + i];
+    if (lane == 0) {
         Win f{c << p.cb, (c + 1) << p.cb};
         for (int lev = p.top; lev >= p.bot; --lev) {
             wlo[lev] = f.lo;
@@ -956,49 +958,34 @@ __global__ void __launch_bounds__(NT) k_idwt_pyr(PyrArgs p) {
         }
         if (off > p.dsum) __trap();
     }
-    __syncthreads();
+    __syncthreads();  // filters (CTA-wide) and this warp's windows
     const double* xb = p.x + p.lx.vbase(p.xv0 + v);
     const double* cs = p.src_is_x ? xb : p.src + v * p.src_vs;
     {
         const int lo = wlo[p.bot], w = whi[p.bot] - lo, hb = 1 << p.bot;
-        for (int t = tid; t < w; t += NT) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
+        for (int t = lane; t < w; t += 32) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
     }
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {  // details of level lev (half = 2^(lev-1))
         const int lo = wlo[lev - 1], w = whi[lev - 1] - lo, hf = 1 << (lev - 1);
         const double* ds = xb + hf;
         double* dd = D + doff[lev];
-        for (int t = tid; t < w; t += NT) cp_async8(dd + t, ds + (vmp ? lo + t : ((lo + t) & (hf - 1))));
+        for (int t = lane; t < w; t += 32) cp_async8(dd + t, ds + (vmp ? lo + t : ((lo + t) & (hf - 1))));
     }
     cp_async_wait_all();
-    __syncthreads();
+    __syncwarp();
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
     double* ob = p.out + v * p.out_vs;
-    bool warp_mode = false;
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {
         const int n = 1 << lev;
         const int clo = wlo[lev - 1], lo = wlo[lev], hi = whi[lev];
         const double* dw = D + doff[lev];
-        if (lev < p.top && hi - lo <= 64) {  // small level: one warp, no CTA barrier
-            warp_mode = true;
-            if (tid < 32) {
-                double* q = Q - lo;
-                idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32,
-                                [&](int i, double val) { q[i] = val; });
-                __syncwarp();
-            }
+        if (lev < p.top) {
+            double* q = Q - lo;
+            idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { q[i] = val; });
+            __syncwarp();
         } else {
-            if (warp_mode) __syncthreads();
-            warp_mode = false;
-            if (lev < p.top) {
-                double* q = Q - lo;
-                idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, tid, NT,
-                                [&](int i, double val) { q[i] = val; });
-                __syncthreads();
-            } else {
-                idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, tid, NT,
-                                [&](int i, double val) { ob[i] = val; });
-            }
+            idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { ob[i] = val; });
         }
         double* t0 = P;
         P = Q;
@@ -1006,31 +993,66 @@ __global__ void __launch_bounds__(NT) k_idwt_pyr(PyrArgs p) {
     }
 }
 
-// Analysis: CTA (c, v) owns rows [c, c+1) * 2^(s-1-lognc) of every step s =
-// top..bot+1 (input length 2^s).  It loads the fine window its cone needs
-// (ana_need; the halo grows ~ (2nu-2) 2^(top-bot), chosen by the host to stay
-// ~10% of the chunk), computes the coarse rows of the cone level by level in
-// shared memory and writes its own detail rows and its own level-bot coarse
-// rows (workspace, or the output when bot = r0).  With `tail`, the last CTA of
-// each vector to finish (atomic ticket) runs the remaining coarse levels
-// bot..r0+1 on the whole level-bot vector, so the coarse transform needs no
-// extra launch.
-template <int NU, int NT>
-__global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
+// Coarse tail of an analysis pyramid launch: the last CTA of vector v to
+// finish (atomic ticket) loads the whole level-bot coarse vector from cws and
+// runs levels bot..r0+1 in shared memory (`buf`: 2 * 2^bot doubles).
+template <int NU>
+__device__ __forceinline__ void dwt_coarse_tail(const PyrArgs& p, const FiltSmem<NU>& F, double* buf, int v,
+                                                int tid, int nt) {
+    __shared__ unsigned s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(p.cnt + v, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const bool vmp = p.vmp != 0;
+    double* yb = p.y + p.ly.vbase(p.yv0 + v);
+    const int n0 = 1 << p.bot;
+    double* cur = buf;
+    double* nxt = buf + n0;
+    for (int i = tid; i < n0; i += nt) cur[i] = __ldcg(p.cws + v * p.cws_vs + i);
+    __syncthreads();
+    for (int lev = p.bot; lev > p.r0; --lev) {
+        const int m = 1 << lev, half = m >> 1;
+        for (int k = tid; k < half; k += nt) {
+            double cc, dd;
+            dwt_pair<NU>(F, cur, m, k, vmp, cc, dd);
+            yb[half + k] = dd;
+            nxt[k] = cc;
+        }
+        __syncthreads();
+        double* t0 = cur;
+        cur = nxt;
+        nxt = t0;
+    }
+    for (int i = tid; i < (1 << p.r0); i += nt) yb[i] = cur[i];
+    if (tid == 0) p.cnt[v] = 0u;  // ticket ready for the next launch
+}
+
+// Warp-granular analysis pyramid (steps top..bot+1, optional tail): every WARP
+// owns rows [c, c+1) * 2^(s-1-lognc) of each step, loads its cone's fine
+// window and writes its detail rows and its level-bot coarse rows (to cws, or
+// the output when bot == r0).  __syncwarp only.
+template <int NU>
+__global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
     extern __shared__ double sm[];
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
-    int* rlo = reinterpret_cast<int*>(sm + FS);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int per = 64 + 2 * p.wmax;
+    double* wb = sm + FS + wid * per;
+    int* rlo = reinterpret_cast<int*>(wb);
     int* rhi = rlo + 32;
     int* xlo = rlo + 64;
     int* xhi = rlo + 96;
-    double* buf = sm + FS + 64;
-    __shared__ unsigned s_last;
-    const int tid = threadIdx.x, c = blockIdx.x, v = blockIdx.y;
+    double* X = wb + 64;
+    double* Y = X + p.wmax;
+    const int c = blockIdx.x * nw + wid, v = blockIdx.y;
     const bool vmp = p.vmp != 0;
-    const int lnc = p.top - p.cb;  // log2(chunks per vector)
-    for (int i = tid; i < FS; i += NT) filt[i] = p.tab[p.t.o_h + i];
-    if (tid == 0) {
+    const int lnc = p.top - p.cb;
+    for (int i = tid; i < FS; i += blockDim.x) filt[i] = p.tab[p.t.o_h + i];
+    if (lane == 0) {
         Win r{c << (p.bot - lnc), (c + 1) << (p.bot - lnc)};
         for (int s = p.bot + 1; s <= p.top; ++s) {
             const Win w = ana_need(NU, 1 << s, r, vmp);
@@ -1043,15 +1065,13 @@ __global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
         }
     }
     __syncthreads();
-    double* X = buf;
-    double* Y = buf + p.wmax;
     {
         const double* src = p.src + v * p.src_vs;
         const int lo = xlo[p.top], w = xhi[p.top] - lo, n = 1 << p.top;
-        for (int t = tid; t < w; t += NT) cp_async8(X + t, src + (vmp ? lo + t : ((lo + t) & (n - 1))));
+        for (int t = lane; t < w; t += 32) cp_async8(X + t, src + (vmp ? lo + t : ((lo + t) & (n - 1))));
     }
     cp_async_wait_all();
-    __syncthreads();
+    __syncwarp();
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
     double* yb = p.y + p.ly.vbase(p.yv0 + v);  // large path: contiguous 1D output
@@ -1062,53 +1082,24 @@ __global__ void __launch_bounds__(NT) k_dwt_pyr(PyrArgs p) {
         const double* xv = X - xlo[s];
         double* yv = Y - lo;
         const bool last = s == p.bot + 1;
-        auto row = [&](int mm, double cc, double dd) {
-            if (!last) yv[mm] = cc;
-            if (mm >= plo && mm < phi) {
-                yb[half + mm] = dd;
-                if (last) {
-                    if (p.cws) p.cws[v * p.cws_vs + mm] = cc;
-                    else yb[mm] = cc;
-                }
-            }
-        };
-        for (int mm = lo + tid; mm < hi; mm += NT) {
+        for (int mm = lo + lane; mm < hi; mm += 32) {
             double c0, d0;
             dwt_pair_log<NU>(F, tp, xv, n, mm, vmp, c0, d0);
-            row(mm, c0, d0);
+            if (!last) yv[mm] = c0;
+            if (mm >= plo && mm < phi) {
+                yb[half + mm] = d0;
+                if (last) {
+                    if (p.cws) p.cws[v * p.cws_vs + mm] = c0;
+                    else yb[mm] = c0;
+                }
+            }
         }
-        __syncthreads();
+        __syncwarp();
         double* t0 = X;
         X = Y;
         Y = t0;
     }
-    if (!p.tail) return;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(p.cnt + v, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const int n0 = 1 << p.bot;
-    double* cur = buf;
-    double* nxt = buf + n0;
-    for (int i = tid; i < n0; i += NT) cur[i] = __ldcg(p.cws + v * p.cws_vs + i);
-    __syncthreads();
-    for (int lev = p.bot; lev > p.r0; --lev) {
-        const int m = 1 << lev, half = m >> 1;
-        for (int k = tid; k < half; k += NT) {
-            double cc, dd;
-            dwt_pair<NU>(F, cur, m, k, vmp, cc, dd);
-            yb[half + k] = dd;
-            nxt[k] = cc;
-        }
-        __syncthreads();
-        double* t0 = cur;
-        cur = nxt;
-        nxt = t0;
-    }
-    for (int i = tid; i < (1 << p.r0); i += NT) yb[i] = cur[i];
-    if (tid == 0) p.cnt[v] = 0u;  // ticket ready for the next launch
+    if (p.tail) dwt_coarse_tail<NU>(p, F, sm + FS, v, tid, blockDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -75,7 +75,8 @@ struct WavArgs {
     long long yv0;
 };
 
-// Multilevel wavelet pyramids (large path).  Synthesis: levels bot+1..top,
+// Multilevel wavelet pyramids (large path), one chunk of 2^cb samples of
+// level `top` per warp.  Synthesis: levels bot+1..top,
 // coarse c_bot from src (or the op input x when src_is_x), details from x, top
 // level to out.  Analysis: steps top..bot+1 from src (fine level top), details
 // to y, coarse c_bot to cws (or y when cws == nullptr); tail: the last CTA per

@@ -103,22 +103,24 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
 }
 
 cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t st) {
-    dim3 g(1u << (a.top - a.cb), (unsigned)a.nvec);
     constexpr long long FS = FiltSmem<CWW_NU>::SIZE;
+    const int nchunk = 1 << (a.top - a.cb);  // one chunk per warp
+    const int nw = nchunk < 8 ? nchunk : 8;
+    const dim3 grid((unsigned)(nchunk / nw), (unsigned)a.nvec);
     if (analysis) {
-        long long nb = 2ll * a.wmax;
+        long long nb = (long long)nw * (64 + 2ll * a.wmax);
         if (a.tail && nb < (2ll << a.bot)) nb = 2ll << a.bot;
-        const long long smem = (FS + 64 + nb) * 8;
+        const long long smem = (FS + nb) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-        auto k = k_dwt_pyr<CWW_NU, CWW_NT>;
+        auto k = k_dwt_wpyr<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<g, CWW_NT, smem, st>>>(a);
+        k<<<grid, 32 * nw, smem, st>>>(a);
     } else {
-        const long long smem = (FS + 48 + 2ll * a.wmax + a.dsum) * 8;
+        const long long smem = (FS + (long long)nw * (48 + 2ll * a.wmax + a.dsum)) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-        auto k = k_idwt_pyr<CWW_NU, CWW_NT>;
+        auto k = k_idwt_wpyr<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<g, CWW_NT, smem, st>>>(a);
+        k<<<grid, 32 * nw, smem, st>>>(a);
     }
     return cudaGetLastError();
 }
