@@ -68,6 +68,13 @@ typedef struct {
     int kernel_resolution; /* cascade/quadrature resolution R; 0 = 14           */
     int device;            /* CUDA device ordinal; -1 = current                 */
     const char* data_dir;  /* CWWF directory; NULL = $CWW_DATA_DIR or built-in  */
+    /* Sampling mask P_Omega of ComposedOp(op, SamplingMask, use_idwt)
+     * (fastop.hpp:33-39, fastop.cpp:12-25, 231-281): sorted, unique output
+     * indices (host memory, copied at create).  NULL / mask_len == output
+     * size = full mask.  A subsampled op has output_size = mask_len: forward
+     * gathers the masked rows, adjoint scatters into zeros first. */
+    const uint64_t* mask;
+    size_t mask_len;
 } cww_op_desc;
 
 typedef struct cww_op cww_op;

@@ -6,7 +6,8 @@
 //   reference (proj/include/cww/fastop.hpp)        here
 //   struct LinearOp { rows, cols, forward, adjoint } cww_b200::LinearOp     (fastop.hpp:14-31)
 //   class FastOp(filters, spec, j, q, kernels, dim) cww_b200::FastOp(spec, j, q, dim)  (:44-92)
-//   class ComposedOp(op, mask, use_idwt)           cww_b200::ComposedOp(op, use_idwt, r0) (:114-127)
+//   class ComposedOp(op, mask, use_idwt)           cww_b200::ComposedOp(op, [mask,] use_idwt, r0) (:114-127)
+//   struct SamplingMask                             cww_b200::SamplingMask (:33-39)
 //   class HaarFullRankOp(j)                        cww_b200::HaarFullRankOp(j)  (:131-142)
 //   CwwError                                       cww_b200::CwwError (wavelet.hpp:11-13)
 //
@@ -15,6 +16,7 @@
 // device pointers and a stream (asynchronous, the fast path).
 #pragma once
 #include <cstddef>
+#include <cstdint>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -49,6 +51,13 @@ struct WaveletSpec {
     }
 };
 
+// SamplingMask (fastop.hpp:33-39): sorted, unique output indices; empty = full.
+struct SamplingMask {
+    std::vector<std::uint64_t> indices;
+    static SamplingMask full(std::uint64_t) { return {}; }
+    std::size_t size() const { return indices.size(); }
+};
+
 struct LinearOp {
     virtual ~LinearOp() = default;
     virtual std::size_t rows() const = 0;
@@ -71,7 +80,7 @@ struct LinearOp {
 class Op : public LinearOp {
 public:
     Op(const WaveletSpec& s, unsigned j, unsigned q, int dim, bool use_idwt, int min_level = -1,
-       const char* data_dir = nullptr, int device = -1) {
+       const char* data_dir = nullptr, int device = -1, const SamplingMask* mask = nullptr) {
         cww_op_desc d;
         cww_op_desc_init(&d);
         d.family = int(s.family);
@@ -84,6 +93,10 @@ public:
         d.use_idwt = use_idwt ? 1 : 0;
         d.device = device;
         d.data_dir = data_dir;
+        if (mask && !mask->indices.empty()) {
+            d.mask = mask->indices.data();
+            d.mask_len = mask->indices.size();
+        }
         cww_op* h = nullptr;
         check(cww_op_create(&d, &h));
         h_.reset(h, [](cww_op* p) { cww_op_destroy(p); });
@@ -138,6 +151,9 @@ public:
     // full sampling mask; r0 (min_level) -1 = the spec's J0 as in the reference
     ComposedOp(const FastOp& op, bool use_idwt = true, int min_level = -1)
         : Op(op.spec(), op.j(), op.q(), op.dim(), use_idwt, min_level) {}
+    // ComposedOp(op, SamplingMask, use_idwt) (fastop.hpp:116): rows() = mask size
+    ComposedOp(const FastOp& op, const SamplingMask& mask, bool use_idwt, int min_level = -1)
+        : Op(op.spec(), op.j(), op.q(), op.dim(), use_idwt, min_level, nullptr, -1, &mask) {}
 };
 
 class HaarFullRankOp : public Op {

@@ -187,6 +187,18 @@ class OracleOp:
         self.o._check(self.o.L.orc_op_adjoint(self.h, _ptr(y), _ptr(x), int(use_idwt)))
         return x
 
+    def forward_masked(self, mask, x, use_idwt=True):
+        """ComposedOp::forward with a subsampled mask (fastop.cpp:253-259):
+        full forward, then y[i] = full[mask[i]]."""
+        return self.forward(x, use_idwt)[np.asarray(mask, dtype=np.int64)]
+
+    def adjoint_masked(self, mask, y, use_idwt=True):
+        """ComposedOp::adjoint with a subsampled mask (fastop.cpp:265-270):
+        scatter into zeros, then the full adjoint."""
+        full = np.zeros(self.nout)
+        full[np.asarray(mask, dtype=np.int64)] = y
+        return self.adjoint(full, use_idwt)
+
     def edge_terms(self):
         cap = 512
         p = (C.c_uint64 * cap)()
@@ -224,6 +236,8 @@ class Reference:
         L.ref_op_forward.argtypes = [C.c_void_p, _dp, _dp, C.c_int]
         L.ref_op_adjoint.argtypes = [C.c_void_p, _dp, _dp, C.c_int]
         L.ref_haar_fullrank.argtypes = [C.c_uint, _dp, _dp, C.c_int]
+        L.ref_composed_masked.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int,
+                                          _dp, _dp]
         L.ref_bench.restype = C.c_double
         L.ref_bench.argtypes = [C.c_void_p, C.c_int, _dp, _dp, C.c_size_t, C.c_int, C.c_int,
                                 C.c_int]
@@ -305,6 +319,15 @@ class ReferenceOp:
         x = np.empty(self.nin)
         self.r._check(self.r.L.ref_op_adjoint(self.h, _ptr(y), _ptr(x), int(use_idwt)))
         return x
+
+    def masked(self, mask, v, adjoint=False, use_idwt=True):
+        """The reference ComposedOp(op, SamplingMask{mask}, use_idwt) (fastop.cpp:231-281)."""
+        m = np.ascontiguousarray(mask, dtype=np.uint64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty(self.nin if adjoint else m.size)
+        self.r._check(self.r.L.ref_composed_masked(self.h, m.ctypes.data, m.size, int(use_idwt),
+                                                   int(adjoint), _ptr(v), _ptr(out)))
+        return out
 
     def bench(self, mode, inp, out, batch, threads, iters=1, use_idwt=True) -> float:
         t = self.r.L.ref_bench(self.h, mode, _ptr(inp), _ptr(out), batch, threads, iters,

@@ -215,6 +215,24 @@ int ref_op_adjoint(void* h, const double* y, double* x, int use_idwt) {
     return guarded([&] { composed_adjoint(*static_cast<RefOp*>(h), y, x, use_idwt != 0); });
 }
 
+// The reference ComposedOp with a (subsampled) SamplingMask (fastop.cpp:231-281;
+// its IDWT/DWT use min_level = J0).  Mask validation errors come back as the
+// reference's CwwError messages.
+int ref_composed_masked(void* h, const uint64_t* idx, std::size_t cnt, int use_idwt, int adjoint,
+                        const double* in, double* out) {
+    return guarded([&] {
+        auto* o = static_cast<RefOp*>(h);
+        if (!o->op) throw CwwError("shim: no FastOp for this spec");
+        SamplingMask m;
+        m.indices.assign(idx, idx + cnt);
+        ComposedOp c(o->op, m, use_idwt != 0);
+        if (adjoint)
+            c.adjoint(std::span<const double>(in, c.rows()), std::span<double>(out, c.cols()));
+        else
+            c.forward(std::span<const double>(in, c.cols()), std::span<double>(out, c.rows()));
+    });
+}
+
 // The square HaarFullRankOp itself (fastop.cpp:285-302), for its own tests.
 int ref_haar_fullrank(unsigned j, const double* in, double* out, int adjoint) {
     return guarded([&] {

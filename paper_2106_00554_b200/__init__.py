@@ -67,7 +67,8 @@ class Boundary(enum.IntEnum):
 class _Desc(C.Structure):
     _fields_ = [("family", C.c_int), ("nu", C.c_int), ("boundary", C.c_int), ("j", C.c_uint),
                 ("q", C.c_uint), ("dim", C.c_int), ("min_level", C.c_int), ("use_idwt", C.c_int),
-                ("kernel_resolution", C.c_int), ("device", C.c_int), ("data_dir", C.c_char_p)]
+                ("kernel_resolution", C.c_int), ("device", C.c_int), ("data_dir", C.c_char_p),
+                ("mask", C.c_void_p), ("mask_len", C.c_size_t)]
 
 
 _lib = None
@@ -189,16 +190,30 @@ def parse_wavelet_name(name: str, boundary: Boundary) -> WaveletSpec:
 
 
 class SamplingMask:
-    """Full masks only (SamplingMask::full, fastop.cpp:12-16); subsampled
-    masks are a later row of the scope table."""
+    """SamplingMask (fastop.hpp:33-39): sorted, unique output indices Omega.
+    full(n) is the identity (fastop.cpp:12-17); validate(n) raises like the
+    reference (fastop.cpp:19-25).  A subsampled ComposedOp gathers the masked
+    rows on the GPU (forward) and scatters into zeros (adjoint)."""
 
     def __init__(self, indices=None, n: Optional[int] = None):
-        self.indices = None if indices is None else np.asarray(indices, dtype=np.uint64)
+        self.indices = None if indices is None else np.ascontiguousarray(indices, dtype=np.uint64)
         self.n = n
 
     @staticmethod
     def full(n: int) -> "SamplingMask":
         return SamplingMask(None, n)
+
+    def size(self) -> int:
+        return int(self.n) if self.indices is None else int(self.indices.size)
+
+    def validate(self, n: int) -> None:
+        if self.indices is None:
+            return
+        idx = self.indices
+        if idx.size and int(idx.max()) >= n:
+            raise CwwError("sampling mask index out of range", 3)
+        if idx.size > 1 and not np.all(idx[1:] > idx[:-1]):
+            raise CwwError("sampling mask indices must be sorted and unique", 3)
 
     def is_full(self, n: int) -> bool:
         if self.indices is None:
@@ -225,11 +240,13 @@ class LinearOp:
 class _Handle:
     def __init__(self, spec: WaveletSpec, j: int, q: int, dim: int, min_level: int, use_idwt: bool,
                  kernel_resolution: int = 0, device: Optional[int] = None,
-                 data_dir: Optional[str] = None):
+                 data_dir: Optional[str] = None, mask: Optional[np.ndarray] = None):
         L = _load()
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint64)
         d = _Desc(int(spec.family), spec.nu, int(spec.boundary), j, q, dim, min_level,
                   1 if use_idwt else 0, kernel_resolution, -1 if device is None else device,
-                  (data_dir or DATA_DIR).encode())
+                  (data_dir or DATA_DIR).encode(), None if m is None else m.ctypes.data,
+                  0 if m is None else m.size)
         h = C.c_void_p()
         _check(L.cww_op_create(C.byref(d), C.byref(h)))
         self.h = h
@@ -400,12 +417,15 @@ class ComposedOp(LinearOp):
 
     def __init__(self, op: FastOp, mask: Optional[SamplingMask] = None, use_idwt: bool = True,
                  min_level: Optional[int] = None):
-        if mask is not None and not mask.is_full(op.output_size()):
-            raise CwwError("subsampled masks are not implemented (full mask only)", 7)
+        if mask is not None:
+            mask.validate(op.output_size())
         self.op = op
+        self.mask = mask
         self.use_idwt = bool(use_idwt)
         self.r0 = op.spec().min_level() if min_level is None else int(min_level)
-        self._h = _Handle(op.spec(), op.j(), op.q(), op.dim(), self.r0, self.use_idwt, **op._opts)
+        sub = mask is not None and not mask.is_full(op.output_size())
+        self._h = _Handle(op.spec(), op.j(), op.q(), op.dim(), self.r0, self.use_idwt,
+                          mask=mask.indices if sub else None, **op._opts)
 
     def rows(self):
         return self._h.nout

@@ -63,6 +63,34 @@ cudaError_t launch_pyr(int nu, bool analysis, const PyrArgs& a, cudaStream_t st)
     return cudaErrorInvalidValue;
 }
 
+// Sampling mask P_Omega (fastop.cpp:253-281): one vector per blockIdx.y,
+// sorted indices -> nearly contiguous full-vector accesses.
+__global__ void k_mask(double* full, long long nfull, const uint64_t* __restrict__ idx, long long cnt,
+                       double* y, int scatter) {
+    const long long b = blockIdx.y;
+    double* fb = full + b * nfull;
+    double* yb = y + b * cnt;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long k = (long long)__ldg(idx + i);
+        if (scatter) fb[k] = yb[i];
+        else yb[i] = fb[k];
+    }
+}
+
+cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long long cnt, double* y,
+                        long long batch, bool scatter, cudaStream_t st) {
+    if (cnt == 0 || batch == 0) return cudaSuccess;
+    long long blocks = (cnt + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    for (long long b0 = 0; b0 < batch; b0 += 65535) {
+        const long long nb = batch - b0 < 65535 ? batch - b0 : 65535;
+        k_mask<<<dim3((unsigned)blocks, (unsigned)nb), 256, 0, st>>>(full + b0 * nfull, nfull, idx, cnt,
+                                                                     y + b0 * cnt, scatter ? 1 : 0);
+    }
+    return cudaGetLastError();
+}
+
 long long large_nslot(int nu, int q, int j, int kl, int ng) {
     const int nt = 256;
     const int kh = (j - kLogB) - kl, R1 = 1 << kl, R2 = 1 << kh;

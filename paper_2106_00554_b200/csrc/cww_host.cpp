@@ -452,6 +452,11 @@ struct cww_op {
     cww::Tables tabs{};
     double* d_tab = nullptr;
     std::string data_dir;
+    // subsampled output (ComposedOp with a SamplingMask, fastop.cpp:231-281)
+    std::vector<uint64_t> mask;
+    uint64_t* d_mask = nullptr;
+    bool masked = false;
+    long long full_out = 0;  // output size of the unmasked operator
 };
 
 namespace {
@@ -935,13 +940,36 @@ cww_status run_2d(const cww_op* op, const double* in, double* out, long long bat
     return run_small(op, T.p, t_rows, out, x_rows, batch * M, true, st);
 }
 
+cww_status run_full(const cww_op* op, const double* in, double* out, long long batch, bool adj,
+                    cudaStream_t st) {
+    if (op->dim == 1) return run_1d(op, in, out, batch, adj, st);
+    return run_2d(op, in, out, batch, adj, st);
+}
+
 cww_status run(const cww_op* op, const double* in, double* out, long long batch, bool adj,
                cudaStream_t st) {
     int cur = -1;
     CUDA_TRY(cudaGetDevice(&cur));
     if (cur != op->device) CUDA_TRY(cudaSetDevice(op->device));
-    if (op->dim == 1) return run_1d(op, in, out, batch, adj, st);
-    return run_2d(op, in, out, batch, adj, st);
+    if (!op->masked) return run_full(op, in, out, batch, adj, st);
+    // subsampled mask (fastop.cpp:253-281): full operator + gather / scatter
+    const long long cnt = (long long)op->mask.size();
+    DevBuf full;
+    CUDA_TRY(full.alloc(size_t(batch * op->full_out), st));
+    if (!adj) {
+        cww_status s = run_full(op, in, full.p, batch, false, st);
+        if (s != CWW_OK) return s;
+        Prof pr("mask_gather", st);
+        CUDA_TRY(cww::launch_mask(full.p, op->full_out, op->d_mask, cnt, out, batch, false, st));
+        return CWW_OK;
+    }
+    CUDA_TRY(cudaMemsetAsync(full.p, 0, size_t(batch * op->full_out) * sizeof(double), st));
+    {
+        Prof pr("mask_scatter", st);
+        CUDA_TRY(cww::launch_mask(full.p, op->full_out, op->d_mask, cnt, const_cast<double*>(in), batch,
+                                  true, st));
+    }
+    return run_full(op, full.p, out, batch, true, st);
 }
 
 }  // namespace
@@ -968,6 +996,8 @@ void cww_op_desc_init(cww_op_desc* d) {
     d->kernel_resolution = 0;
     d->device = -1;
     d->data_dir = nullptr;
+    d->mask = nullptr;
+    d->mask_len = 0;
 }
 
 cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
@@ -975,6 +1005,15 @@ cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
     *out = nullptr;
     cww_status s = validate(desc);
     if (s != CWW_OK) return s;
+    if (desc->mask && desc->mask_len) {  // SamplingMask::validate (fastop.cpp:19-25)
+        const long long n1 = 1ll << (desc->j + desc->q);
+        const uint64_t nout = uint64_t(desc->dim == 2 ? n1 * n1 : n1);
+        for (size_t i = 0; i < desc->mask_len; ++i) {
+            if (desc->mask[i] >= nout) return fail(CWW_ERR_SPEC, "sampling mask index out of range");
+            if (i > 0 && desc->mask[i] <= desc->mask[i - 1])
+                return fail(CWW_ERR_SPEC, "sampling mask indices must be sorted and unique");
+        }
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(CWW_ERR_CUDA, "no CUDA device available (the operator has no CPU fallback)");
@@ -1002,6 +1041,17 @@ cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
     if ((s = kernel_table(op->f, desc->boundary, int(desc->q), R, op->kt)) != CWW_OK) return s;
     build_edge_terms(*op);
     if ((s = build_tables(*op)) != CWW_OK) return s;
+    op->full_out = op->dim == 2 ? op->N * op->N : op->N;
+    if (desc->mask && desc->mask_len) {
+        if (desc->mask_len != size_t(op->full_out)) {  // sorted + unique + full length = identity
+            op->mask.assign(desc->mask, desc->mask + desc->mask_len);
+            op->masked = true;
+            CUDA_TRY(cudaMalloc(&op->d_mask, op->mask.size() * sizeof(uint64_t)));
+            CUDA_TRY(cudaMemcpy(op->d_mask, op->mask.data(), op->mask.size() * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice));
+        }
+    }
+    op->d.mask = nullptr;  // the caller's array is not retained
     // keep freed workspace in the stream-ordered pool between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, op->device) == cudaSuccess) {
@@ -1015,6 +1065,7 @@ cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
 cww_status cww_op_destroy(cww_op* op) {
     if (!op) return CWW_OK;
     if (op->d_tab) cudaFree(op->d_tab);
+    if (op->d_mask) cudaFree(op->d_mask);
     delete op;
     return CWW_OK;
 }
@@ -1023,6 +1074,7 @@ cww_status cww_op_sizes(const cww_op* op, size_t* in, size_t* out) {
     if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
     size_t i = size_t(op->M), o = size_t(op->N);
     if (op->dim == 2) i *= i, o *= o;
+    if (op->masked) o = op->mask.size();  // ComposedOp::rows (fastop.cpp:237-239)
     if (in) *in = i;
     if (out) *out = o;
     return CWW_OK;

@@ -148,6 +148,10 @@ cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st);
 cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, double* scratch,
                         cudaStream_t st);
 cudaError_t launch_seq_perm(uint32_t* perm, int bits, cudaStream_t st);
+// Sampling-mask epilogues: gather y[b][i] = full[b][idx[i]] (scatter = false) or
+// scatter full[b][idx[i]] = y[b][i] (scatter = true; full pre-zeroed).
+cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long long cnt, double* y,
+                        long long batch, bool scatter, cudaStream_t st);
 cudaError_t launch_sign_rows(const uint64_t* pos, long long npos, int j, double* out,
                              cudaStream_t st);
 

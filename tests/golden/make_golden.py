@@ -26,6 +26,10 @@ CASES = [
     (0, 2, 1, 4, 1, 2, 3), (0, 4, 1, 4, 1, 2, 4), (0, 3, 0, 4, 1, 2, -1),
 ]
 
+# (family, nu, boundary, j, q, dim, sampled fraction) for masked ComposedOps
+MASKED = [(0, 2, 1, 5, 1, 1, 0.25), (0, 4, 1, 6, 2, 1, 0.1), (1, 3, 0, 6, 1, 1, 0.5),
+          (0, 3, 1, 4, 1, 2, 0.2)]
+
 
 def main():
     o, r = Oracle(), Reference()
@@ -64,6 +68,22 @@ def main():
         out[k + "_x"] = x
         out[k + "_fwd"] = r.dwt(0, nu, bnd, j, x, 0, r0)
         out[k + "_inv"] = r.dwt(0, nu, bnd, j, x, 1, r0)
+    # subsampled ComposedOp (SamplingMask; the reference's ComposedOp uses r0 = J0)
+    rng = np.random.default_rng(2106)
+    for mi, (fam, nu, bnd, j, q, dim, frac) in enumerate(MASKED):
+        op = r.op(fam, nu, bnd, j, q, dim, -1)
+        cnt = max(1, int(frac * op.nout))
+        mask = np.sort(rng.choice(op.nout, cnt, replace=False)).astype(np.uint64)
+        x = o.normals(9100 + mi, op.nin)
+        y = o.normals(9200 + mi, cnt)
+        k = f"m{mi}"
+        out[k + "_case"] = np.array([fam, nu, bnd, j, q, dim])
+        out[k + "_mask"] = mask
+        out[k + "_x"] = x
+        out[k + "_y"] = y
+        for use in (0, 1):
+            out[k + f"_fwd{use}"] = op.masked(mask, x, adjoint=False, use_idwt=use)
+            out[k + f"_adj{use}"] = op.masked(mask, y, adjoint=True, use_idwt=use)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
     print("wrote", len(out), "arrays")
 

@@ -110,6 +110,7 @@ def test_c_and_cpp_headers_compile_and_link(tmp_path):
     cpp_src.write_text('#include "cww_b200.hpp"\n#include <vector>\nint main(){ try { '
                        'cww_b200::WaveletSpec s{cww_b200::Family::Daubechies, 4, cww_b200::Boundary::Vmp};'
                        ' cww_b200::FastOp op(s, 6, 2); cww_b200::ComposedOp c(op, true, 4);'
+                       ' cww_b200::SamplingMask m{{1, 5, 9}}; cww_b200::ComposedOp cm(op, m, true);'
                        ' std::vector<double> x(c.cols()), y(c.rows()); c.forward(x, y); }'
                        ' catch (const cww_b200::CwwError& e) { return e.status == CWW_ERR_CUDA ? 0 : 1; }'
                        ' return 0; }\n')
@@ -126,3 +127,31 @@ def test_c_and_cpp_headers_compile_and_link(tmp_path):
     assert out.returncode == 0
     run = subprocess.run([str(tmp_path / "cpp_caller")], capture_output=True, text=True)
     assert run.returncode == 0, run.stdout + run.stderr
+
+
+@pytest.mark.parametrize("mask,status", [([0, 5, 3], 3), ([0, 1, 1], 3), ([0, 1 << 20], 3)])
+def test_mask_validation(mask, status):
+    """SamplingMask::validate (fastop.cpp:19-25): unsorted, duplicate or
+    out-of-range indices are rejected before any device work."""
+    import paper_2106_00554_b200 as cw
+    L = cw._load()
+    m = np.array(mask, dtype=np.uint64)
+    d = _desc(nu=2, j=5, q=1)
+    d.mask = m.ctypes.data
+    d.mask_len = m.size
+    h = C.c_void_p()
+    assert L.cww_op_create(C.byref(d), C.byref(h)) == status
+    assert b"sampling mask" in L.cww_last_error()
+
+
+def test_python_mask_mirror():
+    import paper_2106_00554_b200 as cw
+    m = cw.SamplingMask([1, 4, 9])
+    m.validate(16)
+    assert m.size() == 3 and not m.is_full(16)
+    assert cw.SamplingMask.full(8).is_full(8)
+    assert cw.SamplingMask(np.arange(8)).is_full(8)
+    with pytest.raises(cw.CwwError, match="out of range"):
+        cw.SamplingMask([1, 16]).validate(16)
+    with pytest.raises(cw.CwwError, match="sorted and unique"):
+        cw.SamplingMask([3, 2]).validate(16)

@@ -114,6 +114,58 @@ def test_parity_large(orc, cuda, case, use_idwt):
         assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL
 
 
+# ---- subsampled ComposedOp (SamplingMask, fastop.cpp:231-281) --------------
+MASKED = [(0, 4, 1, 8, 2, 1, -1, 0.1), (0, 3, 1, 14, 2, 1, 4, 0.3), (1, 2, 0, 9, 1, 1, -1, 0.5),
+          (0, 4, 1, 5, 1, 2, -1, 0.2), (0, 2, 1, 6, 1, 2, 3, 0.05), (0, 1, 0, 10, 1, 1, 1, 0.4)]
+
+
+@pytest.mark.parametrize("case", MASKED, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d_%.2f" % c)
+@pytest.mark.parametrize("use_idwt", [1, 0])
+def test_parity_masked(orc, cuda, case, use_idwt):
+    cw = _cw()
+    fam, nu, bnd, j, q, dim, r0, frac = case
+    if nu == 1 and not use_idwt:
+        pytest.skip("Haar op always composes the IDWT")
+    ref = orc.op(fam, nu, bnd, j, q, dim, r0)
+    rng = np.random.default_rng(j * 31 + nu)
+    mask = np.sort(rng.choice(ref.nout, max(1, int(frac * ref.nout)), replace=False)).astype(np.uint64)
+    if nu == 1:
+        op = cw.ComposedOp.__new__(cw.ComposedOp)  # HaarFullRankOp with a mask: via the handle
+        op._h = cw._Handle(cw.WaveletSpec(cw.Family.Daubechies, 1, cw.Boundary.Periodic), j, q, 1, r0,
+                           True, mask=mask)
+    else:
+        spec = cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd))
+        op = cw.ComposedOp(cw.FastOp(spec, j, q, dim), cw.SamplingMask(mask), bool(use_idwt),
+                           None if r0 < 0 else r0)
+    assert op.rows() == mask.size and op.cols() == ref.nin
+    x = np.stack([orc.normals(700 + b, ref.nin) for b in range(2)])
+    y = np.stack([orc.normals(800 + b, mask.size) for b in range(2)])
+    fx, ay = host(op.forward(gpu(x))), host(op.adjoint(gpu(y)))
+    fh = op.forward(x)  # host-pointer path
+    for b in range(2):
+        assert rel(fx[b], ref.forward_masked(mask, x[b], use_idwt)) <= TOL
+        assert rel(ay[b], ref.adjoint_masked(mask, y[b], use_idwt)) <= TOL
+        assert rel(fh[b], fx[b]) <= 1e-15
+    # normal operator of the subsampled op: A* A = W U* P^T P U W^-1
+    if use_idwt and nu > 1:
+        xt = gpu(x[:1].copy())
+        op.normal(xt, iters=1)
+        want = ref.adjoint_masked(mask, ref.forward_masked(mask, x[0]))
+        assert rel(host(xt)[0], want) <= TOL
+
+
+def test_masked_errors(cuda):
+    cw = _cw()
+    spec = cw.WaveletSpec(cw.Family.Daubechies, 2, cw.Boundary.Vmp)
+    op = cw.FastOp(spec, 6, 1)
+    with pytest.raises(cw.CwwError, match="sorted and unique"):
+        cw.ComposedOp(op, cw.SamplingMask([5, 3]))
+    with pytest.raises(cw.CwwError, match="out of range"):
+        cw.ComposedOp(op, cw.SamplingMask([1, 128]))
+    full = cw.ComposedOp(op, cw.SamplingMask(np.arange(128)))  # full mask = identity
+    assert full.rows() == 128
+
+
 # ---- BASELINE.json configurations ------------------------------------------
 CONFIGS = {  # (family, nu, boundary, j, q, dim, r0), (kind, density)
     1: ((0, 1, 0, 10, 1, 1, 1), (0, 1.0)),

@@ -73,6 +73,21 @@ def test_golden_fwht_perm_signs_dwt(orc, gold):
             assert rel(inv, gold[base + "_inv"]) <= 1e-15
 
 
+def test_golden_masked_composed_op(orc, gold):
+    """Subsampled ComposedOp (SamplingMask, fastop.cpp:231-281): the oracle's
+    gather/scatter restatement against the reference's own outputs."""
+    cases = sorted({k.split("_")[0] for k in gold.files if k.startswith("m") and k.endswith("_case")})
+    assert len(cases) >= 4
+    for c in cases:
+        fam, nu, bnd, j, q, dim = (int(v) for v in gold[c + "_case"])
+        op = orc.op(fam, nu, bnd, j, q, dim, -1)
+        mask = gold[c + "_mask"]
+        assert mask.size < op.nout and np.all(np.diff(mask.astype(np.int64)) > 0)
+        for use in (0, 1):
+            assert rel(op.forward_masked(mask, gold[c + "_x"], use), gold[f"{c}_fwd{use}"]) <= 1e-14
+            assert rel(op.adjoint_masked(mask, gold[c + "_y"], use), gold[f"{c}_adj{use}"]) <= 1e-14
+
+
 # ---- live reference (this container, or a prebuilt oracle/_ref) ------------
 @pytest.mark.parametrize("case", [
     (0, 2, 1, 8, 1, 1, 3), (0, 4, 1, 9, 2, 1, 4), (0, 3, 1, 10, 2, 1, 4), (1, 5, 0, 8, 2, 1, -1),
