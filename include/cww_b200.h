@@ -49,7 +49,8 @@ typedef enum {
     CWW_ERR_CUDA = 5,        /* CUDA runtime error or no device                */
     CWW_ERR_NCCL = 6,
     CWW_ERR_UNSUPPORTED = 7,
-    CWW_ERR_INTERNAL = 8
+    CWW_ERR_INTERNAL = 8,
+    CWW_ERR_NOT_CONVERGED = 9 /* gs_solve: residual above tolerance at max_iters */
 } cww_status;
 
 typedef enum { CWW_DAUBECHIES = 0, CWW_SYMLET = 1 } cww_family;       /* wavelet.hpp:15 */
@@ -99,6 +100,19 @@ cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* 
  * of a least-squares / CG loop).  work: NULL or batch*output_size doubles. */
 cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work,
                       size_t work_len, size_t batch, int iters, void* stream);
+
+/* Least-squares reconstruction (generalised sampling, the reference spec's
+ * gs_solve; its src/reconstruct.cpp is empty): CGLS on the
+ * normal equations A* A x = A* y with A = this op (full or masked), for
+ * `batch` independent systems (device pointers, batch-major).  Stops when
+ * every system's relative normal-equation residual ||A*(y - A x)|| / ||A* y||
+ * <= residual_tol (checked once per iteration), else returns
+ * CWW_ERR_NOT_CONVERGED after max_iters with x = the last iterate.  use_x0:
+ * start from the x passed in (else 0).  iters / residuals (batch doubles,
+ * host) may be NULL. */
+cww_status cww_gs_solve(const cww_op* op, const double* y, size_t y_len, double* x, size_t x_len,
+                        size_t batch, double residual_tol, int max_iters, int use_x0, int* iters,
+                        double* residuals, void* stream);
 
 /* Host-pointer entry points: a literal drop-in for the reference's span API.
  * Stages through pinned buffers and synchronises before returning. */

@@ -96,6 +96,8 @@ def _load():
     for name in ("cww_forward_host", "cww_adjoint_host"):
         getattr(L, name).argtypes = [vp, dp, sz, dp, sz, sz]
     L.cww_normal.argtypes = [vp, dp, sz, dp, sz, sz, C.c_int, vp]
+    L.cww_gs_solve.argtypes = [vp, dp, sz, dp, sz, sz, C.c_double, C.c_int, C.c_int,
+                               C.POINTER(C.c_int), dp, vp]
     L.cww_dwt.argtypes = [vp, dp, sz, sz, C.c_int, vp]
     L.cww_fwht.argtypes = [dp, C.c_uint, sz, C.c_int, vp]
     L.cww_sequency_perm.argtypes = [C.c_uint, dp, vp]
@@ -483,6 +485,34 @@ class HaarFullRankOp(LinearOp):
 
 # ---------------------------------------------------------------------------
 # free functions over device tensors
+def gs_solve(op, y, residual_tol: float = 1e-10, max_iters: int = 1000, x0=None, raise_on_fail: bool = True):
+    """Generalised-sampling least squares (SPEC.md gs_solve, min_z ||A z - y||
+    with A = op): CGLS on A* A x = A* y on the GPU (cww_gs_solve), batched over
+    the leading dimension of y (a contiguous float64 CUDA tensor).  Returns
+    (x, iterations, relative normal-equation residuals).  Raises CwwError
+    (status 9) when max_iters is reached above tolerance, unless raise_on_fail
+    is False."""
+    torch = _torch()
+    h = op._h
+    y = _dev_tensor(y, "gs_solve")
+    if y.numel() % h.nout:
+        raise CwwError("gs_solve: dimension mismatch", 2)
+    batch = y.numel() // h.nout
+    shape = (h.nin,) if y.dim() == 1 else tuple(y.shape[:-1]) + (h.nin,)
+    if x0 is None:
+        x = torch.empty(shape, dtype=torch.float64, device=y.device)
+    else:
+        x = _dev_tensor(x0, "gs_solve x0").clone()
+    it = C.c_int(0)
+    res = np.zeros(batch)
+    rc = h.L.cww_gs_solve(h.h, y.data_ptr(), y.numel(), x.data_ptr(), x.numel(), batch,
+                          float(residual_tol), int(max_iters), 0 if x0 is None else 1, C.byref(it),
+                          _np_ptr(res), _stream_ptr(y))
+    if rc != 0 and (raise_on_fail or rc != 9):
+        _check(rc)
+    return x, it.value, res
+
+
 def _dev_tensor(v, what):
     torch = _torch()
     if not (_is_tensor(v) and v.is_cuda and v.dtype == torch.float64 and v.is_contiguous()):

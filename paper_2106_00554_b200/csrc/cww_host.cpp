@@ -1131,6 +1131,92 @@ cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work, s
     return CWW_OK;
 }
 
+// Least-squares driver (generalised sampling, SPEC.md gs_solve; SURVEY.md 8f
+// row f1): CGLS on A* A x = A* y with A this op (masked or full), batched.
+// Stops when every system's relative normal-equation residual
+// ||A*(y - A x)|| / ||A* y|| <= residual_tol, or after max_iters.
+cww_status gs_solve(const cww_op* op, const double* y, double* x, long long B, double tol, int max_iters,
+                    bool use_x0, int* iters_out, double* resid_out, cudaStream_t st) {
+    size_t ni, no;
+    cww_op_sizes(op, &ni, &no);
+    const long long nx = (long long)ni, nr = (long long)no;
+    DevBuf r, sv, pv, qv, part, sc;
+    CUDA_TRY(r.alloc(size_t(B * nr), st));
+    CUDA_TRY(qv.alloc(size_t(B * nr), st));
+    CUDA_TRY(sv.alloc(size_t(B * nx), st));
+    CUDA_TRY(pv.alloc(size_t(B * nx), st));
+    const long long nb = std::max(cww::dot_nblk(nx, B), cww::dot_nblk(nr, B));
+    CUDA_TRY(part.alloc(size_t(B * nb), st));
+    CUDA_TRY(sc.alloc(size_t(5 * B), st));  // gam[2B] | qq | s0 | active (as int)
+    double* gam[2] = {sc.p, sc.p + B};
+    double* qq = sc.p + 2 * B;
+    double* s0 = sc.p + 3 * B;
+    int* active = reinterpret_cast<int*>(sc.p + 4 * B);
+    cww_status rs;
+    if (use_x0) {
+        if ((rs = run(op, x, r.p, B, false, st)) != CWW_OK) return rs;
+        Prof pr("cg_vec", st);
+        CUDA_TRY(cww::launch_sub_from(r.p, y, B * nr, st));
+    } else {
+        CUDA_TRY(cudaMemsetAsync(x, 0, size_t(B * nx) * sizeof(double), st));
+        CUDA_TRY(cudaMemcpyAsync(r.p, y, size_t(B * nr) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    if ((rs = run(op, r.p, sv.p, B, true, st)) != CWW_OK) return rs;
+    {
+        Prof pr("cg_vec", st, 4);
+        CUDA_TRY(cww::launch_dot(sv.p, sv.p, nx, B, part.p, gam[0], st));
+        CUDA_TRY(cww::launch_sqrt(gam[0], s0, B, st));
+        CUDA_TRY(cww::launch_cgls_flags(gam[0], s0, tol, active, B, st));
+    }
+    CUDA_TRY(cudaMemcpyAsync(pv.p, sv.p, size_t(B * nx) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    std::vector<double> hg(size_t(2 * B));
+    auto residuals = [&](const double* g, bool& done) -> cww_status {
+        CUDA_TRY(cudaMemcpyAsync(hg.data(), g, size_t(B) * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(hg.data() + B, s0, size_t(B) * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        done = true;
+        for (long long b = 0; b < B; ++b) {
+            const double n0 = hg[size_t(B + b)];
+            const double rel = n0 > 0.0 ? std::sqrt(hg[size_t(b)]) / n0 : 0.0;
+            if (resid_out) resid_out[b] = rel;
+            if (rel > tol) done = false;
+        }
+        return CWW_OK;
+    };
+    int it = 0, cur = 0;
+    bool done = false;
+    for (; it < max_iters; ++it) {
+        if ((rs = residuals(gam[cur], done)) != CWW_OK) return rs;
+        if (done) break;
+        if ((rs = run(op, pv.p, qv.p, B, false, st)) != CWW_OK) return rs;  // q = A p
+        {
+            Prof pr("cg_vec", st, 3);
+            CUDA_TRY(cww::launch_dot(qv.p, qv.p, nr, B, part.p, qq, st));
+            CUDA_TRY(cww::launch_cgls_xr(x, r.p, pv.p, qv.p, nx, nr, B, gam[cur], qq, active, st));
+        }
+        if ((rs = run(op, r.p, sv.p, B, true, st)) != CWW_OK) return rs;  // s = A* r
+        {
+            Prof pr("cg_vec", st, 4);
+            CUDA_TRY(cww::launch_dot(sv.p, sv.p, nx, B, part.p, gam[cur ^ 1], st));
+            CUDA_TRY(cww::launch_cgls_p(pv.p, sv.p, nx, B, gam[cur ^ 1], gam[cur], st));
+            CUDA_TRY(cww::launch_cgls_flags(gam[cur ^ 1], s0, tol, active, B, st));
+        }
+        cur ^= 1;
+    }
+    if (!done && (rs = residuals(gam[cur], done)) != CWW_OK) return rs;
+    if (iters_out) *iters_out = it;
+    if (!done) {
+        double worst = 0.0;
+        for (long long b = 0; b < B; ++b) {
+            const double n0 = hg[size_t(B + b)];
+            worst = std::max(worst, n0 > 0.0 ? std::sqrt(hg[size_t(b)]) / n0 : 0.0);
+        }
+        return fail(CWW_ERR_NOT_CONVERGED, "gs_solve: CG did not converge in %d iterations (relative residual %.3e)",
+                    it, worst);
+    }
+    return CWW_OK;
+}
+
 static cww_status host_call(const cww_op* op, const double* in, size_t in_len, double* out,
                             size_t out_len, size_t batch, bool adj) {
     cww_status s = check_lens(op, in_len, out_len, batch, adj, adj ? "adjoint" : "forward");
@@ -1156,6 +1242,20 @@ static cww_status host_call(const cww_op* op, const double* in, size_t in_len, d
     if (rs == CWW_OK && e != cudaSuccess) rs = fail(CWW_ERR_CUDA, "%s", cudaGetErrorString(e));
     cudaStreamDestroy(st);
     return rs;
+}
+
+cww_status cww_gs_solve(const cww_op* op, const double* y, size_t y_len, double* x, size_t x_len,
+                        size_t batch, double residual_tol, int max_iters, int use_x0, int* iters,
+                        double* residuals, void* stream) {
+    cww_status s = check_lens(op, x_len, y_len, batch, false, "gs_solve");
+    if (s != CWW_OK) return s;
+    if (iters) *iters = 0;
+    if (batch == 0) return CWW_OK;
+    if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (max_iters < 0 || !(residual_tol >= 0.0)) return fail(CWW_ERR_INVALID_ARG, "gs_solve: bad parameters");
+    CUDA_TRY(cudaSetDevice(op->device));
+    return gs_solve(op, y, x, (long long)batch, residual_tol, max_iters, use_x0 != 0, iters, residuals,
+                    S_(stream));
 }
 
 cww_status cww_forward_host(const cww_op* op, const double* x, size_t x_len, double* y,

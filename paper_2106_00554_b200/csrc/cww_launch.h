@@ -148,6 +148,19 @@ cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st);
 cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, double* scratch,
                         cudaStream_t st);
 cudaError_t launch_seq_perm(uint32_t* perm, int bits, cudaStream_t st);
+// CGLS vector algebra (cww_solver.cu)
+int dot_nblk(long long n, long long batch);
+cudaError_t launch_dot(const double* a, const double* b, long long n, long long batch, double* part,
+                       double* out, cudaStream_t st);
+cudaError_t launch_cgls_xr(double* x, double* r, const double* p, const double* q, long long nx, long long nr,
+                           long long batch, const double* gam, const double* qq, const int* active,
+                           cudaStream_t st);
+cudaError_t launch_cgls_p(double* p, const double* s, long long nx, long long batch, const double* gnew,
+                          const double* gold, cudaStream_t st);
+cudaError_t launch_cgls_flags(const double* gam, const double* s0, double tol, int* active, long long batch,
+                              cudaStream_t st);
+cudaError_t launch_sqrt(const double* a, double* out, long long batch, cudaStream_t st);
+cudaError_t launch_sub_from(double* r, const double* y, long long n, cudaStream_t st);
 // Sampling-mask epilogues: gather y[b][i] = full[b][idx[i]] (scatter = false) or
 // scatter full[b][idx[i]] = y[b][i] (scatter = true; full pre-zeroed).
 cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long long cnt, double* y,
