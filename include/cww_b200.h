@@ -20,6 +20,7 @@
  *   sequency_to_natural_index (walsh.hpp)       :60-62     cww_sequency_perm
  *   walsh_sign_row (walsh.hpp)                  :66        cww_walsh_sign_rows
  *   compute_kernel_table (kernel.hpp)           :46-47     cww_op_kernel_table
+ *   save/load_kernel_table, get_kernel_table    :49-60     cww_kernel_table_save/_load, desc.cache_dir
  *   CwwError (std::runtime_error) thrown        wavelet.hpp:11-13  -> cww_status + cww_last_error()
  *
  * All arithmetic is IEEE fp64.  Batches are batch-major and contiguous: item b
@@ -76,6 +77,11 @@ typedef struct {
      * gathers the masked rows, adjoint scatters into zeros first. */
     const uint64_t* mask;
     size_t mask_len;
+    /* Kernel-table cache directory (get_kernel_table, kernel.cpp:173-198):
+     * NULL/"" = $CWW_CACHE_DIR, else no cache.  A valid matching CWWK file is
+     * loaded instead of recomputing the table; otherwise the table is computed
+     * and written back. */
+    const char* cache_dir;
 } cww_op_desc;
 
 typedef struct cww_op cww_op;
@@ -100,6 +106,17 @@ cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* 
  * of a least-squares / CG loop).  work: NULL or batch*output_size doubles. */
 cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work,
                       size_t work_len, size_t batch, int iters, void* stream);
+
+/* Kernel-table cache files (CWWK, kernel.cpp:79-164; device-free).  save:
+ * compute the table of (family, nu, boundary, q, R; R <= 0 = 14) from the
+ * filter data and write it (save_kernel_table).  load: read and validate
+ * (CRC, magic, version, shapes -- the reference's messages); header[5] =
+ * family, nu, boundary, q, R; counts[3] = interior/left/right lengths (always
+ * written); arrays copied when non-NULL (CWW_ERR_DIMENSION if too small). */
+cww_status cww_kernel_table_save(int family, int nu, int boundary, unsigned q, int resolution,
+                                 const char* data_dir, const char* path);
+cww_status cww_kernel_table_load(const char* path, int* header, double* interior, size_t ni, double* left,
+                                 size_t nl, double* right, size_t nr, size_t* counts);
 
 /* Least-squares reconstruction (generalised sampling, the reference spec's
  * gs_solve; its src/reconstruct.cpp is empty): CGLS on the

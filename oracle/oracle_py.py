@@ -238,6 +238,10 @@ class Reference:
         L.ref_haar_fullrank.argtypes = [C.c_uint, _dp, _dp, C.c_int]
         L.ref_composed_masked.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int,
                                           _dp, _dp]
+        L.ref_kernel_cache_save.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p,
+                                            C.c_char_p]
+        L.ref_kernel_cache_load.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.POINTER(C.c_size_t)]
         L.ref_bench.restype = C.c_double
         L.ref_bench.argtypes = [C.c_void_p, C.c_int, _dp, _dp, C.c_size_t, C.c_int, C.c_int,
                                 C.c_int]
@@ -273,6 +277,20 @@ class Reference:
         self._check(self.L.ref_dwt(family, nu, boundary, j, _ptr(d), int(inverse), min_level,
                                    dim, DATA_DIR.encode()))
         return d
+
+    def kernel_cache_save(self, family, nu, boundary, q, path, R=14):
+        """The reference's save_kernel_table of its own computed table."""
+        self._check(self.L.ref_kernel_cache_save(family, nu, boundary, q, R, DATA_DIR.encode(),
+                                                 path.encode()))
+
+    def kernel_cache_load(self, path):
+        """The reference's load_kernel_table: (header, interior, left, right)."""
+        hdr = (C.c_int * 5)()
+        cnt = (C.c_size_t * 3)()
+        big = [np.empty(1 << 16) for _ in range(3)]
+        self._check(self.L.ref_kernel_cache_load(path.encode(), hdr, big[0].ctypes.data, big[1].ctypes.data,
+                                                 big[2].ctypes.data, cnt))
+        return list(hdr), big[0][:cnt[0]].copy(), big[1][:cnt[1]].copy(), big[2][:cnt[2]].copy()
 
     def kernel_table(self, family, nu, boundary, q, R=14):
         W, S = 2 * nu - 1, 1 << q

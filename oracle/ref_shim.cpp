@@ -176,6 +176,37 @@ int ref_kernel_table(int family, int nu, int boundary, int q, int R, const char*
     });
 }
 
+// CWWK cache files through the reference's own save/load (kernel.cpp:79-164)
+int ref_kernel_cache_save(int family, int nu, int boundary, int q, int R, const char* data_dir,
+                          const char* path) {
+    return guarded([&] {
+        FilterSet f = load_filters(fam(family), nu, data_dir ? data_dir : "");
+        KernelTable t = compute_kernel_table(f, bnd(boundary), q, R);
+        t.family = fam(family);
+        t.nu = nu;
+        save_kernel_table(t, path);
+    });
+}
+
+// header[5] = family, nu, boundary, q, R; counts[3]; arrays sized by the caller
+int ref_kernel_cache_load(const char* path, int* header, double* interior, double* left, double* right,
+                          std::size_t* counts) {
+    return guarded([&] {
+        KernelTable t = load_kernel_table(path);
+        header[0] = t.family == Family::Daubechies ? 0 : 1;
+        header[1] = t.nu;
+        header[2] = t.boundary == Boundary::Periodic ? 0 : 1;
+        header[3] = t.q;
+        header[4] = t.R;
+        counts[0] = t.interior.size();
+        counts[1] = t.left.size();
+        counts[2] = t.right.size();
+        if (interior) std::memcpy(interior, t.interior.data(), t.interior.size() * 8);
+        if (left && !t.left.empty()) std::memcpy(left, t.left.data(), t.left.size() * 8);
+        if (right && !t.right.empty()) std::memcpy(right, t.right.data(), t.right.size() * 8);
+    });
+}
+
 // ---- fastop.hpp -----------------------------------------------------------
 void* ref_op_create(int family, int nu, int boundary, unsigned j, unsigned q, int dim,
                     int min_level, const char* data_dir) {

@@ -68,7 +68,7 @@ class _Desc(C.Structure):
     _fields_ = [("family", C.c_int), ("nu", C.c_int), ("boundary", C.c_int), ("j", C.c_uint),
                 ("q", C.c_uint), ("dim", C.c_int), ("min_level", C.c_int), ("use_idwt", C.c_int),
                 ("kernel_resolution", C.c_int), ("device", C.c_int), ("data_dir", C.c_char_p),
-                ("mask", C.c_void_p), ("mask_len", C.c_size_t)]
+                ("mask", C.c_void_p), ("mask_len", C.c_size_t), ("cache_dir", C.c_char_p)]
 
 
 _lib = None
@@ -242,13 +242,14 @@ class LinearOp:
 class _Handle:
     def __init__(self, spec: WaveletSpec, j: int, q: int, dim: int, min_level: int, use_idwt: bool,
                  kernel_resolution: int = 0, device: Optional[int] = None,
-                 data_dir: Optional[str] = None, mask: Optional[np.ndarray] = None):
+                 data_dir: Optional[str] = None, mask: Optional[np.ndarray] = None,
+                 cache_dir: Optional[str] = None):
         L = _load()
         m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint64)
         d = _Desc(int(spec.family), spec.nu, int(spec.boundary), j, q, dim, min_level,
                   1 if use_idwt else 0, kernel_resolution, -1 if device is None else device,
                   (data_dir or DATA_DIR).encode(), None if m is None else m.ctypes.data,
-                  0 if m is None else m.size)
+                  0 if m is None else m.size, None if cache_dir is None else cache_dir.encode())
         h = C.c_void_p()
         _check(L.cww_op_create(C.byref(d), C.byref(h)))
         self.h = h
@@ -309,12 +310,13 @@ class FastOp:
 
     def __init__(self, spec: WaveletSpec, j: int, q: int, dim: int = 1, *,
                  kernel_resolution: int = 0, device: Optional[int] = None,
-                 data_dir: Optional[str] = None):
+                 data_dir: Optional[str] = None, cache_dir: Optional[str] = None):
         spec.validate()
         if spec.nu < 2:
             raise CwwError("FastOp requires nu >= 2; use HaarFullRankOp for Haar", 3)
         self._spec, self._j, self._q, self._dim = spec, int(j), int(q), int(dim)
-        self._opts = dict(kernel_resolution=kernel_resolution, device=device, data_dir=data_dir)
+        self._opts = dict(kernel_resolution=kernel_resolution, device=device, data_dir=data_dir,
+                          cache_dir=cache_dir)
         self._h = _Handle(spec, self._j, self._q, self._dim, -1, False, **self._opts)
 
     def M(self) -> int:
@@ -511,6 +513,38 @@ def gs_solve(op, y, residual_tol: float = 1e-10, max_iters: int = 1000, x0=None,
     if rc != 0 and (raise_on_fail or rc != 9):
         _check(rc)
     return x, it.value, res
+
+
+def kernel_table_save(spec: WaveletSpec, q: int, path: str, resolution: int = 14,
+                      data_dir: Optional[str] = None) -> None:
+    """save_kernel_table (kernel.cpp:95-117): compute the kappa tables of
+    (spec, q, R) and write a CWWK cache file (host only, no device)."""
+    L = _load()
+    L.cww_kernel_table_save.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint, C.c_int, C.c_char_p, C.c_char_p]
+    _check(L.cww_kernel_table_save(int(spec.family), spec.nu, int(spec.boundary), int(q), int(resolution),
+                                   (data_dir or DATA_DIR).encode(), path.encode()))
+
+
+def kernel_table_load(path: str) -> dict:
+    """load_kernel_table (kernel.cpp:119-164): read and validate a CWWK file
+    (CRC, magic, version, shapes).  Returns header fields and the arrays."""
+    L = _load()
+    dp, sz = C.c_void_p, C.c_size_t
+    L.cww_kernel_table_load.argtypes = [C.c_char_p, C.POINTER(C.c_int), dp, sz, dp, sz, dp, sz,
+                                        C.POINTER(C.c_size_t)]
+    hdr = (C.c_int * 5)()
+    cnt = (C.c_size_t * 3)()
+    _check(L.cww_kernel_table_load(path.encode(), hdr, None, 0, None, 0, None, 0, cnt))
+    it, le, ri = (np.empty(int(cnt[k])) for k in range(3))
+    _check(L.cww_kernel_table_load(path.encode(), hdr, _np_ptr(it), it.size, _np_ptr(le), le.size,
+                                   _np_ptr(ri), ri.size, cnt))
+    return {"family": hdr[0], "nu": hdr[1], "boundary": hdr[2], "q": hdr[3], "R": hdr[4],
+            "interior": it, "left": le, "right": ri}
+
+
+def kernel_cache_filename(spec: WaveletSpec, q: int, resolution: int = 14) -> str:
+    """kernel_cache_filename (kernel.cpp:161-165)."""
+    return f"cwwk_{spec.name()}_{'periodic' if spec.boundary == Boundary.Periodic else 'vmp'}_q{q}_R{resolution}_v1.bin"
 
 
 def _dev_tensor(v, what):

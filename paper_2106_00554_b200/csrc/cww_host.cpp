@@ -312,6 +312,140 @@ cww_status kernel_table(const Filters& f, int vmp, int q, int R, KernelTable& t)
     return CWW_OK;
 }
 
+// ---- kernel-table cache: CWWK files (kernel.cpp:79-198) --------------------
+// "CWWK" | u32 version (1) | u32 family | u32 nu | u32 boundary | u32 q | u32 R
+// | 3 x (u32 count, count f64: interior, left, right) | u32 CRC-32 of all
+// preceding bytes; little-endian, as the reference writes it.
+constexpr uint32_t kCwwkVersion = 1;
+
+struct CwwkHeader {
+    int family = 0, nu = 0, vmp = 0, q = 0, R = 0;
+};
+
+std::string cwwk_filename(int family, int nu, int vmp, int q, int R) {
+    return std::string("cwwk_") + (family == 0 ? "db" : "sym") + std::to_string(nu) + "_" +
+           (vmp ? "vmp" : "periodic") + "_q" + std::to_string(q) + "_R" + std::to_string(R) + "_v" +
+           std::to_string(kCwwkVersion) + ".bin";
+}
+
+cww_status cwwk_save(const KernelTable& t, const CwwkHeader& h, const std::string& path) {
+    std::vector<unsigned char> b;
+    auto put = [&](const void* p, size_t n) {
+        const auto* c = static_cast<const unsigned char*>(p);
+        b.insert(b.end(), c, c + n);
+    };
+    auto u32 = [&](uint32_t v) { put(&v, 4); };
+    auto arr = [&](const std::vector<double>& a) {
+        u32(uint32_t(a.size()));
+        put(a.data(), a.size() * 8);
+    };
+    put("CWWK", 4);
+    u32(kCwwkVersion);
+    u32(uint32_t(h.family));
+    u32(uint32_t(h.nu));
+    u32(uint32_t(h.vmp));
+    u32(uint32_t(h.q));
+    u32(uint32_t(h.R));
+    arr(t.interior);
+    arr(t.left);
+    arr(t.right);
+    const uint32_t crc = crc32_zlib(b.data(), b.size());
+    u32(crc);
+    FILE* fp = std::fopen(path.c_str(), "wb");
+    if (!fp) return fail(CWW_ERR_DATA_IO, "cannot write kernel cache: %s", path.c_str());
+    const size_t w = std::fwrite(b.data(), 1, b.size(), fp);
+    const int c = std::fclose(fp);
+    if (w != b.size() || c != 0) return fail(CWW_ERR_DATA_IO, "short write to kernel cache: %s", path.c_str());
+    return CWW_OK;
+}
+
+cww_status cwwk_load(const std::string& path, KernelTable& t, CwwkHeader& h) {
+    FILE* fp = std::fopen(path.c_str(), "rb");
+    if (!fp) return fail(CWW_ERR_DATA_IO, "cannot open kernel cache: %s", path.c_str());
+    std::vector<unsigned char> b;
+    unsigned char buf[4096];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) b.insert(b.end(), buf, buf + got);
+    std::fclose(fp);
+    if (b.size() < 32) return fail(CWW_ERR_DATA_IO, "truncated kernel cache: %s", path.c_str());
+    uint32_t stored;
+    std::memcpy(&stored, b.data() + b.size() - 4, 4);
+    if (crc32_zlib(b.data(), b.size() - 4) != stored)
+        return fail(CWW_ERR_DATA_IO, "checksum failure in kernel cache: %s", path.c_str());
+    if (std::memcmp(b.data(), "CWWK", 4) != 0)
+        return fail(CWW_ERR_DATA_IO, "bad magic in kernel cache: %s", path.c_str());
+    size_t pos = 4;
+    const size_t end = b.size() - 4;
+    auto u32 = [&]() {
+        uint32_t v = 0;
+        if (pos + 4 <= end) std::memcpy(&v, b.data() + pos, 4);
+        pos += 4;
+        return v;
+    };
+    if (u32() != kCwwkVersion) return fail(CWW_ERR_DATA_IO, "kernel cache version mismatch: %s", path.c_str());
+    h.family = int(u32());
+    h.nu = int(u32());
+    h.vmp = int(u32());
+    h.q = int(u32());
+    h.R = int(u32());
+    auto arr = [&](std::vector<double>& a) {
+        const uint32_t n = u32();
+        if (pos > end || pos + size_t(n) * 8 > end) return false;
+        a.resize(n);
+        std::memcpy(a.data(), b.data() + pos, size_t(n) * 8);
+        pos += size_t(n) * 8;
+        return true;
+    };
+    if (!arr(t.interior) || !arr(t.left) || !arr(t.right))
+        return fail(CWW_ERR_DATA_IO, "truncated kernel cache payload: %s", path.c_str());
+    if (h.nu < 1 || h.nu > 6 || h.q < 0 || h.q > 20)
+        return fail(CWW_ERR_DATA_IO, "kernel cache shape mismatch (header): %s", path.c_str());
+    const size_t W = size_t(2 * h.nu - 1), S = size_t(1) << h.q;
+    if (t.interior.size() != W * S)
+        return fail(CWW_ERR_DATA_IO, "kernel cache shape mismatch (interior): %s", path.c_str());
+    const size_t edge = h.vmp ? size_t(h.nu) * W * S : 0;
+    if (t.left.size() != edge || t.right.size() != edge)
+        return fail(CWW_ERR_DATA_IO, "kernel cache shape mismatch (edge): %s", path.c_str());
+    return CWW_OK;
+}
+
+// get_kernel_table (kernel.cpp:173-198): a valid, matching cache file is
+// used; a missing / corrupt one is recomputed silently, a stale one with a
+// note; the computed table is written back (failures noted, not fatal).
+cww_status cached_kernel_table(const Filters& f, int family, int vmp, int q, int R, const std::string& dir,
+                               KernelTable& t) {
+    std::string path;
+    if (!dir.empty()) {
+        path = dir + "/" + cwwk_filename(family, f.nu, vmp, q, R);
+        KernelTable c;
+        CwwkHeader h;
+        const std::string saved = g_err;
+        if (cwwk_load(path, c, h) == CWW_OK) {
+            if (h.family == family && h.nu == f.nu && h.vmp == vmp && h.q == q && h.R == R) {
+                t = std::move(c);
+                return CWW_OK;
+            }
+            std::fprintf(stderr, "cww: stale kernel cache %s, recomputing\n", path.c_str());
+        }
+        g_err = saved;
+    }
+    cww_status s = kernel_table(f, vmp, q, R, t);
+    if (s != CWW_OK || path.empty()) return s;
+    CwwkHeader h{family, f.nu, vmp, q, R};
+    const std::string saved = g_err;
+    if (cwwk_save(t, h, path) != CWW_OK) {
+        std::fprintf(stderr, "cww: %s (continuing without cache)\n", g_err.c_str());
+        g_err = saved;
+    }
+    return CWW_OK;
+}
+
+std::string cache_dir_of(const char* flag) {  // resolve_cache_dir (kernel.cpp:167-171)
+    if (flag && *flag) return flag;
+    if (const char* e = std::getenv("CWW_CACHE_DIR"); e && *e) return e;
+    return "";
+}
+
 std::string default_data_dir() {
     if (const char* e = std::getenv("CWW_DATA_DIR"); e && *e) return e;
 #ifdef CWW_DEFAULT_DATA_DIR
@@ -998,6 +1132,7 @@ void cww_op_desc_init(cww_op_desc* d) {
     d->data_dir = nullptr;
     d->mask = nullptr;
     d->mask_len = 0;
+    d->cache_dir = nullptr;
 }
 
 cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
@@ -1038,7 +1173,9 @@ cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
     CUDA_TRY(cudaSetDevice(op->device));
     if ((s = load_filters(desc->family, desc->nu, op->data_dir.c_str(), op->f)) != CWW_OK) return s;
     int R = desc->kernel_resolution > 0 ? desc->kernel_resolution : 14;
-    if ((s = kernel_table(op->f, desc->boundary, int(desc->q), R, op->kt)) != CWW_OK) return s;
+    if ((s = cached_kernel_table(op->f, desc->family, desc->boundary, int(desc->q), R,
+                                 cache_dir_of(desc->cache_dir), op->kt)) != CWW_OK)
+        return s;
     build_edge_terms(*op);
     if ((s = build_tables(*op)) != CWW_OK) return s;
     op->full_out = op->dim == 2 ? op->N * op->N : op->N;
@@ -1051,7 +1188,9 @@ cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
                                 cudaMemcpyHostToDevice));
         }
     }
-    op->d.mask = nullptr;  // the caller's array is not retained
+    op->d.mask = nullptr;  // the caller's arrays / strings are not retained
+    op->d.cache_dir = nullptr;
+    op->d.data_dir = nullptr;
     // keep freed workspace in the stream-ordered pool between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, op->device) == cudaSuccess) {
@@ -1256,6 +1395,49 @@ cww_status cww_gs_solve(const cww_op* op, const double* y, size_t y_len, double*
     CUDA_TRY(cudaSetDevice(op->device));
     return gs_solve(op, y, x, (long long)batch, residual_tol, max_iters, use_x0 != 0, iters, residuals,
                     S_(stream));
+}
+
+cww_status cww_kernel_table_save(int family, int nu, int boundary, unsigned q, int resolution,
+                                 const char* data_dir, const char* path) {
+    if (!path) return fail(CWW_ERR_INVALID_ARG, "null path");
+    if (nu < 1 || nu > 6 || family < 0 || family > 1 || boundary < 0 || boundary > 1 || q > 20)
+        return fail(CWW_ERR_SPEC, "unsupported kernel table spec");
+    if (q < 1) return fail(CWW_ERR_SPEC, "kernel table requires q >= 1");  // kernel.cpp:32-33
+    if (nu < 2) return fail(CWW_ERR_SPEC, "kernel tables are for nu >= 2 (Haar uses the FWHT/DWT composition)");
+    Filters f;
+    cww_status s = load_filters(family, nu, data_dir, f);
+    if (s != CWW_OK) return s;
+    const int R = resolution > 0 ? resolution : 14;
+    KernelTable t;
+    if ((s = kernel_table(f, boundary, int(q), R, t)) != CWW_OK) return s;
+    return cwwk_save(t, CwwkHeader{family, nu, boundary, int(q), R}, path);
+}
+
+cww_status cww_kernel_table_load(const char* path, int* header, double* interior, size_t ni, double* left,
+                                 size_t nl, double* right, size_t nr, size_t* counts) {
+    if (!path) return fail(CWW_ERR_INVALID_ARG, "null path");
+    KernelTable t;
+    CwwkHeader h;
+    cww_status s = cwwk_load(path, t, h);
+    if (s != CWW_OK) return s;
+    if (header) {
+        header[0] = h.family;
+        header[1] = h.nu;
+        header[2] = h.vmp;
+        header[3] = h.q;
+        header[4] = h.R;
+    }
+    if (counts) {
+        counts[0] = t.interior.size();
+        counts[1] = t.left.size();
+        counts[2] = t.right.size();
+    }
+    if ((interior && ni < t.interior.size()) || (left && nl < t.left.size()) || (right && nr < t.right.size()))
+        return fail(CWW_ERR_DIMENSION, "kernel table buffers too small");
+    if (interior) std::memcpy(interior, t.interior.data(), t.interior.size() * 8);
+    if (left) std::memcpy(left, t.left.data(), t.left.size() * 8);
+    if (right) std::memcpy(right, t.right.data(), t.right.size() * 8);
+    return CWW_OK;
 }
 
 cww_status cww_forward_host(const cww_op* op, const double* x, size_t x_len, double* y,

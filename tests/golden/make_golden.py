@@ -30,6 +30,9 @@ CASES = [
 MASKED = [(0, 2, 1, 5, 1, 1, 0.25), (0, 4, 1, 6, 2, 1, 0.1), (1, 3, 0, 6, 1, 1, 0.5),
           (0, 3, 1, 4, 1, 2, 0.2)]
 
+# kernel-cache fixtures (family, nu, boundary, q)
+CWWK = [(0, 2, 1, 1), (1, 3, 0, 3), (0, 4, 1, 2)]
+
 
 def main():
     o, r = Oracle(), Reference()
@@ -85,6 +88,10 @@ def main():
             out[k + f"_fwd{use}"] = op.masked(mask, x, adjoint=False, use_idwt=use)
             out[k + f"_adj{use}"] = op.masked(mask, y, adjoint=True, use_idwt=use)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
+    # CWWK kernel-cache files written by the reference's save_kernel_table
+    for fam, nu, bnd, q in CWWK:
+        name = f"cwwk_{'db' if fam == 0 else 'sym'}{nu}_{'vmp' if bnd else 'periodic'}_q{q}_R14_v1.bin"
+        r.kernel_cache_save(fam, nu, bnd, q, os.path.join(HERE, name))
     print("wrote", len(out), "arrays")
 
 

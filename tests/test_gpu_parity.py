@@ -3,6 +3,8 @@ the same seeded inputs.  Tolerance: relative L2 <= 1e-12 (fp64, BASELINE.json
 north_star); index / permutation / sign tables bit-exact.  At the full
 BASELINE sizes the size-independent properties (adjoint identity, linearity,
 normal operator) are checked, plus one full-size vector against the oracle."""
+import os
+
 import numpy as np
 import pytest
 
@@ -312,3 +314,30 @@ def test_dimension_mismatch_raises(cuda):
     op = make(0, 2, 1, 5, 1)
     with pytest.raises(cw.CwwError):
         op.forward(gpu(np.zeros(33)))
+
+
+# ---- kernel-table cache on op creation (get_kernel_table, kernel.cpp:173-198) ----
+def test_op_uses_kernel_cache(orc, cuda, tmp_path):
+    import struct
+    import zlib
+    cw = _cw()
+    spec = cw.WaveletSpec(cw.Family.Daubechies, 4, cw.Boundary.Vmp)
+    path = tmp_path / cw.kernel_cache_filename(spec, 2)
+    op = cw.FastOp(spec, 6, 2, cache_dir=str(tmp_path))  # miss: computed and written back
+    assert path.exists()
+    gold = os.path.join(os.path.dirname(__file__), "golden", "cwwk_db4_vmp_q2_R14_v1.bin")
+    assert path.read_bytes() == open(gold, "rb").read()
+    it0 = op.kernel_table()[0]
+    # a valid file with different values is loaded instead of recomputing
+    body = bytearray(path.read_bytes()[:-4])
+    v = struct.unpack_from("<d", body, 32)[0]
+    struct.pack_into("<d", body, 32, v + 1.0)
+    path.write_bytes(bytes(body) + struct.pack("<I", zlib.crc32(bytes(body)) & 0xFFFFFFFF))
+    it1 = cw.FastOp(spec, 6, 2, cache_dir=str(tmp_path)).kernel_table()[0]
+    assert it1.ravel()[0] == it0.ravel()[0] + 1.0
+    # stale header (R != 14): recomputed and rewritten
+    struct.pack_into("<I", body, 24, 12)
+    path.write_bytes(bytes(body) + struct.pack("<I", zlib.crc32(bytes(body)) & 0xFFFFFFFF))
+    it2 = cw.FastOp(spec, 6, 2, cache_dir=str(tmp_path)).kernel_table()[0]
+    assert np.array_equal(it2, it0)
+    assert path.read_bytes() == open(gold, "rb").read()
