@@ -372,6 +372,10 @@ class FastOp:
         self._dim_guard(2, "adjoint_2d")
         return self.adjoint(y, x)
 
+    def normal(self, x, iters: int = 1, work=None):
+        """x <- (U* U)^iters x in place on a CUDA tensor (banded normal form)."""
+        return _normal(self._h, x, iters, work)
+
     def kernel_table(self):
         """(interior, left, right) in the reference layout (kernel.hpp:23-38)."""
         nu, S = self._spec.nu, 1 << self._q
@@ -446,17 +450,20 @@ class ComposedOp(LinearOp):
     def normal(self, x, iters: int = 1, work=None):
         """x <- (A* A)^iters x in place on a CUDA tensor (the CG / least-squares
         inner loop; config 5).  work: optional output_size buffer."""
-        torch = _torch()
-        if not (_is_tensor(x) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()):
-            raise CwwError("normal() needs a contiguous float64 CUDA tensor", 1)
-        batch = x.numel() // self._h.nin
-        wp, wn = (0, 0) if work is None else (work.data_ptr(), work.numel())
-        _check(self._h.L.cww_normal(self._h.h, x.data_ptr(), x.numel(), wp, wn, batch, int(iters),
-                                    _stream_ptr(x)))
-        return x
+        return _normal(self._h, x, iters, work)
 
     def handle(self):
         return self._h
+
+
+def _normal(h, x, iters, work):
+    torch = _torch()
+    if not (_is_tensor(x) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()):
+        raise CwwError("normal() needs a contiguous float64 CUDA tensor", 1)
+    batch = x.numel() // h.nin
+    wp, wn = (0, 0) if work is None else (work.data_ptr(), work.numel())
+    _check(h.L.cww_normal(h.h, x.data_ptr(), x.numel(), wp, wn, batch, int(iters), _stream_ptr(x)))
+    return x
 
 
 class HaarFullRankOp(LinearOp):
@@ -480,6 +487,10 @@ class HaarFullRankOp(LinearOp):
 
     def adjoint(self, y, x=None):
         return self._h._apply(y, x, True)
+
+    def normal(self, x, iters: int = 1, work=None):
+        """x <- (A* A)^iters x in place on a CUDA tensor."""
+        return _normal(self._h, x, iters, work)
 
     def handle(self):
         return self._h

@@ -14,7 +14,8 @@ namespace cww {
     long long small_smem_nu##N(int, int, int, bool, bool);                                \
     cudaError_t launch_large_nu##N(int, const LargeArgs&, cudaStream_t);            \
     cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);                    \
-    cudaError_t launch_pyr_nu##N(bool, const PyrArgs&, cudaStream_t);
+    cudaError_t launch_pyr_nu##N(bool, const PyrArgs&, cudaStream_t);               \
+    cudaError_t launch_normal_rows_nu##N(const NormArgs&, cudaStream_t);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6)
 #undef DECL
 
@@ -87,6 +88,41 @@ cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long
         const long long nb = batch - b0 < 65535 ? batch - b0 : 65535;
         k_mask<<<dim3((unsigned)blocks, (unsigned)nb), 256, 0, st>>>(full + b0 * nfull, nfull, idx, cnt,
                                                                      y + b0 * cnt, scatter ? 1 : 0);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st) {
+#define C(N) launch_normal_rows_nu##N(a, st)
+    SWITCH_NU(nu, C)
+#undef C
+    return cudaErrorInvalidValue;
+}
+
+// 32 x 32 tiles through shared memory (odd row stride: conflict-free both ways)
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, long long n) {
+    __shared__ double tile[32][33];
+    const long long base = (long long)blockIdx.z * n * n;
+    const long long bx = (long long)blockIdx.x * 32, by = (long long)blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+#pragma unroll
+    for (int r = 0; r < 32; r += 8) {
+        const long long row = by + ty + r, col = bx + tx;
+        if (row < n && col < n) tile[ty + r][tx] = in[base + row * n + col];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 32; r += 8) {
+        const long long row = bx + ty + r, col = by + tx;
+        if (row < n && col < n) out[base + row * n + col] = tile[tx][ty + r];
+    }
+}
+
+cudaError_t launch_transpose(const double* in, double* out, long long n, long long batch, cudaStream_t st) {
+    const unsigned g = (unsigned)((n + 31) / 32);
+    for (long long b0 = 0; b0 < batch; b0 += 65535) {
+        const long long nb = batch - b0 < 65535 ? batch - b0 : 65535;
+        k_transpose<<<dim3(g, g, (unsigned)nb), dim3(32, 8), 0, st>>>(in + b0 * n * n, out + b0 * n * n, n);
     }
     return cudaGetLastError();
 }

@@ -591,6 +591,14 @@ struct cww_op {
     uint64_t* d_mask = nullptr;
     bool masked = false;
     long long full_out = 0;  // output size of the unmasked operator
+    // banded normal form G = U* U along one axis (built on first use)
+    struct Gram {
+        std::once_flag once;
+        bool ok = false;
+        int E = 0, b = 0;
+        double* d = nullptr;
+    };
+    std::shared_ptr<Gram> gram = std::make_shared<Gram>();
 };
 
 namespace {
@@ -1205,6 +1213,7 @@ cww_status cww_op_destroy(cww_op* op) {
     if (!op) return CWW_OK;
     if (op->d_tab) cudaFree(op->d_tab);
     if (op->d_mask) cudaFree(op->d_mask);
+    if (op->gram->d) cudaFree(op->gram->d);
     delete op;
     return CWW_OK;
 }
@@ -1248,6 +1257,144 @@ cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* 
     return run(op, y, x, (long long)batch, true, S_(stream));
 }
 
+// ---- banded normal form (U* U along one axis) -----------------------------
+// Probes G = U* U with the op's own FastOp kernels on unit vectors: the
+// first / last E columns, one interior column, and two verification columns.
+// G is symmetric, so probed column i gives row i's band.  Rows outside the
+// edge strips must equal the interior (Toeplitz) row, else the normal form is
+// not used (the op falls back to forward + adjoint).
+void build_gram(const cww_op* op) {
+    const long long M = op->M;
+    const int b = 2 * op->nu - 2, w = 2 * b + 1;
+    if (M < 4 * (b + 2) || M < 64) return;
+    cww_op u = *op;  // the plain 1D FastOp over the same device tables
+    u.d.use_idwt = 0;
+    u.dim = 1;
+    u.masked = false;
+    const bool wrap = !op->vmp;
+    int E = std::min<long long>(6 * op->nu + 4, M / 4);
+    std::vector<long long> cols;
+    for (int i = 0; i < E; ++i) cols.push_back(i);
+    for (int i = 0; i < E; ++i) cols.push_back(M - E + i);
+    cols.push_back(M / 2);
+    cols.push_back(E);
+    cols.push_back(M - E - 1);
+    const long long nc = (long long)cols.size(), N = op->N;
+    std::vector<double> band(size_t(nc) * w, 0.0);
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
+    const long long chunk = std::max<long long>(1, std::min<long long>(nc, (256ll << 20) / (8 * (N + M))));
+    double *e = nullptr, *f = nullptr;
+    bool good = cudaMallocAsync(&e, size_t(chunk * M) * 8, st) == cudaSuccess &&
+                cudaMallocAsync(&f, size_t(chunk * N) * 8, st) == cudaSuccess;
+    for (long long c0 = 0; good && c0 < nc; c0 += chunk) {
+        const long long cn = std::min(chunk, nc - c0);
+        good = cudaMemsetAsync(e, 0, size_t(cn * M) * 8, st) == cudaSuccess;
+        const double one = 1.0;
+        for (long long c = 0; good && c < cn; ++c)
+            good = cudaMemcpyAsync(e + c * M + cols[size_t(c0 + c)], &one, 8, cudaMemcpyHostToDevice, st) ==
+                   cudaSuccess;
+        good = good && run_1d(&u, e, f, cn, false, st) == CWW_OK && run_1d(&u, f, e, cn, true, st) == CWW_OK;
+        for (long long c = 0; good && c < cn; ++c) {
+            const long long k = cols[size_t(c0 + c)];
+            for (int d = 0; d < w && good; ++d) {
+                long long i = k + d - b;
+                if (wrap) i &= M - 1;
+                else if (i < 0 || i >= M) continue;
+                good = cudaMemcpyAsync(&band[size_t((c0 + c) * w + d)], e + c * M + i, 8, cudaMemcpyDeviceToHost,
+                                       st) == cudaSuccess;
+            }
+        }
+        good = good && cudaStreamSynchronize(st) == cudaSuccess;
+    }
+    if (e) cudaFreeAsync(e, st);
+    if (f) cudaFreeAsync(f, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    cudaGetLastError();
+    if (!good) return;
+    // verification columns E and M-E-1 against the interior row
+    const double* gI = &band[size_t(2 * E) * w];
+    double mx = 0.0;
+    for (int d = 0; d < w; ++d) mx = std::max(mx, std::fabs(gI[d]));
+    for (int v = 1; v <= 2; ++v)
+        for (int d = 0; d < w; ++d)
+            if (std::fabs(band[size_t((2 * E + v) * w + d)] - gI[d]) > 1e-12 * mx) return;
+    // band rows: column k probed = row k (symmetry): entry d multiplies x[k + d - b]
+    std::vector<double> tab(size_t(2 * E + 1) * w);
+    std::copy(band.begin(), band.begin() + size_t(2 * E + 1) * w, tab.begin());
+    double* d = nullptr;
+    if (cudaMalloc(&d, tab.size() * 8) != cudaSuccess) return;
+    if (cudaMemcpy(d, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return;
+    }
+    op->gram->d = d;
+    op->gram->E = E;
+    op->gram->b = b;
+    op->gram->ok = true;
+}
+
+cww::NormArgs norm_args(const cww_op* op, double* x, long long nvec) {
+    cww::NormArgs a{};
+    a.tab = op->d_tab;
+    a.t = op->tabs;
+    a.band = op->gram->d;
+    a.E = op->gram->E;
+    a.b = op->gram->b;
+    a.in = x;
+    a.out = x;
+    a.in_vs = a.out_vs = op->M;
+    a.nvec = nvec;
+    a.j = int(op->j);
+    a.r0 = op->r0;
+    a.use_idwt = op->d.use_idwt;
+    a.vmp = op->vmp;
+    a.V = int(std::max<long long>(1, 4096 / op->M));
+    return a;
+}
+
+// x <- (A* A)^iters x with the banded form along every axis.  1D: rows in
+// place.  2D (A* A = N1 (x) N1): each iteration applies N1 to the rows,
+// transposes, applies N1 to the rows again -- the result is transposed, so
+// iterations alternate between x and the work buffer and an odd count ends
+// with one transpose back.
+cww_status normal_banded(const cww_op* op, double* x, double* w, long long batch, int iters, cudaStream_t st) {
+    const long long M = op->M;
+    if (op->dim == 1) {
+        cww::NormArgs a = norm_args(op, x, batch);
+        for (int it = 0; it < iters; ++it) {
+            Prof pr("normal_rows", st);
+            CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
+        }
+        return CWW_OK;
+    }
+    double* cur = x;
+    double* oth = w;
+    for (int it = 0; it < iters; ++it) {
+        cww::NormArgs a = norm_args(op, cur, batch * M);
+        {
+            Prof pr("normal_rows", st);
+            CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
+        }
+        {
+            Prof pr("transpose", st);
+            CUDA_TRY(cww::launch_transpose(cur, oth, M, batch, st));
+        }
+        a = norm_args(op, oth, batch * M);
+        {
+            Prof pr("normal_rows", st);
+            CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
+        }
+        std::swap(cur, oth);  // cur now holds (A* A x)^T of the iterate, or the iterate itself after two
+    }
+    if (cur != x) {  // odd iteration count: result is transposed in w
+        Prof pr("transpose", st);
+        CUDA_TRY(cww::launch_transpose(cur, x, M, batch, st));
+    }
+    return CWW_OK;
+}
+
 cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work, size_t work_len,
                       size_t batch, int iters, void* stream) {
     if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
@@ -1261,6 +1408,15 @@ cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work, s
     if (!w) {
         CUDA_TRY(wb.alloc(no * batch, st));
         w = wb.p;
+    }
+    CUDA_TRY(cudaSetDevice(op->device));
+    static const bool no_banded = [] {
+        const char* e = std::getenv("CWW_NORMAL_EXPLICIT");
+        return e && e[0] == '1';
+    }();
+    if (!op->masked && !no_banded && op->M <= 4096) {
+        std::call_once(op->gram->once, [op] { build_gram(op); });
+        if (op->gram->ok) return normal_banded(op, x, w, (long long)batch, iters, st);
     }
     for (int it = 0; it < iters; ++it) {
         cww_status s = run(op, x, w, (long long)batch, false, st);

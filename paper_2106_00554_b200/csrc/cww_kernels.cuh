@@ -1103,6 +1103,142 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
 }
 
 // ---------------------------------------------------------------------------
+// normal form along rows: out_v = N1 in_v, N1 = W G W^-1 (use_idwt) or G
+// ---------------------------------------------------------------------------
+// V rows per CTA (V * M <= 4096), three smem buffers of V*M doubles: A holds
+// the input (coarse + all details), the IDWT ping-pongs through B/C, the band
+// product lands in A, the DWT ping-pongs back through B/C and streams the
+// detail rows straight to `out` (which may alias `in`: every row is fully
+// staged before any write).  Every level loop runs over (row, index) pairs.
+// One analysis level of one vector: coarse c[0:n/2] -> dstc, detail rows ->
+// dstd[k] (any address space).  Interior rows with register taps, edge rows
+// (VMP) / all rows (periodic, masked) through dwt_pair.
+template <int NU>
+__device__ __forceinline__ void dwt_level_vec(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* x,
+                                              double* dstc, double* dstd, int n, bool vmp, int t0, int nthr) {
+    const int half = n >> 1;
+    const int klo = vmp ? NU : (NU + 1) / 2 + 1, khi = vmp ? half - NU : half - NU;
+    for (int k = klo + t0; k < khi; k += nthr) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            const double xv = x[2 * k + u];
+            if (u & 1) {
+                a1 = fma(tp.h[u + NU - 1], xv, a1);
+                b1 = fma(tp.g[u + NU - 1], xv, b1);
+            } else {
+                a0 = fma(tp.h[u + NU - 1], xv, a0);
+                b0 = fma(tp.g[u + NU - 1], xv, b0);
+            }
+        }
+        dstc[k] = a0 + a1;
+        dstd[k] = b0 + b1;
+    }
+    const int nl = klo, nr = half - khi;
+    for (int r = nthr - 1 - t0; r < nl + nr; r += nthr) {  // boundary rows
+        const int k = r < nl ? r : khi + (r - nl);
+        double c, d;
+        dwt_pair<NU>(F, x, n, k, vmp, c, d);
+        dstc[k] = c;
+        dstd[k] = d;
+    }
+}
+
+// Band product y = G x of one vector (G: see NormArgs); interior rows use
+// the Toeplitz row held in registers (half-bandwidth B = 2nu - 2).
+template <int NU>
+__device__ __forceinline__ void band_vec(const double* __restrict__ gE, const double (&gI)[4 * NU - 3], int E,
+                                         const double* x, double* y, int M, bool wrap, int t0, int nthr) {
+    constexpr int B = 2 * NU - 2, W = 2 * B + 1;
+    for (int i = E + t0; i < M - E; i += nthr) {
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+            if (d & 1) acc1 = fma(gI[d], x[i + d - B], acc1);
+            else acc0 = fma(gI[d], x[i + d - B], acc0);
+        }
+        y[i] = acc0 + acc1;
+    }
+    for (int r = t0; r < 2 * E; r += nthr) {  // edge rows: tabulated band
+        const int i = r < E ? r : M - 2 * E + r;
+        const double* g = gE + r * W;
+        double acc = 0.0;
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+            int k = i + d - B;
+            if (wrap) k &= M - 1;
+            if (k >= 0 && k < M) acc = fma(g[d], x[k], acc);
+        }
+        y[i] = acc;
+    }
+}
+
+template <int NU, int NT>
+__global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
+    // smem: filters | band edge rows | A, B, C [V][M] each.  A holds the
+    // staged input (coarse + every level's details); the synthesis ping-pongs
+    // B/C, the band product lands in A (free by then), the analysis ping-pongs
+    // B/C and streams detail rows to `out` (may alias `in`: rows are staged).
+    extern __shared__ double sm[];
+    constexpr int FS = FiltSmem<NU>::SIZE;
+    constexpr int W = 4 * NU - 3;
+    double* filt = sm;
+    const int j = p.j, M = 1 << j, tid = threadIdx.x;
+    const long long v0 = (long long)blockIdx.x * p.V;
+    const int nv = (int)(p.nvec - v0 < p.V ? p.nvec - v0 : p.V);
+    double* gE = sm + FS;  // [2E][W] edge rows of the band
+    double* A = gE + 2 * p.E * W;
+    double* B = A + p.V * M;
+    double* Cb = B + p.V * M;
+    const bool vmp = p.vmp != 0;
+    for (int i = tid; i < FS; i += NT) filt[i] = p.tab[p.t.o_h + i];
+    for (int i = tid; i < 2 * p.E * W; i += NT) gE[i] = p.band[i];
+    double gI[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) gI[d] = __ldg(p.band + 2 * p.E * W + d);
+    for (int t = tid; t < nv * M; t += NT) cp_async8(A + t, p.in + (v0 + (t >> j)) * p.in_vs + (t & (M - 1)));
+    cp_async_wait_all();
+    __syncthreads();
+    const FiltSmem<NU> F{filt};
+    const Taps<NU> tp(F);
+    const bool wav = p.use_idwt && p.r0 < j;
+    double* fine = A;
+    if (wav) {
+        double* src = A;  // level-r0 coarse rows live at the start of each input row
+        for (int lev = p.r0 + 1; lev <= j; ++lev) {
+            const int n = 1 << lev, half = n >> 1;
+            double* dst = (src == B) ? Cb : B;
+            for (int v = 0; v < nv; ++v)
+                idwt_level_vec<NU>(F, src + v * M, A + v * M + half, dst + v * M, n, vmp, tid, NT);
+            __syncthreads();
+            src = dst;
+        }
+        fine = src;
+    }
+    double* Y = wav ? A : B;  // A is free once the details are consumed
+    for (int v = 0; v < nv; ++v) band_vec<NU>(gE, gI, p.E, fine + v * M, Y + v * M, M, !vmp, tid, NT);
+    __syncthreads();
+    if (!wav) {
+        for (int t = tid; t < nv * M; t += NT) p.out[(v0 + (t >> j)) * p.out_vs + (t & (M - 1))] = Y[t];
+        return;
+    }
+    double* cur = Y;
+    for (int lev = j; lev > p.r0; --lev) {
+        const int n = 1 << lev, half = n >> 1;
+        double* dst = (cur == B) ? Cb : B;
+        for (int v = 0; v < nv; ++v)
+            dwt_level_vec<NU>(F, tp, cur + v * M, dst + v * M, p.out + (v0 + v) * p.out_vs + half, n, vmp, tid, NT);
+        __syncthreads();
+        cur = dst;
+    }
+    const int nc = 1 << p.r0;
+    for (int t = tid; t < nv * nc; t += NT) {
+        const int v = t >> p.r0, i = t & (nc - 1);
+        p.out[(v0 + v) * p.out_vs + i] = cur[v * M + i];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // large path: two-pass Hadamard over K with an L2-resident intermediate
 // ---------------------------------------------------------------------------
 // G per vector: [2^kh chunks][R1 physical rows][CW]; chunk c = K_hi (forward

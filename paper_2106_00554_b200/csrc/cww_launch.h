@@ -106,6 +106,26 @@ struct PyrArgs {
 
 cudaError_t launch_pyr(int nu, bool analysis, const PyrArgs& a, cudaStream_t st);
 
+// Normal form of the full-mask operator along one axis (SURVEY.md 8d "K10
+// normal-op form"): U* U = sum_s (D_s + E_s)^T H^T H (D_s + E_s) and H^T H =
+// M I, so U* U is a symmetric BANDED matrix G (half-bandwidth b = 2nu - 2,
+// wrapping for periodic boundaries).  N1 = W G W^-1 for the ComposedOp.
+// band: rows [0, E) gL[E][2b+1], rows [M-E, M) gR[E][2b+1], other rows the
+// Toeplitz row gI[2b+1]; entry d of row i multiplies x[i + d - b].
+struct NormArgs {
+    const double* tab;
+    Tables t;
+    const double* band;  // gL | gR | gI
+    int E, b;
+    const double* in;
+    double* out;
+    long long in_vs, out_vs, nvec;
+    int j, r0, use_idwt, vmp, V;
+};
+cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st);
+// Batched out-of-place transpose of n x n fp64 matrices (matrix stride n*n).
+cudaError_t launch_transpose(const double* in, double* out, long long n, long long batch, cudaStream_t st);
+
 // Largest window (over all CTAs and levels) of a synthesis pyramid producing
 // chunks of 2^cb samples of level top from level bot.
 // Also returns the largest total detail-window length of one CTA (dsum).

@@ -4,6 +4,8 @@
 #pragma once
 #include "cww_kernels.cuh"
 
+#include <cstdlib>
+
 #ifndef CWW_NU
 #error "define CWW_NU before including cww_nu_impl.cuh"
 #endif
@@ -121,6 +123,26 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
         auto k = k_idwt_wpyr<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<grid, 32 * nw, smem, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t CWW_FN(launch_normal_rows_nu)(const NormArgs& a, cudaStream_t st) {
+    const long long smem = (FiltSmem<CWW_NU>::SIZE + 2ll * a.E * (4 * CWW_NU - 3) + 3ll * a.V * (1ll << a.j)) * 8;
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    static const int nt = [] {
+        const char* e = std::getenv("CWW_NORMAL_NT");
+        return e && std::atoi(e) == 256 ? 256 : 512;
+    }();
+    const unsigned grid = (unsigned)((a.nvec + a.V - 1) / a.V);
+    if (nt == 256) {
+        auto k = k_normal_rows<CWW_NU, 256>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, 256, smem, st>>>(a);
+    } else {
+        auto k = k_normal_rows<CWW_NU, 512>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, 512, smem, st>>>(a);
     }
     return cudaGetLastError();
 }

@@ -232,6 +232,36 @@ def test_normal_operator_matches_two_calls(cuda):
     assert torch.isfinite(out).all()
 
 
+NORMAL = [(0, 2, 1, 7, 1, 1, 3), (0, 4, 1, 10, 2, 1, 4), (1, 6, 1, 9, 1, 1, -1), (0, 3, 0, 8, 2, 1, -1),
+          (0, 1, 0, 8, 1, 1, 2), (0, 4, 1, 12, 1, 1, 4), (0, 2, 1, 6, 1, 2, 3), (0, 4, 1, 7, 1, 2, 4),
+          (1, 5, 0, 7, 2, 2, -1), (0, 3, 1, 8, 1, 2, 4)]
+
+
+@pytest.mark.parametrize("case", NORMAL, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
+@pytest.mark.parametrize("use_idwt", [1, 0])
+@pytest.mark.parametrize("iters", [1, 2, 3])
+def test_normal_form_matches_forward_adjoint(orc, cuda, case, use_idwt, iters):
+    """cww_normal uses the banded normal form (U* U = sum_s C_s^T H^T H C_s
+    with H^T H = M I); it must equal repeated adjoint(forward(x)) and the
+    oracle's to <= 1e-12 relative."""
+    fam, nu, bnd, j, q, dim, r0 = case
+    if nu == 1 and not use_idwt:
+        pytest.skip("Haar op always composes the IDWT")
+    op = make(fam, nu, bnd, j, q, dim, r0, bool(use_idwt))
+    ref = orc.op(fam, nu, bnd, j, q, dim, r0)
+    x = np.stack([orc.normals(300 + b, ref.nin) for b in range(2)])
+    want = gpu(x)
+    for _ in range(iters):
+        want = op.adjoint(op.forward(want))
+    got = op.normal(gpu(x), iters=iters)
+    z = x[0]
+    for _ in range(iters):
+        z = ref.adjoint(ref.forward(z, use_idwt), use_idwt)
+    for b in range(2):
+        assert rel(host(got)[b], host(want)[b]) <= 1e-12
+    assert rel(host(got)[0], z) <= 1e-12
+
+
 def test_host_pointer_path(orc, cuda):
     (fam, nu, bnd, j, q, dim, r0), (kind, dens) = CONFIGS[2]
     ref = orc.op(fam, nu, bnd, 12, q, dim, r0)
