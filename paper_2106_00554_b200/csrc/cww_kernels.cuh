@@ -1175,6 +1175,7 @@ __device__ __forceinline__ void band_vec(const double* __restrict__ gE, const do
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
+    PHASE(0);
     // smem: filters | band edge rows | A, B, C [V][M] each.  A holds the
     // staged input (coarse + every level's details); the synthesis ping-pongs
     // B/C, the band product lands in A (free by then), the analysis ping-pongs
@@ -1199,6 +1200,7 @@ __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
     for (int t = tid; t < nv * M; t += NT) cp_async8(A + t, p.in + (v0 + (t >> j)) * p.in_vs + (t & (M - 1)));
     cp_async_wait_all();
     __syncthreads();
+    PHASE(1);
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
     const bool wav = p.use_idwt && p.r0 < j;
@@ -1215,9 +1217,11 @@ __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
         }
         fine = src;
     }
+    PHASE(2);
     double* Y = wav ? A : B;  // A is free once the details are consumed
     for (int v = 0; v < nv; ++v) band_vec<NU>(gE, gI, p.E, fine + v * M, Y + v * M, M, !vmp, tid, NT);
     __syncthreads();
+    PHASE(3);
     if (!wav) {
         for (int t = tid; t < nv * M; t += NT) p.out[(v0 + (t >> j)) * p.out_vs + (t & (M - 1))] = Y[t];
         return;
@@ -1231,11 +1235,13 @@ __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
         __syncthreads();
         cur = dst;
     }
+    PHASE(4);
     const int nc = 1 << p.r0;
     for (int t = tid; t < nv * nc; t += NT) {
         const int v = t >> p.r0, i = t & (nc - 1);
         p.out[(v0 + v) * p.out_vs + i] = cur[v * M + i];
     }
+    PHASE(5);
 }
 
 // ---------------------------------------------------------------------------

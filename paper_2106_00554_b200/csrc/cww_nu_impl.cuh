@@ -132,7 +132,7 @@ cudaError_t CWW_FN(launch_normal_rows_nu)(const NormArgs& a, cudaStream_t st) {
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static const int nt = [] {
         const char* e = std::getenv("CWW_NORMAL_NT");
-        return e && std::atoi(e) == 256 ? 256 : 512;
+        return e && std::atoi(e) == 512 ? 512 : 256;
     }();
     const unsigned grid = (unsigned)((a.nvec + a.V - 1) / a.V);
     if (nt == 256) {
@@ -171,7 +171,10 @@ cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
 
 }  // namespace cww
 
-#if defined(CWW_PHASE_TIMING) && CWW_NU == 4
+#ifndef CWW_PHASE_NU
+#define CWW_PHASE_NU 4
+#endif
+#if defined(CWW_PHASE_TIMING) && CWW_NU == CWW_PHASE_NU
 extern "C" int cww_debug_phase_read(long long* host, size_t n) {
     return (int)cudaMemcpyFromSymbol(host, cww::cww_phase_buf, n * sizeof(long long));
 }
