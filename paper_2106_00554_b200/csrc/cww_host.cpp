@@ -1257,6 +1257,15 @@ cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* 
     return run(op, y, x, (long long)batch, true, S_(stream));
 }
 
+// CWW_NORMAL_EXPLICIT=1: normal operator / solver through forward + adjoint
+bool normal_explicit() {
+    static const bool v = [] {
+        const char* e = std::getenv("CWW_NORMAL_EXPLICIT");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // ---- banded normal form (U* U along one axis) -----------------------------
 // Probes G = U* U with the op's own FastOp kernels on unit vectors: the
 // first / last E columns, one interior column, and two verification columns.
@@ -1410,11 +1419,7 @@ cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work, s
         w = wb.p;
     }
     CUDA_TRY(cudaSetDevice(op->device));
-    static const bool no_banded = [] {
-        const char* e = std::getenv("CWW_NORMAL_EXPLICIT");
-        return e && e[0] == '1';
-    }();
-    if (!op->masked && !no_banded && op->M <= 4096) {
+    if (!op->masked && !normal_explicit() && op->M <= 4096) {
         std::call_once(op->gram->once, [op] { build_gram(op); });
         if (op->gram->ok) return normal_banded(op, x, w, (long long)batch, iters, st);
     }
@@ -1430,6 +1435,95 @@ cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work, s
 // row f1): CGLS on A* A x = A* y with A this op (masked or full), batched.
 // Stops when every system's relative normal-equation residual
 // ||A*(y - A x)|| / ||A* y|| <= residual_tol, or after max_iters.
+// CG on the normal equations with the banded normal form N = A* A (full-mask
+// ops): b = A* y once, then one banded N application per iteration instead of
+// a forward and an adjoint.  Same stopping rule as CGLS: ||b - N x|| / ||b||.
+cww_status gs_solve_normal(const cww_op* op, const double* y, double* x, long long B, double tol,
+                           int max_iters, bool use_x0, int* iters_out, double* resid_out, cudaStream_t st) {
+    size_t ni, no;
+    cww_op_sizes(op, &ni, &no);
+    const long long nx = (long long)ni;
+    DevBuf bv, r, pv, qv, wv, part, sc;
+    CUDA_TRY(bv.alloc(size_t(B * nx), st));
+    CUDA_TRY(r.alloc(size_t(B * nx), st));
+    CUDA_TRY(pv.alloc(size_t(B * nx), st));
+    CUDA_TRY(qv.alloc(size_t(B * nx), st));
+    CUDA_TRY(wv.alloc(size_t(B * nx), st));
+    CUDA_TRY(part.alloc(size_t(B * cww::dot_nblk(nx, B)), st));
+    CUDA_TRY(sc.alloc(size_t(5 * B), st));
+    double* gam[2] = {sc.p, sc.p + B};
+    double* pq = sc.p + 2 * B;
+    double* s0 = sc.p + 3 * B;
+    int* active = reinterpret_cast<int*>(sc.p + 4 * B);
+    const size_t bytes = size_t(B * nx) * sizeof(double);
+    cww_status rs;
+    if ((rs = run(op, y, bv.p, B, true, st)) != CWW_OK) return rs;  // b = A* y
+    if (use_x0) {  // r = b - N x0
+        CUDA_TRY(cudaMemcpyAsync(qv.p, x, bytes, cudaMemcpyDeviceToDevice, st));
+        if ((rs = normal_banded(op, qv.p, wv.p, B, 1, st)) != CWW_OK) return rs;
+        CUDA_TRY(cudaMemcpyAsync(r.p, qv.p, bytes, cudaMemcpyDeviceToDevice, st));
+        Prof pr("cg_vec", st);
+        CUDA_TRY(cww::launch_sub_from(r.p, bv.p, B * nx, st));
+    } else {
+        CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
+        CUDA_TRY(cudaMemcpyAsync(r.p, bv.p, bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    {
+        Prof pr("cg_vec", st, 6);
+        CUDA_TRY(cww::launch_dot(bv.p, bv.p, nx, B, part.p, gam[1], st));  // ||A* y||: the reference norm
+        CUDA_TRY(cww::launch_sqrt(gam[1], s0, B, st));
+        CUDA_TRY(cww::launch_dot(r.p, r.p, nx, B, part.p, gam[0], st));
+        CUDA_TRY(cww::launch_cgls_flags(gam[0], s0, tol, active, B, st));
+    }
+    CUDA_TRY(cudaMemcpyAsync(pv.p, r.p, bytes, cudaMemcpyDeviceToDevice, st));
+    std::vector<double> hg(size_t(2 * B));
+    auto residuals = [&](const double* g, bool& done) -> cww_status {
+        CUDA_TRY(cudaMemcpyAsync(hg.data(), g, size_t(B) * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(hg.data() + B, s0, size_t(B) * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        done = true;
+        for (long long b = 0; b < B; ++b) {
+            const double n0 = hg[size_t(B + b)];
+            const double rel = n0 > 0.0 ? std::sqrt(hg[size_t(b)]) / n0 : 0.0;
+            if (resid_out) resid_out[b] = rel;
+            if (rel > tol) done = false;
+        }
+        return CWW_OK;
+    };
+    int it = 0, cur = 0;
+    bool done = false;
+    for (; it < max_iters; ++it) {
+        if ((rs = residuals(gam[cur], done)) != CWW_OK) return rs;
+        if (done) break;
+        CUDA_TRY(cudaMemcpyAsync(qv.p, pv.p, bytes, cudaMemcpyDeviceToDevice, st));
+        if ((rs = normal_banded(op, qv.p, wv.p, B, 1, st)) != CWW_OK) return rs;  // q = N p
+        {
+            Prof pr("cg_vec", st, 3);
+            CUDA_TRY(cww::launch_dot(pv.p, qv.p, nx, B, part.p, pq, st));
+            CUDA_TRY(cww::launch_cgls_xr(x, r.p, pv.p, qv.p, nx, nx, B, gam[cur], pq, active, st));
+        }
+        {
+            Prof pr("cg_vec", st, 4);
+            CUDA_TRY(cww::launch_dot(r.p, r.p, nx, B, part.p, gam[cur ^ 1], st));
+            CUDA_TRY(cww::launch_cgls_p(pv.p, r.p, nx, B, gam[cur ^ 1], gam[cur], st));
+            CUDA_TRY(cww::launch_cgls_flags(gam[cur ^ 1], s0, tol, active, B, st));
+        }
+        cur ^= 1;
+    }
+    if (!done && (rs = residuals(gam[cur], done)) != CWW_OK) return rs;
+    if (iters_out) *iters_out = it;
+    if (!done) {
+        double worst = 0.0;
+        for (long long b = 0; b < B; ++b) {
+            const double n0 = hg[size_t(B + b)];
+            worst = std::max(worst, n0 > 0.0 ? std::sqrt(hg[size_t(b)]) / n0 : 0.0);
+        }
+        return fail(CWW_ERR_NOT_CONVERGED, "gs_solve: CG did not converge in %d iterations (relative residual %.3e)",
+                    it, worst);
+    }
+    return CWW_OK;
+}
+
 cww_status gs_solve(const cww_op* op, const double* y, double* x, long long B, double tol, int max_iters,
                     bool use_x0, int* iters_out, double* resid_out, cudaStream_t st) {
     size_t ni, no;
@@ -1456,11 +1550,17 @@ cww_status gs_solve(const cww_op* op, const double* y, double* x, long long B, d
         CUDA_TRY(cudaMemsetAsync(x, 0, size_t(B * nx) * sizeof(double), st));
         CUDA_TRY(cudaMemcpyAsync(r.p, y, size_t(B * nr) * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
+    if (use_x0) {  // reference norm ||A* y||
+        if ((rs = run(op, y, sv.p, B, true, st)) != CWW_OK) return rs;
+        Prof pr("cg_vec", st, 3);
+        CUDA_TRY(cww::launch_dot(sv.p, sv.p, nx, B, part.p, gam[1], st));
+        CUDA_TRY(cww::launch_sqrt(gam[1], s0, B, st));
+    }
     if ((rs = run(op, r.p, sv.p, B, true, st)) != CWW_OK) return rs;
     {
         Prof pr("cg_vec", st, 4);
         CUDA_TRY(cww::launch_dot(sv.p, sv.p, nx, B, part.p, gam[0], st));
-        CUDA_TRY(cww::launch_sqrt(gam[0], s0, B, st));
+        if (!use_x0) CUDA_TRY(cww::launch_sqrt(gam[0], s0, B, st));
         CUDA_TRY(cww::launch_cgls_flags(gam[0], s0, tol, active, B, st));
     }
     CUDA_TRY(cudaMemcpyAsync(pv.p, sv.p, size_t(B * nx) * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1549,6 +1649,12 @@ cww_status cww_gs_solve(const cww_op* op, const double* y, size_t y_len, double*
     if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     if (max_iters < 0 || !(residual_tol >= 0.0)) return fail(CWW_ERR_INVALID_ARG, "gs_solve: bad parameters");
     CUDA_TRY(cudaSetDevice(op->device));
+    if (!op->masked && op->M <= 4096 && !normal_explicit()) {
+        std::call_once(op->gram->once, [op] { build_gram(op); });
+        if (op->gram->ok)
+            return gs_solve_normal(op, y, x, (long long)batch, residual_tol, max_iters, use_x0 != 0, iters,
+                                   residuals, S_(stream));
+    }
     return gs_solve(op, y, x, (long long)batch, residual_tol, max_iters, use_x0 != 0, iters, residuals,
                     S_(stream));
 }
