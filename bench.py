@@ -115,6 +115,12 @@ def algorithmic_bytes(cfg, kernel: str, batch: int) -> float:
     """Minimal DRAM bytes of one step's launches of `kernel`."""
     fam, nu, bnd, j, q, dim, r0 = cfg[:7]
     M, N = 1 << j, 1 << (j + q)
+    if kernel in ("normal_rows", "transpose"):
+        # banded normal form (config 5): every launch reads and writes each
+        # M-row once; per U*U: 2 row passes + 1 transpose over the M x M image
+        per_iter = 2 if kernel == "normal_rows" else 1
+        iters = CFG5_ITERS if cfg is CONFIGS[5] else 1
+        return 16.0 * batch * (M * M if dim == 2 else M) * per_iter * iters
     if dim == 2:
         mats = CFG5_ITERS if cfg is CONFIGS[5] else 1
         # small_fwd: row pass (M^2 -> MN) + column pass (MN -> N^2); small_adj mirrored
@@ -280,9 +286,9 @@ def main():
     if nu == 1:
         op = cw.HaarFullRankOp(j, q, r0)
     elif rowpart:
-        from paper_2106_00554_b200.dist import RowPartitioned2D, cuda_apply_1d
+        from paper_2106_00554_b200.dist import RowPartitioned2D, cuda_apply_1d, cuda_normal_1d
         op1 = cw.ComposedOp(cw.FastOp(spec, j, q, 1), None, True, r0)
-        d2 = RowPartitioned2D(1 << j, 1 << (j + q), cuda_apply_1d(op1))
+        d2 = RowPartitioned2D(1 << j, 1 << (j + q), cuda_apply_1d(op1), apply_normal_1d=cuda_normal_1d(op1))
         op = cw.ComposedOp(cw.FastOp(spec, j, q, dim), None, True, r0)
     else:
         op = cw.ComposedOp(cw.FastOp(spec, j, q, dim), None, True, r0)
@@ -410,11 +416,17 @@ def main():
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded test_rng inputs, SURVEY.md 8d)",
         "config": {"workload": name, "batch_per_gpu": batch,
-                   "step": (f"{CFG5_ITERS} x U*U on the image" if is5 else "forward + adjoint of the batch"),
+                   "step": (f"{CFG5_ITERS} x U*U on the image (cww_normal: banded normal form W G W^-1 per "
+                            "axis, G = U*U exactly banded since H^T H = M I; rows fused IDWT-band-DWT, tiled "
+                            "transposes)" if is5 else "forward + adjoint of the batch"),
                    "l2": "flushed (256 MiB write) between timed steps",
                    "parallelism": (f"rows/{world} + NCCL all-to-all transposes" if rowpart
                                    else f"dp{world} (independent batches)")},
         "path_gbs_per_gpu": round(path_gbs, 1), "path_frac": round(path_gbs / peak, 4),
+        **({"path_frac_kind": "effective (algorithmic bytes 2*8(M^2+N^2) per U*U; the banded normal form "
+                              "moves 3*16*M^2 per U*U on one GPU)",
+            "actual_hbm_frac": round(3 * 16 * (1 << j) ** 2 * CFG5_ITERS * args.steps
+                                     / (ms / 1e3) / 1e9 / peak, 4)} if is5 and not rowpart else {}),
         "roofline": roof,
         "kernels": {k: [round(v[0] / args.steps, 4), v[1] // args.steps] for k, v in prof.items()},
         "gpu_launches": launches,

@@ -17,6 +17,12 @@ SURVEY.md section 8e:
     so the normal operator U*U keeps X row-partitioned and moves 2 x M x N
     doubles through the network per iteration.
 
+    With the banded normal form (A*A = N1 (x) N1, N1 = W (U*U) W^-1 applied
+    by `apply_normal_1d` to rows), an iteration is
+        rows X_r <- X_r N1  (local),  distributed transpose,
+        rows     <- . N1    (local),  distributed transpose back,
+    moving 2 x M^2 doubles per iteration instead of 2 x M x N.
+
 The local 1D passes are a callable `apply_1d(batch_rows, adjoint) -> rows`
 (the GPU ComposedOp on CUDA tensors in production; any host implementation
 in the CPU tests), so the partition / exchange logic is backend-neutral and
@@ -24,7 +30,7 @@ is tested with the gloo backend at world_size 2.
 """
 from __future__ import annotations
 
-from typing import Callable, Tuple
+from typing import Callable, Optional, Tuple
 
 import torch
 import torch.distributed as dist
@@ -55,9 +61,10 @@ class RowPartitioned2D:
     (length N -> M) to each row of the 2D tensor v."""
 
     def __init__(self, M: int, N: int, apply_1d: Callable[[torch.Tensor, bool], torch.Tensor],
-                 group=None):
+                 group=None, apply_normal_1d: Optional[Callable[[torch.Tensor], torch.Tensor]] = None):
         self.M, self.N = M, N
         self.apply_1d = apply_1d
+        self.apply_normal_1d = apply_normal_1d
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -84,9 +91,22 @@ class RowPartitioned2D:
         t_rows = torch.cat([g.view(mr, nc) for g in got], dim=1)               # (M/P, N)
         return self.apply_1d(t_rows, True)                                     # (M/P, M)
 
+    def transpose(self, x_rows: torch.Tensor) -> torch.Tensor:
+        """Distributed transpose of the row-partitioned M x M matrix: rank p
+        sends block X[p rows, q cols] to rank q and receives X[q rows, p cols]."""
+        P, mr = self.world, self.mr
+        blocks = [x_rows[:, q * mr:(q + 1) * mr].contiguous() for q in range(P)]
+        got = _all_to_all_blocks(blocks, self.group)
+        return torch.cat([g.view(mr, mr).t() for g in got], dim=1).contiguous()
+
     def normal(self, x_rows: torch.Tensor, iters: int = 1) -> torch.Tensor:
-        for _ in range(iters):
-            x_rows = self.adjoint(self.forward(x_rows))
+        if self.apply_normal_1d is None:
+            for _ in range(iters):
+                x_rows = self.adjoint(self.forward(x_rows))
+            return x_rows
+        for _ in range(iters):  # X <- N1 X N1 (N1 symmetric)
+            x_rows = self.transpose(self.apply_normal_1d(x_rows))
+            x_rows = self.transpose(self.apply_normal_1d(x_rows))
         return x_rows
 
 
@@ -103,6 +123,14 @@ def gather_cols(local: torch.Tensor, group=None) -> torch.Tensor:
     parts = [torch.empty_like(local) for _ in range(world)]
     dist.all_gather(parts, local.contiguous(), group=group)
     return torch.cat(parts, dim=1)
+
+
+def cuda_normal_1d(op) -> Callable[[torch.Tensor], torch.Tensor]:
+    """The production local normal pass: rows <- N1 rows in place (1D op)."""
+    def f(v: torch.Tensor) -> torch.Tensor:
+        v = v.contiguous()
+        return op.normal(v, iters=1)
+    return f
 
 
 def cuda_apply_1d(op) -> Callable[[torch.Tensor, bool], torch.Tensor]:

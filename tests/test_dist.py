@@ -48,13 +48,20 @@ def _worker(rank, world, port, case, q):
         for b in (1, 7, 64):
             s, c = shard_batch(b, rank, world)
             seen.append((b, s, c))
+        def normal_1d(v):
+            a = v.numpy()
+            return torch.from_numpy(np.stack([op1.adjoint(op1.forward(r)) for r in a]))
+
         d2 = RowPartitioned2D(M, N, apply_1d)
+        d2n = RowPartitioned2D(M, N, apply_1d, apply_normal_1d=normal_1d)
         x = torch.from_numpy(o.normals(77, M * M).reshape(M, M))
         xr = x[rank * M // world:(rank + 1) * M // world].contiguous()
         yc = d2.forward(xr)
         y = gather_cols(yc)
         xa = d2.adjoint(yc)
         xn = gather_rows(d2.normal(xr, 2))
+        xnb = gather_rows(d2n.normal(xr, 3))  # odd count: transposes must cancel
+        xt = gather_rows(d2.transpose(xr))
         xa_full = gather_rows(xa)
         if rank == 0:
             op2 = o.op(fam, nu, bnd, j, qq, 2, r0)
@@ -63,9 +70,11 @@ def _worker(rank, world, port, case, q):
             z = x.numpy().ravel()
             for _ in range(2):
                 z = op2.adjoint(op2.forward(z))
+            z3 = op2.adjoint(op2.forward(z))
             rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+            assert np.array_equal(xt.numpy(), x.numpy().T)
             q.put(("ok", seen, rel(y.numpy(), ref_y), rel(xa_full.numpy(), ref_a),
-                   rel(xn.numpy().ravel(), z)))
+                   max(rel(xn.numpy().ravel(), z), rel(xnb.numpy().ravel(), z3))))
         else:
             q.put(("ok", seen, 0.0, 0.0, 0.0))
     except Exception as e:  # noqa: BLE001
