@@ -400,9 +400,16 @@ def main():
         kms, kn = prof[kname]
         steps_bytes = algorithmic_bytes(cfg, kname, batch) * args.steps
         achieved = steps_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+        traffic, tnote = None, None
+        try:  # committed ncu capture of this config's dominant kernel (profiles/r01_traffic.json)
+            tr = json.load(open(os.path.join(REPO, "profiles", "r01_traffic.json")))[str(args.config)]
+            if tr["kernel"] == kname:
+                traffic, tnote = tr["bytes"], tr["launch"] + " (ncu dram__bytes_read+write, profiles/)"
+        except (OSError, KeyError, ValueError):
+            pass
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "kernel_ms_per_launch": kms / kn, "launches": kn,
+                "traffic": traffic, "traffic_launch": tnote, "kernel_ms_per_launch": kms / kn, "launches": kn,
                 "kernel_share_of_step": round(kms / ms, 4)}
     M, N = 1 << j, 1 << (j + q)
     per_mv = 8 * ((M + N) if dim == 1 else (M * M + N * N))
