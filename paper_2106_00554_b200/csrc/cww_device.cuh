@@ -476,6 +476,12 @@ __device__ __forceinline__ void dwt_pair(const FiltSmem<NU>& F, const double* x,
     d = b;
 }
 
+// Programmatic dependent launch (PDL): every kernel triggers its dependents
+// at entry and waits for its predecessor's results before touching memory;
+// both are no-ops when the launch did not use the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Asynchronous 8-byte global -> shared copy (LDGSTS): many loads in flight
 // per thread without register staging.
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {

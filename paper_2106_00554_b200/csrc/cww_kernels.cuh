@@ -381,6 +381,8 @@ __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 
 template <int NU, int LOGB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     using G = Geo<NU, LOGB>;
     constexpr int B = G::B, H = G::H, CW = G::CW, RS = G::RS, NP = G::NP;
     extern __shared__ double sm[];
@@ -541,6 +543,8 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
 
 template <int NU, int LOGB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     using G = Geo<NU, LOGB>;
     constexpr int B = G::B, H = G::H, CW = G::CW, RS = G::RS, NP = G::NP;
     extern __shared__ double sm[];
@@ -708,54 +712,6 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
 // wavelet levels in global memory (large path)
 // ---------------------------------------------------------------------------
 
-// One IDWT level: fine[0:n] from c = lo[0:n/2] (workspace) and the details
-// d = elements [n/2, n) of the op input.  The large path is 1D with
-// contiguous vectors (host-enforced), so the details are unit-stride.
-template <int NU>
-__global__ void __launch_bounds__(256) k_idwt_level(const double* tab, Tables t, const double* lo,
-                                                    long long lo_vs, const double* x, Layout lx,
-                                                    long long xv0, double* out, long long out_vs,
-                                                    int lev, int nvec, int vmp) {
-    __shared__ double filt[FiltSmem<NU>::SIZE];
-    for (int i = threadIdx.x; i < FiltSmem<NU>::SIZE; i += blockDim.x) filt[i] = tab[t.o_h + i];
-    __syncthreads();
-    const FiltSmem<NU> F{filt};
-    const int n = 1 << lev, half = n >> 1;
-    const long long tot = (long long)nvec * half;  // pairs
-    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
-         f += (long long)gridDim.x * blockDim.x) {
-        const int v = (int)(f >> (lev - 1)), m = (int)(f & (half - 1));
-        const double* xb = x + lx.vbase(xv0 + v) + half;
-        double o0, o1;
-        idwt_pair<NU>(F, lo + v * lo_vs, xb, n, m, vmp, o0, o1);
-        out[v * out_vs + 2 * m] = o0;
-        out[v * out_vs + 2 * m + 1] = o1;
-    }
-}
-
-// One DWT level: from fine samples in[0:n] (workspace) write the coarse half
-// to cout[0:n/2] (workspace) and the detail half directly to the op output.
-template <int NU>
-__global__ void __launch_bounds__(256) k_dwt_level(const double* tab, Tables t, const double* in,
-                                                   long long in_vs, double* cout, long long cout_vs,
-                                                   double* y, Layout ly, long long yv0, int lev,
-                                                   int nvec, int vmp) {
-    __shared__ double filt[FiltSmem<NU>::SIZE];
-    for (int i = threadIdx.x; i < FiltSmem<NU>::SIZE; i += blockDim.x) filt[i] = tab[t.o_h + i];
-    __syncthreads();
-    const FiltSmem<NU> F{filt};
-    const int n = 1 << lev, half = n >> 1;
-    const long long tot = (long long)nvec * half;
-    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
-         f += (long long)gridDim.x * blockDim.x) {
-        const int v = (int)(f >> (lev - 1)), mm = (int)(f & (half - 1));
-        double c, d;
-        dwt_pair<NU>(F, in + v * in_vs, n, mm, vmp, c, d);
-        cout[v * cout_vs + mm] = c;
-        y[ly.at(yv0 + v, half + mm)] = d;
-    }
-}
-
 // Coarse levels in one CTA per vector (shared memory ping-pong).
 //   inverse: levels r0+1..Lc of x (layout) -> dst[0:2^Lc] (workspace, dst_vs)
 //   forward: levels Lc..r0+1 of src[0:2^Lc] (workspace) -> y layout [0:2^Lc)
@@ -765,6 +721,8 @@ __global__ void __launch_bounds__(256) k_wav_coarse(const double* tab, Tables t,
                                                     double* dst, Layout ld, long long dv0,
                                                     long long dst_vs, int r0, int Lc, int inverse,
                                                     int vmp) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ double sm[];
     double* filt = sm;
     const int n = 1 << Lc;
@@ -926,6 +884,8 @@ __device__ __forceinline__ void dwt_pair_log(const FiltSmem<NU>& F, const Taps<N
 // compute and store phases freely.
 template <int NU>
 __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     extern __shared__ double sm[];
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
@@ -1036,6 +996,8 @@ __device__ __forceinline__ void dwt_coarse_tail(const PyrArgs& p, const FiltSmem
 // the output when bot == r0).  __syncwarp only.
 template <int NU>
 __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     extern __shared__ double sm[];
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
@@ -1175,6 +1137,8 @@ __device__ __forceinline__ void band_vec(const double* __restrict__ gE, const do
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     PHASE(0);
     // smem: filters | band edge rows | A, B, C [V][M] each.  A holds the
     // staged input (coarse + every level's details); the synthesis ping-pongs
@@ -1252,6 +1216,8 @@ __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS;
     extern __shared__ double sm[];
@@ -1289,6 +1255,8 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
@@ -1340,6 +1308,8 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
@@ -1407,6 +1377,8 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];

@@ -4,10 +4,43 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 #include "cww_device.cuh"
 
 namespace cww {
+
+// Kernel launch, optionally with programmatic stream serialization (PDL,
+// CWW_PDL=1): the next kernel of a chain is scheduled while this one's last
+// wave drains; kernels order their memory accesses with griddepcontrol.wait
+// (cww_device.cuh).  Off by default: measured on B200 it did not pay (config
+// 2: 0.280 vs 0.274 ms, config 3: 2.96 vs 2.69 ms per step) -- the waiting
+// dependents hold SM slots the primary's tail could use.
+inline bool pdl_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("CWW_PDL");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    if (pdl_enabled()) {
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 constexpr int kSmallMaxLog = 12;  // M <= 2^12: whole map in one CTA's shared memory
 
@@ -53,7 +86,7 @@ struct LargeArgs {
 };
 
 struct WavArgs {
-    int kind;  // 0 coarse (one CTA per vector, shared memory); 1 idwt level; 2 dwt level
+    int kind;  // 0: coarse levels (one CTA per vector, shared memory)
     const double* tab;
     Tables t;
     long long nvec;

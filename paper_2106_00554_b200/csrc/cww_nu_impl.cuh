@@ -32,11 +32,11 @@ cudaError_t small_t(const SmallArgs& a, bool adj, cudaStream_t st) {
         if (adj) {
             auto k = k_small_adj<CWW_NU, LOGB, kSmallNT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k<<<grid, kSmallNT, smem, st>>>(a);
+            if (cudaError_t e = launch_k(k, grid, kSmallNT, smem, st, a); e != cudaSuccess) return e;
         } else {
             auto k = k_small_fwd<CWW_NU, LOGB, kSmallNT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k<<<grid, kSmallNT, smem, st>>>(a);
+            if (cudaError_t e = launch_k(k, grid, kSmallNT, smem, st, a); e != cudaSuccess) return e;
         }
         return cudaGetLastError();
     }
@@ -79,25 +79,25 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
         case 0: {
             auto k = k_large_fwd1<CWW_NU, CWW_NT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-            k<<<g1, CWW_NT, s1, st>>>(a);
+            if (cudaError_t e = launch_k(k, g1, CWW_NT, s1, st, a); e != cudaSuccess) return e;
             break;
         }
         case 1: {
             auto k = k_large_fwd2<CWW_NU, CWW_NT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-            k<<<g2, CWW_NT, s2, st>>>(a);
+            if (cudaError_t e = launch_k(k, g2, CWW_NT, s2, st, a); e != cudaSuccess) return e;
             break;
         }
         case 2: {
             auto k = k_large_adj2<CWW_NU, CWW_NT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2a);
-            k<<<g2, CWW_NT, s2a, st>>>(a);
+            if (cudaError_t e = launch_k(k, g2, CWW_NT, s2a, st, a); e != cudaSuccess) return e;
             break;
         }
         default: {
             auto k = k_large_adj1<CWW_NU, CWW_NT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1a);
-            k<<<g1, CWW_NT, s1a, st>>>(a);
+            if (cudaError_t e = launch_k(k, g1, CWW_NT, s1a, st, a); e != cudaSuccess) return e;
             break;
         }
     }
@@ -116,13 +116,13 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_dwt_wpyr<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<grid, 32 * nw, smem, st>>>(a);
+        if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     } else {
         const long long smem = (FS + (long long)nw * (48 + 2ll * a.wmax + a.dsum)) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_idwt_wpyr<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<grid, 32 * nw, smem, st>>>(a);
+        if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
@@ -138,11 +138,11 @@ cudaError_t CWW_FN(launch_normal_rows_nu)(const NormArgs& a, cudaStream_t st) {
     if (nt == 256) {
         auto k = k_normal_rows<CWW_NU, 256>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<grid, 256, smem, st>>>(a);
+        if (cudaError_t e = launch_k(k, grid, 256, smem, st, a); e != cudaSuccess) return e;
     } else {
         auto k = k_normal_rows<CWW_NU, 512>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<grid, 512, smem, st>>>(a);
+        if (cudaError_t e = launch_k(k, grid, 512, smem, st, a); e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
@@ -153,18 +153,10 @@ cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
         long long smem = (FiltSmem<CWW_NU>::SIZE + 3 * (1ll << w.lev)) * 8;
         auto k = k_wav_coarse<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<(unsigned)w.nvec, nt, smem, st>>>(w.tab, w.t, w.src, w.ls, w.sv0, w.src_vs, w.dst, w.ld,
-                                              w.dv0, w.dst_vs, w.r0, w.lev, w.inverse, w.vmp);
-    } else {
-        long long tot = (long long)w.nvec << w.lev;
-        int grid = (int)((tot + nt - 1) / nt);
-        if (grid > 148 * 16) grid = 148 * 16;
-        if (w.kind == 1)
-            k_idwt_level<CWW_NU><<<grid, nt, 0, st>>>(w.tab, w.t, w.src, w.src_vs, w.x, w.lx, w.xv0,
-                                                      w.dst, w.dst_vs, w.lev, (int)w.nvec, w.vmp);
-        else
-            k_dwt_level<CWW_NU><<<grid, nt, 0, st>>>(w.tab, w.t, w.src, w.src_vs, w.dst, w.dst_vs,
-                                                     w.y, w.ly, w.yv0, w.lev, (int)w.nvec, w.vmp);
+        if (cudaError_t e = launch_k(k, dim3((unsigned)w.nvec), dim3(nt), (size_t)smem, st, w.tab, w.t, w.src, w.ls,
+                                     w.sv0, w.src_vs, w.dst, w.ld, w.dv0, w.dst_vs, w.r0, w.lev, w.inverse, w.vmp);
+            e != cudaSuccess)
+            return e;
     }
     return cudaGetLastError();
 }
