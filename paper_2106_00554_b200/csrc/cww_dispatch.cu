@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "cww_device.cuh"
 #include "cww_launch.h"
@@ -15,7 +16,8 @@ namespace cww {
     cudaError_t launch_large_nu##N(int, const LargeArgs&, cudaStream_t);            \
     cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);                    \
     cudaError_t launch_pyr_nu##N(bool, const PyrArgs&, cudaStream_t);               \
-    cudaError_t launch_normal_rows_nu##N(const NormArgs&, cudaStream_t);
+    cudaError_t launch_normal_rows_nu##N(const NormArgs&, cudaStream_t);               \
+    cudaError_t launch_normal_rows_reg_nu##N(const NormArgs&, cudaStream_t);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6)
 #undef DECL
 
@@ -93,6 +95,15 @@ cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long
 }
 
 cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st) {
+    static const bool reg = [] {
+        const char* e = std::getenv("CWW_NORMAL_REG");
+        return !(e && e[0] == '0');
+    }();
+    if (reg && a.use_idwt && a.j >= 9 && a.j <= 12 && a.r0 < kRegLog && a.V <= 1) {
+#define C(N) launch_normal_rows_reg_nu##N(a, st)
+        SWITCH_NU(nu, C)
+#undef C
+    }
 #define C(N) launch_normal_rows_nu##N(a, st)
     SWITCH_NU(nu, C)
 #undef C

@@ -1209,6 +1209,305 @@ __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
 }
 
 // ---------------------------------------------------------------------------
+// register-resident normal rows: 2^9 <= M <= 2^12, one row per CTA, 256 threads
+// ---------------------------------------------------------------------------
+// Above 2^kRegLog samples every thread owns a contiguous segment of each
+// level: a synthesis level turns its K coarse values into 2K fine values
+// that are exactly the next level's input segment, so levels chain in
+// registers.  Only the halos (a few values from the neighbouring segments)
+// and the VMP edge samples read a shared-memory copy of the level.  The
+// analysis runs the same way downward.  Levels <= 2^kRegLog and the band
+// edge rows use the shared-memory helpers.
+
+// Register levels keep a shared-memory copy of each level for the halos in a
+// padded layout (one spare double per 32) so that the segment stores / loads
+// of a warp (lane stride 2K doubles) are bank-conflict free.
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 5); }
+
+// synthesis of a length-n level: coarse segment c[K] (indices m0..) -> fine f[2K].
+// cs: copy of the coarse level (padded when PADIN), ds: details (plain).
+template <int NU, int K, bool PADIN>
+__device__ __forceinline__ void syn_seg(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* cs,
+                                        const double* ds, int n, int m0, bool vmp, const double (&c)[K],
+                                        double (&f)[2 * K]) {
+    constexpr int OFF = (NU + 1) / 2, WN = K + NU + 1;
+    const int half = n >> 1;
+    auto cat = [&](int i) { return PADIN ? cs[pidx(i)] : cs[i]; };
+    double cw[WN], dw[WN];
+#pragma unroll
+    for (int w = 0; w < WN; ++w) {
+        int idx = m0 - OFF + w;
+        const bool ok = !vmp || (idx >= 0 && idx < half);
+        idx &= half - 1;
+        if (w >= OFF && w < OFF + K) cw[w] = c[w - OFF];
+        else cw[w] = ok ? cat(idx) : 0.0;
+        dw[w] = ok ? ds[pidx(idx)] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            if ((u & 1) == 0) {
+                const int idx = OFF - u / 2 + q;
+                a0 = fma(tp.h[u + NU - 1], cw[idx], a0);
+                b0 = fma(tp.g[u + NU - 1], dw[idx], b0);
+            } else {
+                const int idx = OFF - (u - 1) / 2 + q;
+                a1 = fma(tp.h[u + NU - 1], cw[idx], a1);
+                b1 = fma(tp.g[u + NU - 1], dw[idx], b1);
+            }
+        }
+        f[2 * q] = a0 + b0;
+        f[2 * q + 1] = a1 + b1;
+    }
+}
+
+// analysis rows k0..k0+K of a length-n level from the fine segment x[2K];
+// xs: padded copy of the fine level (halos, VMP edge rows)
+template <int NU, int K>
+__device__ __forceinline__ void ana_seg(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* xs, int n, int k0,
+                                        bool vmp, const double (&x)[2 * K], double (&c)[K], double (&d)[K]) {
+    constexpr int WL = NU - 1, WN = 2 * K + 2 * NU - 2;
+    double xw[WN];
+#pragma unroll
+    for (int w = 0; w < WN; ++w) {
+        int idx = 2 * k0 - WL + w;
+        const bool ok = !vmp || (idx >= 0 && idx < n);
+        idx &= n - 1;
+        if (w >= WL && w < WL + 2 * K) xw[w] = x[w - WL];
+        else xw[w] = ok ? xs[pidx(idx)] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int u = -NU + 1; u <= NU; ++u) {
+            const double xv = xw[2 * r + u + WL];
+            if (u & 1) {
+                a1 = fma(tp.h[u + NU - 1], xv, a1);
+                b1 = fma(tp.g[u + NU - 1], xv, b1);
+            } else {
+                a0 = fma(tp.h[u + NU - 1], xv, a0);
+                b0 = fma(tp.g[u + NU - 1], xv, b0);
+            }
+        }
+        c[r] = a0 + a1;
+        d[r] = b0 + b1;
+    }
+}
+
+// synthesis levels with K coarse values per thread, recursing up to KT; the
+// level written by each step goes (padded) to `dst`, the next step swaps.
+template <int NU, int K, int KT, bool PADIN>
+__device__ __forceinline__ void syn_up(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* xin,
+                                       const double* cs, double* dst, double* alt, bool vmp, const double (&c)[K],
+                                       double (&fine)[2 * KT], double*& top) {
+    const int tid = threadIdx.x;
+    const int half = K * kRegNT, n = 2 * half;
+    double f[2 * K];
+    const double* ds = xin + pidx(half);  // details of this level (xin padded)
+    syn_seg<NU, K, PADIN>(F, tp, cs, ds, n, tid * K, vmp, c, f);
+    constexpr int EL = FiltSmem<NU>::EL, CI = FiltSmem<NU>::CI;
+    const int i0 = 2 * K * tid;
+    const bool edge = vmp && (i0 < EL || i0 + 2 * K > n - EL);
+#pragma unroll
+    for (int q = 0; q < 2 * K; ++q)
+        if (!(edge && (i0 + q < EL || i0 + q >= n - EL))) dst[pidx(i0 + q)] = f[q];
+    if (vmp && tid < 2 * EL) {  // VMP edge samples from the dense edge blocks, one per helper thread
+        const int side = tid < EL ? 0 : 1, ii = side ? tid - EL : tid, i = side ? n - 1 - ii : ii;
+        const double* sc = F.syn(side, ii, 0);
+        const double* sd = F.syn(side, ii, 1);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < CI; ++k) {
+            const int idx = side ? half - 1 - k : k;
+            const double cv = PADIN ? cs[pidx(idx)] : cs[idx];
+            acc += sc[k * EL] * cv + sd[k * EL] * ds[pidx(idx)];
+        }
+        dst[pidx(i)] = acc;
+    }
+    __syncthreads();
+    if (edge) {
+#pragma unroll
+        for (int q = 0; q < 2 * K; ++q)
+            if (i0 + q < EL || i0 + q >= n - EL) f[q] = dst[pidx(i0 + q)];
+    }
+    if constexpr (K == KT) {
+#pragma unroll
+        for (int q = 0; q < 2 * K; ++q) fine[q] = f[q];
+        top = dst;
+    } else {
+        syn_up<NU, 2 * K, KT, true>(F, tp, xin, dst, alt, dst, vmp, f, fine, top);
+    }
+}
+
+// analysis levels with 2K fine values per thread, recursing down to K = 1;
+// xs: padded copy of the level being analysed, other: free padded buffer;
+// the K = 1 step leaves its 2^kRegLog coarse values PLAIN in `low`
+template <int NU, int K>
+__device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& tp, double* out, double* xs,
+                                         double* other, double* low, bool vmp, const double (&x)[2 * K]) {
+    const int tid = threadIdx.x;
+    const int half = K * kRegNT;
+    double c[K], d[K];
+    const int n = 2 * half, k0 = tid * K;
+    ana_seg<NU, K>(F, tp, xs, n, k0, vmp, x, c, d);
+    const bool edge = vmp && (k0 < NU || k0 + K > half - NU);
+    auto is_edge = [&](int k) { return k < NU || k >= half - NU; };
+    double* od = out + half + k0;
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+        if (!(edge && is_edge(k0 + r))) od[r] = d[r];
+    if (vmp && tid < 2 * NU) {  // VMP edge rows (wavelet.cpp:403-445), one per helper thread
+        constexpr int EL = FiltSmem<NU>::EL;
+        const int side = tid < NU ? 0 : 1, m = side ? tid - NU : tid, k = side ? half - 1 - m : m;
+        const double* ra = F.ana(side, 0, m);
+        const double* rb = F.ana(side, 1, m);
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int q = 0; q < EL; ++q) {
+            const double xv = xs[pidx(side ? n - 1 - q : q)];
+            a += ra[q] * xv;
+            b += rb[q] * xv;
+        }
+        out[half + k] = b;
+        if (K == 1) low[k] = a;
+        else other[pidx(k)] = a;
+    }
+    if constexpr (K == 1) {
+        if (!edge) low[tid] = c[0];
+        __syncthreads();
+    } else {
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+            if (!(edge && is_edge(k0 + r))) other[pidx(k0 + r)] = c[r];
+        __syncthreads();
+        if (edge) {
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+                if (is_edge(k0 + r)) c[r] = other[pidx(k0 + r)];
+        }
+        double x2[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) x2[r] = c[r];
+        ana_down<NU, K / 2>(F, tp, out, other, xs, low, vmp, x2);
+    }
+}
+
+template <int NU, int J>
+__global__ void __launch_bounds__(kRegNT, 2) k_normal_rows_reg(NormArgs p) {
+    constexpr int M = 1 << J, KT = M / (2 * kRegNT), FT = 2 * KT;  // fine values per thread
+    constexpr int FS = FiltSmem<NU>::SIZE, W = 4 * NU - 3, Bw = 2 * NU - 2, PM = M + M / 32;
+    constexpr int NL = 1 << kRegLog;
+    static_assert(NL == kRegNT, "one level-kRegLog value per thread");
+    extern __shared__ double sm[];
+    double* filt = sm;
+    double* gE = sm + FS;
+    double* X = gE + 2 * p.E * W;  // staged input row, padded (coarse + every level's details)
+    double* Pa = X + PM;           // padded level copies
+    double* Pb = Pa + PM;
+    double* L0 = Pb + PM;          // plain buffers of the coarse (<= 2^kRegLog) levels
+    double* L1 = L0 + NL;
+    double* XL = L1 + NL;          // plain copy of the input's first 2^kRegLog values
+    pdl_trigger();
+    pdl_wait();
+    const int tid = threadIdx.x;
+    const bool vmp = p.vmp != 0;
+    for (int i = tid; i < FS; i += kRegNT) filt[i] = p.tab[p.t.o_h + i];
+    for (int i = tid; i < 2 * p.E * W; i += kRegNT) gE[i] = p.band[i];
+    double gI[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) gI[d] = __ldg(p.band + 2 * p.E * W + d);
+    const double* xg = p.in + (long long)blockIdx.x * p.in_vs;
+    double* out = p.out + (long long)blockIdx.x * p.out_vs;
+#pragma unroll
+    for (int r = 0; r < M / kRegNT; ++r) cp_async8(X + pidx(tid + r * kRegNT), xg + tid + r * kRegNT);
+    cp_async8(XL + tid, xg + tid);  // kRegNT == 2^kRegLog
+    cp_async_wait_all();
+    __syncthreads();
+    const FiltSmem<NU> F{filt};
+    const Taps<NU> tp(F);
+    // coarse synthesis levels r0+1 .. kRegLog (plain shared memory)
+    const int nc = 1 << p.r0;
+    const double* src = XL;  // the level-r0 coarse values lead the input row
+    double* dst = L0;
+    for (int lev = p.r0 + 1; lev <= kRegLog; ++lev) {
+        const int n = 1 << lev;
+        idwt_level_vec<NU>(F, src, XL + (n >> 1), dst, n, vmp, tid, kRegNT);
+        __syncthreads();
+        src = dst;
+        dst = (dst == L0) ? L1 : L0;
+    }
+    // register levels kRegLog+1 .. J
+    double fine[FT];
+    double* top = nullptr;
+    {
+        const double c1[1] = {src[tid]};
+        syn_up<NU, 1, KT, false>(F, tp, X, src, Pa, Pb, vmp, c1, fine, top);
+    }
+    double* fre = (top == Pa) ? Pb : Pa;
+    // band product in registers (halos / edge rows from the padded top level)
+    double y[FT];
+    {
+        const int i0 = tid * FT;
+        constexpr int WN = FT + 2 * Bw;
+        double xw[WN];
+#pragma unroll
+        for (int w = 0; w < WN; ++w) {
+            const int idx = i0 - Bw + w;
+            if (w >= Bw && w < Bw + FT) xw[w] = fine[w - Bw];
+            else xw[w] = (!vmp || (idx >= 0 && idx < M)) ? top[pidx(idx & (M - 1))] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < FT; ++r) {
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                if (d & 1) a1 = fma(gI[d], xw[r + d], a1);
+                else a0 = fma(gI[d], xw[r + d], a0);
+            }
+            y[r] = a0 + a1;
+        }
+    }
+    const int i0 = tid * FT;
+    const bool bedge = i0 < p.E || i0 + FT > M - p.E;
+#pragma unroll
+    for (int r = 0; r < FT; ++r)
+        if (!(bedge && (i0 + r < p.E || i0 + r >= M - p.E))) fre[pidx(i0 + r)] = y[r];
+    if (tid < 2 * p.E) {  // tabulated edge rows of the band, one per helper thread
+        const int i = tid < p.E ? tid : M - 2 * p.E + tid;
+        double acc = 0.0;
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+            int k = i + d - Bw;
+            if (!vmp) k &= M - 1;
+            if (k >= 0 && k < M) acc = fma(gE[tid * W + d], top[pidx(k)], acc);
+        }
+        fre[pidx(i)] = acc;
+    }
+    __syncthreads();
+    if (bedge) {
+#pragma unroll
+        for (int r = 0; r < FT; ++r)
+            if (i0 + r < p.E || i0 + r >= M - p.E) y[r] = fre[pidx(i0 + r)];
+    }
+    // analysis: register levels J .. kRegLog+1, then the coarse levels (plain)
+    ana_down<NU, KT>(F, tp, out, fre, top, L0, vmp, y);
+    double* cur = L0;
+    double* nxt = L1;
+    for (int lev = kRegLog; lev > p.r0; --lev) {
+        const int n = 1 << lev, half = n >> 1;
+        dwt_level_vec<NU>(F, tp, cur, nxt, out + half, n, vmp, tid, kRegNT);
+        __syncthreads();
+        double* t0 = cur;
+        cur = nxt;
+        nxt = t0;
+    }
+    for (int i = tid; i < nc; i += kRegNT) out[i] = cur[i];
+}
+
+// ---------------------------------------------------------------------------
 // large path: two-pass Hadamard over K with an L2-resident intermediate
 // ---------------------------------------------------------------------------
 // G per vector: [2^kh chunks][R1 physical rows][CW]; chunk c = K_hi (forward

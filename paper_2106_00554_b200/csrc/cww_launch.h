@@ -42,7 +42,8 @@ cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
-constexpr int kSmallMaxLog = 12;  // M <= 2^12: whole map in one CTA's shared memory
+constexpr int kSmallMaxLog = 12;
+constexpr int kRegNT = 256, kRegLog = 8;  // register-resident normal rows: threads, shared-memory levels <= 2^8  // M <= 2^12: whole map in one CTA's shared memory
 
 struct SmallArgs {
     const double* tab;  // per-op device table block

@@ -147,6 +147,30 @@ cudaError_t CWW_FN(launch_normal_rows_nu)(const NormArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+namespace {
+template <int J>
+cudaError_t normal_reg_t(const NormArgs& a, cudaStream_t st) {
+    const long long smem = (FiltSmem<CWW_NU>::SIZE + 2ll * a.E * (4 * CWW_NU - 3) +
+                            3ll * ((1 << J) + (1 << J) / 32) + 3ll * (1 << kRegLog)) * 8;
+    auto k = k_normal_rows_reg<CWW_NU, J>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaError_t e = launch_k(k, dim3((unsigned)a.nvec), dim3(kRegNT), (size_t)smem, st, a); e != cudaSuccess)
+        return e;
+    return cudaGetLastError();
+}
+}  // namespace
+
+// register-resident variant: use_idwt, 2^9 <= M <= 2^12, r0 < kRegLog
+cudaError_t CWW_FN(launch_normal_rows_reg_nu)(const NormArgs& a, cudaStream_t st) {
+    switch (a.j) {
+        case 9: return normal_reg_t<9>(a, st);
+        case 10: return normal_reg_t<10>(a, st);
+        case 11: return normal_reg_t<11>(a, st);
+        case 12: return normal_reg_t<12>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
     const int nt = 256;
     if (w.kind == 0) {
