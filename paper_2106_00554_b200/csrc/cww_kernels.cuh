@@ -1299,12 +1299,12 @@ __device__ __forceinline__ void ana_seg(const FiltSmem<NU>& F, const Taps<NU>& t
 
 // synthesis levels with K coarse values per thread, recursing up to KT; the
 // level written by each step goes (padded) to `dst`, the next step swaps.
-template <int NU, int K, int KT, bool PADIN>
+template <int NU, int K, int KT, bool PADIN, int RNT>
 __device__ __forceinline__ void syn_up(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* xin,
                                        const double* cs, double* dst, double* alt, bool vmp, const double (&c)[K],
                                        double (&fine)[2 * KT], double*& top) {
     const int tid = threadIdx.x;
-    const int half = K * kRegNT, n = 2 * half;
+    const int half = K * RNT, n = 2 * half;
     double f[2 * K];
     const double* ds = xin + pidx(half);  // details of this level (xin padded)
     syn_seg<NU, K, PADIN>(F, tp, cs, ds, n, tid * K, vmp, c, f);
@@ -1338,18 +1338,18 @@ __device__ __forceinline__ void syn_up(const FiltSmem<NU>& F, const Taps<NU>& tp
         for (int q = 0; q < 2 * K; ++q) fine[q] = f[q];
         top = dst;
     } else {
-        syn_up<NU, 2 * K, KT, true>(F, tp, xin, dst, alt, dst, vmp, f, fine, top);
+        syn_up<NU, 2 * K, KT, true, RNT>(F, tp, xin, dst, alt, dst, vmp, f, fine, top);
     }
 }
 
 // analysis levels with 2K fine values per thread, recursing down to K = 1;
 // xs: padded copy of the level being analysed, other: free padded buffer;
-// the K = 1 step leaves its 2^kRegLog coarse values PLAIN in `low`
-template <int NU, int K>
+// the K = 1 step leaves its 2^RLOG coarse values PLAIN in `low`
+template <int NU, int K, int RNT>
 __device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& tp, double* out, double* xs,
                                          double* other, double* low, bool vmp, const double (&x)[2 * K]) {
     const int tid = threadIdx.x;
-    const int half = K * kRegNT;
+    const int half = K * RNT;
     double c[K], d[K];
     const int n = 2 * half, k0 = tid * K;
     ana_seg<NU, K>(F, tp, xs, n, k0, vmp, x, c, d);
@@ -1391,60 +1391,61 @@ __device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& 
         double x2[K];
 #pragma unroll
         for (int r = 0; r < K; ++r) x2[r] = c[r];
-        ana_down<NU, K / 2>(F, tp, out, other, xs, low, vmp, x2);
+        ana_down<NU, K / 2, RNT>(F, tp, out, other, xs, low, vmp, x2);
     }
 }
 
-template <int NU, int J>
-__global__ void __launch_bounds__(kRegNT, 2) k_normal_rows_reg(NormArgs p) {
-    constexpr int M = 1 << J, KT = M / (2 * kRegNT), FT = 2 * KT;  // fine values per thread
+template <int NU, int J, int RNT>
+__global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
+    constexpr int RLOG = RNT == 512 ? 9 : (RNT == 256 ? 8 : 7);  // levels <= 2^RLOG: shared memory
+    constexpr int M = 1 << J, KT = M / (2 * RNT), FT = 2 * KT;  // fine values per thread
     constexpr int FS = FiltSmem<NU>::SIZE, W = 4 * NU - 3, Bw = 2 * NU - 2, PM = M + M / 32;
-    constexpr int NL = 1 << kRegLog;
-    static_assert(NL == kRegNT, "one level-kRegLog value per thread");
+    constexpr int NL = 1 << RLOG;
+    static_assert(NL == RNT, "one level-RLOG value per thread");
     extern __shared__ double sm[];
     double* filt = sm;
     double* gE = sm + FS;
     double* X = gE + 2 * p.E * W;  // staged input row, padded (coarse + every level's details)
     double* Pa = X + PM;           // padded level copies
     double* Pb = Pa + PM;
-    double* L0 = Pb + PM;          // plain buffers of the coarse (<= 2^kRegLog) levels
+    double* L0 = Pb + PM;          // plain buffers of the coarse (<= 2^RLOG) levels
     double* L1 = L0 + NL;
-    double* XL = L1 + NL;          // plain copy of the input's first 2^kRegLog values
+    double* XL = L1 + NL;          // plain copy of the input's first 2^RLOG values
     pdl_trigger();
     pdl_wait();
     const int tid = threadIdx.x;
     const bool vmp = p.vmp != 0;
-    for (int i = tid; i < FS; i += kRegNT) filt[i] = p.tab[p.t.o_h + i];
-    for (int i = tid; i < 2 * p.E * W; i += kRegNT) gE[i] = p.band[i];
+    for (int i = tid; i < FS; i += RNT) filt[i] = p.tab[p.t.o_h + i];
+    for (int i = tid; i < 2 * p.E * W; i += RNT) gE[i] = p.band[i];
     double gI[W];
 #pragma unroll
     for (int d = 0; d < W; ++d) gI[d] = __ldg(p.band + 2 * p.E * W + d);
     const double* xg = p.in + (long long)blockIdx.x * p.in_vs;
     double* out = p.out + (long long)blockIdx.x * p.out_vs;
 #pragma unroll
-    for (int r = 0; r < M / kRegNT; ++r) cp_async8(X + pidx(tid + r * kRegNT), xg + tid + r * kRegNT);
-    cp_async8(XL + tid, xg + tid);  // kRegNT == 2^kRegLog
+    for (int r = 0; r < M / RNT; ++r) cp_async8(X + pidx(tid + r * RNT), xg + tid + r * RNT);
+    cp_async8(XL + tid, xg + tid);  // RNT == 2^RLOG
     cp_async_wait_all();
     __syncthreads();
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
-    // coarse synthesis levels r0+1 .. kRegLog (plain shared memory)
+    // coarse synthesis levels r0+1 .. RLOG (plain shared memory)
     const int nc = 1 << p.r0;
     const double* src = XL;  // the level-r0 coarse values lead the input row
     double* dst = L0;
-    for (int lev = p.r0 + 1; lev <= kRegLog; ++lev) {
+    for (int lev = p.r0 + 1; lev <= RLOG; ++lev) {
         const int n = 1 << lev;
-        idwt_level_vec<NU>(F, src, XL + (n >> 1), dst, n, vmp, tid, kRegNT);
+        idwt_level_vec<NU>(F, src, XL + (n >> 1), dst, n, vmp, tid, RNT);
         __syncthreads();
         src = dst;
         dst = (dst == L0) ? L1 : L0;
     }
-    // register levels kRegLog+1 .. J
+    // register levels RLOG+1 .. J
     double fine[FT];
     double* top = nullptr;
     {
         const double c1[1] = {src[tid]};
-        syn_up<NU, 1, KT, false>(F, tp, X, src, Pa, Pb, vmp, c1, fine, top);
+        syn_up<NU, 1, KT, false, RNT>(F, tp, X, src, Pa, Pb, vmp, c1, fine, top);
     }
     double* fre = (top == Pa) ? Pb : Pa;
     // band product in registers (halos / edge rows from the padded top level)
@@ -1492,19 +1493,19 @@ __global__ void __launch_bounds__(kRegNT, 2) k_normal_rows_reg(NormArgs p) {
         for (int r = 0; r < FT; ++r)
             if (i0 + r < p.E || i0 + r >= M - p.E) y[r] = fre[pidx(i0 + r)];
     }
-    // analysis: register levels J .. kRegLog+1, then the coarse levels (plain)
-    ana_down<NU, KT>(F, tp, out, fre, top, L0, vmp, y);
+    // analysis: register levels J .. RLOG+1, then the coarse levels (plain)
+    ana_down<NU, KT, RNT>(F, tp, out, fre, top, L0, vmp, y);
     double* cur = L0;
     double* nxt = L1;
-    for (int lev = kRegLog; lev > p.r0; --lev) {
+    for (int lev = RLOG; lev > p.r0; --lev) {
         const int n = 1 << lev, half = n >> 1;
-        dwt_level_vec<NU>(F, tp, cur, nxt, out + half, n, vmp, tid, kRegNT);
+        dwt_level_vec<NU>(F, tp, cur, nxt, out + half, n, vmp, tid, RNT);
         __syncthreads();
         double* t0 = cur;
         cur = nxt;
         nxt = t0;
     }
-    for (int i = tid; i < nc; i += kRegNT) out[i] = cur[i];
+    for (int i = tid; i < nc; i += RNT) out[i] = cur[i];
 }
 
 // ---------------------------------------------------------------------------

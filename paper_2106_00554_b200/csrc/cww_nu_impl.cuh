@@ -148,13 +148,14 @@ cudaError_t CWW_FN(launch_normal_rows_nu)(const NormArgs& a, cudaStream_t st) {
 }
 
 namespace {
-template <int J>
+template <int J, int RNT>
 cudaError_t normal_reg_t(const NormArgs& a, cudaStream_t st) {
+    constexpr int RLOG = RNT == 512 ? 9 : 8;
     const long long smem = (FiltSmem<CWW_NU>::SIZE + 2ll * a.E * (4 * CWW_NU - 3) +
-                            3ll * ((1 << J) + (1 << J) / 32) + 3ll * (1 << kRegLog)) * 8;
-    auto k = k_normal_rows_reg<CWW_NU, J>;
+                            3ll * ((1 << J) + (1 << J) / 32) + 3ll * (1 << RLOG)) * 8;
+    auto k = k_normal_rows_reg<CWW_NU, J, RNT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaError_t e = launch_k(k, dim3((unsigned)a.nvec), dim3(kRegNT), (size_t)smem, st, a); e != cudaSuccess)
+    if (cudaError_t e = launch_k(k, dim3((unsigned)a.nvec), dim3(RNT), (size_t)smem, st, a); e != cudaSuccess)
         return e;
     return cudaGetLastError();
 }
@@ -162,11 +163,23 @@ cudaError_t normal_reg_t(const NormArgs& a, cudaStream_t st) {
 
 // register-resident variant: use_idwt, 2^9 <= M <= 2^12, r0 < kRegLog
 cudaError_t CWW_FN(launch_normal_rows_reg_nu)(const NormArgs& a, cudaStream_t st) {
+    static const int rnt = [] {
+        const char* e = std::getenv("CWW_NORMAL_RNT");
+        return e && std::atoi(e) == 256 ? 256 : 512;
+    }();
+    if (rnt == 512 && a.j >= 10 && a.r0 < 9) {
+        switch (a.j) {
+            case 10: return normal_reg_t<10, 512>(a, st);
+            case 11: return normal_reg_t<11, 512>(a, st);
+            case 12: return normal_reg_t<12, 512>(a, st);
+            default: break;
+        }
+    }
     switch (a.j) {
-        case 9: return normal_reg_t<9>(a, st);
-        case 10: return normal_reg_t<10>(a, st);
-        case 11: return normal_reg_t<11>(a, st);
-        case 12: return normal_reg_t<12>(a, st);
+        case 9: return normal_reg_t<9, 256>(a, st);
+        case 10: return normal_reg_t<10, 256>(a, st);
+        case 11: return normal_reg_t<11, 256>(a, st);
+        case 12: return normal_reg_t<12, 256>(a, st);
         default: return cudaErrorInvalidValue;
     }
 }
