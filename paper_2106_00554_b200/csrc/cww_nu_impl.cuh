@@ -165,7 +165,7 @@ cudaError_t normal_reg_t(const NormArgs& a, cudaStream_t st) {
 cudaError_t CWW_FN(launch_normal_rows_reg_nu)(const NormArgs& a, cudaStream_t st) {
     static const int rnt = [] {
         const char* e = std::getenv("CWW_NORMAL_RNT");
-        return e && std::atoi(e) == 256 ? 256 : 512;
+        return e && std::atoi(e) == 512 ? 512 : 256;
     }();
     if (rnt == 512 && a.j >= 10 && a.r0 < 9) {
         switch (a.j) {
