@@ -94,12 +94,17 @@ cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long
     return cudaGetLastError();
 }
 
-cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st) {
+bool normal_reg_ok(int nu, int j, int r0, int use_idwt) {
+    (void)nu;
     static const bool reg = [] {
         const char* e = std::getenv("CWW_NORMAL_REG");
         return !(e && e[0] == '0');
     }();
-    if (reg && a.use_idwt && a.j >= 9 && a.j <= 12 && a.r0 < kRegLog && a.V <= 1) {
+    return reg && use_idwt && j >= 9 && j <= 12 && r0 < kRegLog;
+}
+
+cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st) {
+    if (normal_reg_ok(nu, a.j, a.r0, a.use_idwt) && (a.V <= 1 || a.es > 0)) {
 #define C(N) launch_normal_rows_reg_nu##N(a, st)
         SWITCH_NU(nu, C)
 #undef C

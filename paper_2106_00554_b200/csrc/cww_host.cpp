@@ -1359,7 +1359,7 @@ cww::NormArgs norm_args(const cww_op* op, double* x, long long nvec) {
     a.r0 = op->r0;
     a.use_idwt = op->d.use_idwt;
     a.vmp = op->vmp;
-    a.V = int(std::max<long long>(1, 4096 / op->M));
+    a.V = cww::normal_reg_ok(op->nu, int(op->j), op->r0, op->d.use_idwt) ? 1 : int(std::max<long long>(1, 4096 / op->M));
     return a;
 }
 
@@ -1374,6 +1374,29 @@ cww_status normal_banded(const cww_op* op, double* x, double* w, long long batch
         cww::NormArgs a = norm_args(op, x, batch);
         for (int it = 0; it < iters; ++it) {
             Prof pr("normal_rows", st);
+            CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
+        }
+        return CWW_OK;
+    }
+    static const bool strided = [] {
+        const char* e = std::getenv("CWW_NORMAL_STRIDED");
+        return e && e[0] == '1';
+    }();
+    if (strided && cww::normal_reg_ok(op->nu, int(op->j), op->r0, op->d.use_idwt)) {
+        // register kernel: rows in place, then columns in place (strided, no transposes).
+        // Opt-in: measured at config 5 the strided column pass costs 2.1x a row pass,
+        // more than the transpose it saves (27.3 vs 19.4 ms per 50 iterations).
+        for (int it = 0; it < iters; ++it) {
+            cww::NormArgs a = norm_args(op, x, batch * M);
+            {
+                Prof pr("normal_rows", st);
+                CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
+            }
+            a.vpi = M;
+            a.ivs = M * M;
+            a.in_vs = a.out_vs = 1;
+            a.es = M;
+            Prof pr("normal_cols", st);
             CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
         }
         return CWW_OK;

@@ -1077,7 +1077,8 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
 // (VMP) / all rows (periodic, masked) through dwt_pair.
 template <int NU>
 __device__ __forceinline__ void dwt_level_vec(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* x,
-                                              double* dstc, double* dstd, int n, bool vmp, int t0, int nthr) {
+                                              double* dstc, double* dstd, int n, bool vmp, int t0, int nthr,
+                                              long long dstride = 1) {
     const int half = n >> 1;
     const int klo = vmp ? NU : (NU + 1) / 2 + 1, khi = vmp ? half - NU : half - NU;
     for (int k = klo + t0; k < khi; k += nthr) {
@@ -1094,7 +1095,7 @@ __device__ __forceinline__ void dwt_level_vec(const FiltSmem<NU>& F, const Taps<
             }
         }
         dstc[k] = a0 + a1;
-        dstd[k] = b0 + b1;
+        dstd[k * dstride] = b0 + b1;
     }
     const int nl = klo, nr = half - khi;
     for (int r = nthr - 1 - t0; r < nl + nr; r += nthr) {  // boundary rows
@@ -1102,7 +1103,7 @@ __device__ __forceinline__ void dwt_level_vec(const FiltSmem<NU>& F, const Taps<
         double c, d;
         dwt_pair<NU>(F, x, n, k, vmp, c, d);
         dstc[k] = c;
-        dstd[k] = d;
+        dstd[k * dstride] = d;
     }
 }
 
@@ -1346,8 +1347,8 @@ __device__ __forceinline__ void syn_up(const FiltSmem<NU>& F, const Taps<NU>& tp
 // xs: padded copy of the level being analysed, other: free padded buffer;
 // the K = 1 step leaves its 2^RLOG coarse values PLAIN in `low`
 template <int NU, int K, int RNT>
-__device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& tp, double* out, double* xs,
-                                         double* other, double* low, bool vmp, const double (&x)[2 * K]) {
+__device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& tp, double* out, long long es,
+                                         double* xs, double* other, double* low, bool vmp, const double (&x)[2 * K]) {
     const int tid = threadIdx.x;
     const int half = K * RNT;
     double c[K], d[K];
@@ -1355,10 +1356,10 @@ __device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& 
     ana_seg<NU, K>(F, tp, xs, n, k0, vmp, x, c, d);
     const bool edge = vmp && (k0 < NU || k0 + K > half - NU);
     auto is_edge = [&](int k) { return k < NU || k >= half - NU; };
-    double* od = out + half + k0;
+    double* od = out + (half + k0) * es;
 #pragma unroll
     for (int r = 0; r < K; ++r)
-        if (!(edge && is_edge(k0 + r))) od[r] = d[r];
+        if (!(edge && is_edge(k0 + r))) od[r * es] = d[r];
     if (vmp && tid < 2 * NU) {  // VMP edge rows (wavelet.cpp:403-445), one per helper thread
         constexpr int EL = FiltSmem<NU>::EL;
         const int side = tid < NU ? 0 : 1, m = side ? tid - NU : tid, k = side ? half - 1 - m : m;
@@ -1371,7 +1372,7 @@ __device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& 
             a += ra[q] * xv;
             b += rb[q] * xv;
         }
-        out[half + k] = b;
+        out[(half + k) * es] = b;
         if (K == 1) low[k] = a;
         else other[pidx(k)] = a;
     }
@@ -1391,7 +1392,7 @@ __device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& 
         double x2[K];
 #pragma unroll
         for (int r = 0; r < K; ++r) x2[r] = c[r];
-        ana_down<NU, K / 2, RNT>(F, tp, out, other, xs, low, vmp, x2);
+        ana_down<NU, K / 2, RNT>(F, tp, out, es, other, xs, low, vmp, x2);
     }
 }
 
@@ -1420,11 +1421,14 @@ __global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
     double gI[W];
 #pragma unroll
     for (int d = 0; d < W; ++d) gI[d] = __ldg(p.band + 2 * p.E * W + d);
-    const double* xg = p.in + (long long)blockIdx.x * p.in_vs;
-    double* out = p.out + (long long)blockIdx.x * p.out_vs;
+    const long long v = blockIdx.x;
+    const long long es = p.es > 0 ? p.es : 1;
+    const long long vb = p.es > 0 ? (v / p.vpi) * p.ivs + (v % p.vpi) * p.in_vs : v * p.in_vs;
+    const double* xg = p.in + vb;
+    double* out = p.out + (p.es > 0 ? vb : v * p.out_vs);
 #pragma unroll
-    for (int r = 0; r < M / RNT; ++r) cp_async8(X + pidx(tid + r * RNT), xg + tid + r * RNT);
-    cp_async8(XL + tid, xg + tid);  // RNT == 2^RLOG
+    for (int r = 0; r < M / RNT; ++r) cp_async8(X + pidx(tid + r * RNT), xg + (tid + r * RNT) * es);
+    cp_async8(XL + tid, xg + tid * es);  // RNT == 2^RLOG
     cp_async_wait_all();
     __syncthreads();
     const FiltSmem<NU> F{filt};
@@ -1494,18 +1498,18 @@ __global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
             if (i0 + r < p.E || i0 + r >= M - p.E) y[r] = fre[pidx(i0 + r)];
     }
     // analysis: register levels J .. RLOG+1, then the coarse levels (plain)
-    ana_down<NU, KT, RNT>(F, tp, out, fre, top, L0, vmp, y);
+    ana_down<NU, KT, RNT>(F, tp, out, es, fre, top, L0, vmp, y);
     double* cur = L0;
     double* nxt = L1;
     for (int lev = RLOG; lev > p.r0; --lev) {
         const int n = 1 << lev, half = n >> 1;
-        dwt_level_vec<NU>(F, tp, cur, nxt, out + half, n, vmp, tid, RNT);
+        dwt_level_vec<NU>(F, tp, cur, nxt, out + half * es, n, vmp, tid, RNT, es);
         __syncthreads();
         double* t0 = cur;
         cur = nxt;
         nxt = t0;
     }
-    for (int i = tid; i < nc; i += RNT) out[i] = cur[i];
+    for (int i = tid; i < nc; i += RNT) out[i * es] = cur[i];
 }
 
 // ---------------------------------------------------------------------------

@@ -155,8 +155,14 @@ struct NormArgs {
     double* out;
     long long in_vs, out_vs, nvec;
     int j, r0, use_idwt, vmp, V;
+    // register kernel only: vector v starts at (v / vpi) * ivs + (v % vpi) * vs and
+    // its elements are es apart (columns of row-major images: vpi = M, ivs = M^2,
+    // vs = 1, es = M); es = 0 means the contiguous layout above
+    long long vpi, ivs, es;
 };
 cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st);
+// the register-resident kernel serves this shape (strided layouts need it)
+bool normal_reg_ok(int nu, int j, int r0, int use_idwt);
 // Batched out-of-place transpose of n x n fp64 matrices (matrix stride n*n).
 cudaError_t launch_transpose(const double* in, double* out, long long n, long long batch, cudaStream_t st);
 
