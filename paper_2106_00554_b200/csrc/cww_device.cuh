@@ -122,9 +122,10 @@ __device__ __forceinline__ void tile_hadamard_pass(double* T, int V, int a, int 
                                                    int tid, int nt) {
     const int groups = (1 << a) >> R;
     const int items = V * CW * groups;
+    // (e, rest) = (it % CW, it / CW), stepped incrementally (no division per item)
+    int e = tid % CW, rest = tid / CW;
+    const int de = nt % CW, dr = nt / CW;
     for (int it = tid; it < items; it += nt) {
-        const int e = it % CW;
-        const int rest = it / CW;
         const int fb = rest & (groups - 1);
         const int v = rest >> (a - R);
         const int low = fb & ((1 << lo) - 1);
@@ -136,6 +137,12 @@ __device__ __forceinline__ void tile_hadamard_pass(double* T, int V, int a, int 
         hadamard_reg<R>(x);
 #pragma unroll
         for (int k = 0; k < (1 << R); ++k) t[(k << lo) * RS] = x[k];
+        e += de;
+        rest += dr;
+        if (e >= CW) {
+            e -= CW;
+            ++rest;
+        }
     }
 }
 

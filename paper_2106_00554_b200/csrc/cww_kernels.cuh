@@ -1531,15 +1531,23 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     const int chunk = blockIdx.x, v = blockIdx.y;
     const double* xi = p.xi + (long long)v * p.xi_vs;
     double* T = sm;
-    for (int f = tid; f < R1 * CW; f += NT) {
-        const int rl = f / CW, e = f % CW;  // logical local row K_lo
-        const long long pos = (long long)(chunk * R1 + rl) * B + e - H;
-        const int ph = (int)brev_bits((unsigned)rl, kl);
-        double* dst = T + tile_idx(ph, e, RS, ph);
-        if (pos >= 0 && pos < M && !(NU > 1 && (pos < NU || pos >= M - NU)))
-            cp_async8(dst, p.xi_is_input ? p.in + p.lin.at(p.v0 + v, pos) : xi + pos);
-        else
-            *dst = 0.0;  // outside the vector, or an edge position (edge terms)
+    {
+        const double* src = p.xi_is_input ? p.in + p.lin.vbase(p.v0 + v) : xi;  // large path: contiguous
+        int e = tid % CW, rl = tid / CW;  // (f % CW, f / CW), stepped without division
+        for (int f = tid; f < R1 * CW; f += NT) {
+            const long long pos = (long long)(chunk * R1 + rl) * B + e - H;  // logical local row K_lo = rl
+            double* dst = T + (int)brev_bits((unsigned)rl, kl) * RS + e;
+            if (pos >= 0 && pos < M && !(NU > 1 && (pos < NU || pos >= M - NU)))
+                cp_async8(dst, src + pos);
+            else
+                *dst = 0.0;  // outside the vector, or an edge position (edge terms)
+            e += NT % CW;
+            rl += NT / CW;
+            if (e >= CW) {
+                e -= CW;
+                ++rl;
+            }
+        }
     }
     if (NU > 1 && tid < 2 * NU) {  // raw edge values (first / last chunk)
         const int c = tid;
@@ -1551,9 +1559,17 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     __syncthreads();
     tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
-    for (int f = tid; f < R1 * CW; f += NT) {
-        const int ph = f / CW, e = f % CW;
-        g[f] = T[tile_idx(ph, e, RS, ph)];
+    {
+        int e = tid % CW, ph = tid / CW;
+        for (int f = tid; f < R1 * CW; f += NT) {
+            g[f] = T[ph * RS + e];
+            e += NT % CW;
+            ph += NT / CW;
+            if (e >= CW) {
+                e -= CW;
+                ++ph;
+            }
+        }
     }
 }
 
@@ -1573,11 +1589,19 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
     double* T = sm + S * 2 * NP;    // NG tiles of R2 physical rows
     const int tst = R2 * RS;
     const double* g = p.G + (long long)v * A * CW;
-    for (int f = tid; f < NG * R2 * CW; f += NT) {
-        const int e = f % CW, rest = f / CW;
-        const int ng = rest & (NG - 1), khi = rest >> lng;  // NG = 2^lng
-        const int ph = (int)brev_bits((unsigned)khi, kh);
-        cp_async8(T + ng * tst + tile_idx(ph, e, RS, ph), g + ((long long)khi * R1 + rho0 + ng) * CW + e);
+    {
+        int e = tid % CW, rest = tid / CW;  // (f % CW, f / CW), stepped without division
+        for (int f = tid; f < NG * R2 * CW; f += NT) {
+            const int ng = rest & (NG - 1), khi = rest >> lng;  // NG = 2^lng
+            const int ph = (int)brev_bits((unsigned)khi, kh);
+            cp_async8(T + ng * tst + ph * RS + e, g + ((long long)khi * R1 + rho0 + ng) * CW + e);
+            e += NT % CW;
+            rest += NT / CW;
+            if (e >= CW) {
+                e -= CW;
+                ++rest;
+            }
+        }
     }
     if (NU > 1) {
         for (int f = tid; f < S * 2 * NP; f += NT) {
@@ -1671,11 +1695,17 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
     tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
     // physical row ph of sub-tile ng is logical K_hi = bitrev_kh(ph)
     double* g = p.G + (long long)v * A * CW;
+    int e = tid % CW, rest = tid / CW;  // (f % CW, f / CW), stepped without division
     for (int f = tid; f < NG * R2 * CW; f += NT) {
-        const int e = f % CW, rest = f / CW;
         const int ng = rest & (NG - 1), khi = rest >> lng;  // NG = 2^lng
         const int ph = (int)brev_bits((unsigned)khi, kh);
-        g[((long long)khi * R1 + rho0 + ng) * CW + e] = T[ng * tst + tile_idx(ph, e, RS, ph)];
+        g[((long long)khi * R1 + rho0 + ng) * CW + e] = T[ng * tst + ph * RS + e];
+        e += NT % CW;
+        rest += NT / CW;
+        if (e >= CW) {
+            e -= CW;
+            ++rest;
+        }
     }
 }
 
@@ -1696,9 +1726,18 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     double* T = nb + 2 * NU;
     double* red = T + R1 * RS;       // reduction scratch: [NT/32][2H] and [NT/FE][FE]
     const double* g = p.G + (long long)v * A * CW;
-    for (int f = tid; f < R1 * CW; f += NT) {
-        const int ph = f / CW, e = f % CW;
-        cp_async8(T + tile_idx(ph, e, RS, ph), g + ((long long)chunk * R1 + ph) * CW + e);
+    {
+        const double* gc = g + (long long)chunk * R1 * CW;
+        int e = tid % CW, ph = tid / CW;
+        for (int f = tid; f < R1 * CW; f += NT) {
+            cp_async8(T + ph * RS + e, gc + f);
+            e += NT % CW;
+            ph += NT / CW;
+            if (e >= CW) {
+                e -= CW;
+                ++ph;
+            }
+        }
     }
     // halo contributions from the neighbouring chunks' boundary rows (sums over
     // the physical rows rho of their Hadamard rows; popc is bit-reversal invariant):
