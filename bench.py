@@ -130,7 +130,7 @@ def algorithmic_bytes(cfg, kernel: str, batch: int) -> float:
     lc = min(j - 1, 13)
     per = {
         "small_fwd": M + N, "small_adj": M + N,
-        "large_fwd1": M + A * CW, "large_fwd2": A * CW + N,
+        "large_fwd1": M + A * CW, "large_fwd1_syn": M + A * CW, "large_fwd2": A * CW + N,
         "large_adj2": N + A * CW, "large_adj1": A * CW + M,
         "idwt_level": sum(2 * (1 << lev) for lev in range(lc + 1, j + 1)),
         "dwt_level": sum(2 * (1 << lev) for lev in range(lc + 1, j + 1)),

@@ -17,7 +17,9 @@ namespace cww {
     cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);                    \
     cudaError_t launch_pyr_nu##N(bool, const PyrArgs&, cudaStream_t);               \
     cudaError_t launch_normal_rows_nu##N(const NormArgs&, cudaStream_t);               \
-    cudaError_t launch_normal_rows_reg_nu##N(const NormArgs&, cudaStream_t);
+    cudaError_t launch_normal_rows_reg_nu##N(const NormArgs&, cudaStream_t);          \
+    cudaError_t launch_fwd1_syn_nu##N(const LargeArgs&, const PyrArgs&, cudaStream_t); \
+    long long fwd1_syn_smem_nu##N(int, const PyrArgs&);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6)
 #undef DECL
 
@@ -141,6 +143,20 @@ cudaError_t launch_transpose(const double* in, double* out, long long n, long lo
         k_transpose<<<dim3(g, g, (unsigned)nb), dim3(32, 8), 0, st>>>(in + b0 * n * n, out + b0 * n * n, n);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_fwd1_syn(int nu, const LargeArgs& a, const PyrArgs& p, cudaStream_t st) {
+#define C(N) launch_fwd1_syn_nu##N(a, p, st)
+    SWITCH_NU(nu, C)
+#undef C
+    return cudaErrorInvalidValue;
+}
+
+long long fwd1_syn_smem(int nu, int kl, const PyrArgs& p) {
+#define C(N) fwd1_syn_smem_nu##N(kl, p)
+    SWITCH_NU(nu, C)
+#undef C
+    return -1;
 }
 
 long long large_nslot(int nu, int q, int j, int kl, int ng) {

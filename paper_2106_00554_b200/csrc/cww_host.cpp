@@ -857,6 +857,10 @@ const int kPyrSynBot = env_int("CWW_PYR_SYN_BOT", 10);  // coarse levels <= this
 const int kWpyrLog = env_int("CWW_WPYR_LOG", 9);       // warp pyramid: 2^9 fine samples per warp
 const int kWpyrLevels = env_int("CWW_WPYR_LEVELS", 0);  // synthesis levels per launch (0: 6 if j <= 17, else 4)
 const int kWpyrAnaLevels = env_int("CWW_WPYR_ANA_LEVELS", 3);  // analysis steps per launch
+// last synthesis pyramid inside forward pass 1 (xi never written).  Off: on
+// B200 the fused kernel is no faster (cfg2 68 us vs 42 + 27 us; cfg3 slower) --
+// both halves are latency-bound, so the saved xi round trip does not show.
+const bool kFuseFwd1 = env_int("CWW_FUSE_FWD1", 0) != 0;
 
 cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     cww::PyrArgs y{};
@@ -926,6 +930,8 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     a.vmp = op->vmp;
     if (!adj) {
         const double* xi = nullptr;
+        cww::PyrArgs fused{};
+        bool use_fused = false;
         if (idwt) {
             // coarse levels r0+1..bot in one CTA per vector, then the fine
             // levels in chained warp pyramids of <= kWpyrLevels levels
@@ -958,6 +964,27 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
             int ob = 0;
             while (bot < j) {
                 const int top = std::min(j, bot + (kWpyrLevels > 0 ? kWpyrLevels : (j <= 17 ? 6 : 4)));
+                if (top == j && kFuseFwd1) {  // the last pyramid may run inside forward pass 1
+                    cww::PyrArgs y = pyr_args(op, nvec);
+                    y.top = j;
+                    y.bot = bot;
+                    y.cb = 9;  // 512-sample warp cones
+                    y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum);
+                    const int lev = j - bot, hh = nu - 1;  // halo-extended edge cones: margin
+                    y.wmax += hh + 4;
+                    y.dsum += lev * (hh + 4);
+                    y.x = in;
+                    y.lx = lin;
+                    y.src_is_x = src ? 0 : 1;
+                    y.src = src;
+                    y.src_vs = src_vs;
+                    const long long sm = cww::fwd1_syn_smem(nu, pl.kl, y);
+                    if (sm > 0 && sm <= 227 * 1024) {
+                        fused = y;
+                        use_fused = true;
+                        break;
+                    }
+                }
                 cww::PyrArgs y = pyr_args(op, nvec);
                 y.top = top;
                 y.bot = bot;
@@ -984,7 +1011,10 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
         a.xi = xi;
         a.xi_vs = M;
         a.xi_is_input = idwt ? 0 : 1;
-        {
+        if (use_fused) {
+            Prof pr("large_fwd1_syn", st);
+            CUDA_TRY(cww::launch_fwd1_syn(nu, a, fused, st));
+        } else {
             Prof pr("large_fwd1", st);
             CUDA_TRY(cww::launch_large(nu, 0, a, st));
         }

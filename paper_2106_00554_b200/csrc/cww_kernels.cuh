@@ -882,43 +882,43 @@ __device__ __forceinline__ void dwt_pair_log(const FiltSmem<NU>& F, const Taps<N
 // with __syncwarp only -- no CTA barrier after the filter staging, so the
 // warps of a CTA (and of the other resident CTAs) overlap their load,
 // compute and store phases freely.
+// One warp's synthesis cone, part 1 (lane 0): the windows of fine samples
+// [lo, hi) of level p.top down to level p.bot.  Per-warp scratch wb: ints
+// wlo/whi/doff (48 doubles), then P, Q (p.wmax each) and the detail windows D.
 template <int NU>
-__global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
-    extern __shared__ double sm[];
-    constexpr int FS = FiltSmem<NU>::SIZE;
-    double* filt = sm;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    const int per = 48 + 2 * p.wmax + p.dsum;
-    double* wb = sm + FS + wid * per;
+__device__ __forceinline__ void warp_syn_windows(const PyrArgs& p, double* wb, int lo, int hi, bool vmp) {
     int* wlo = reinterpret_cast<int*>(wb);
     int* whi = wlo + 32;
     int* doff = wlo + 64;
+    Win f{lo, hi};
+    for (int lev = p.top; lev >= p.bot; --lev) {
+        wlo[lev] = f.lo;
+        whi[lev] = f.hi;
+        if (lev > p.bot) {
+            f = syn_need(NU, 1 << lev, f, vmp);
+            if (f.hi - f.lo > p.wmax) __trap();
+        }
+    }
+    int off = 0;
+    for (int lev = p.bot + 1; lev <= p.top; ++lev) {
+        doff[lev] = off;
+        off += whi[lev - 1] - wlo[lev - 1];
+    }
+    if (off > p.dsum) __trap();
+}
+
+// part 2 (the whole warp, after the windows are visible): prefetch the
+// level-bot coarse window and every level's detail window, synthesise up to
+// level p.top and hand the top samples to put(i, value).
+template <int NU, class Put>
+__device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU>& F, const Taps<NU>& tp,
+                                             double* wb, int v, int lane, bool vmp, Put&& put) {
+    const int* wlo = reinterpret_cast<const int*>(wb);
+    const int* whi = wlo + 32;
+    const int* doff = wlo + 64;
     double* P = wb + 48;
     double* Q = P + p.wmax;
     double* D = Q + p.wmax;
-    const int c = blockIdx.x * nw + wid, v = blockIdx.y;
-    const bool vmp = p.vmp != 0;
-    for (int i = tid; i < FS; i += blockDim.x) filt[i] = p.tab[p.t.o_h + i];
-    if (lane == 0) {
-        Win f{c << p.cb, (c + 1) << p.cb};
-        for (int lev = p.top; lev >= p.bot; --lev) {
-            wlo[lev] = f.lo;
-            whi[lev] = f.hi;
-            if (lev > p.bot) {
-                f = syn_need(NU, 1 << lev, f, vmp);
-                if (f.hi - f.lo > p.wmax) __trap();
-            }
-        }
-        int off = 0;
-        for (int lev = p.bot + 1; lev <= p.top; ++lev) {
-            doff[lev] = off;
-            off += whi[lev - 1] - wlo[lev - 1];
-        }
-        if (off > p.dsum) __trap();
-    }
-    __syncthreads();  // filters (CTA-wide) and this warp's windows
     const double* xb = p.x + p.lx.vbase(p.xv0 + v);
     const double* cs = p.src_is_x ? xb : p.src + v * p.src_vs;
     {
@@ -933,9 +933,6 @@ __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
     }
     cp_async_wait_all();
     __syncwarp();
-    const FiltSmem<NU> F{filt};
-    const Taps<NU> tp(F);
-    double* ob = p.out + v * p.out_vs;
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {
         const int n = 1 << lev;
         const int clo = wlo[lev - 1], lo = wlo[lev], hi = whi[lev];
@@ -945,12 +942,37 @@ __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
             idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { q[i] = val; });
             __syncwarp();
         } else {
-            idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { ob[i] = val; });
+            idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32, put);
         }
         double* t0 = P;
         P = Q;
         Q = t0;
     }
+}
+
+// Warp-granular synthesis pyramid: every WARP owns one chunk of 2^cb fine
+// samples of level `top` and runs its own cone (windows, prefetch, levels)
+// with __syncwarp only -- no CTA barrier after the filter staging, so the
+// warps of a CTA (and of the other resident CTAs) overlap their load,
+// compute and store phases freely.
+template <int NU>
+__global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
+    pdl_trigger();  // let the next launch in the stream get resident during our tail
+    pdl_wait();     // the previous launch's results are visible from here on
+    extern __shared__ double sm[];
+    constexpr int FS = FiltSmem<NU>::SIZE;
+    double* filt = sm;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    double* wb = sm + FS + wid * (48 + 2 * p.wmax + p.dsum);
+    const int c = blockIdx.x * nw + wid, v = blockIdx.y;
+    const bool vmp = p.vmp != 0;
+    for (int i = tid; i < FS; i += blockDim.x) filt[i] = p.tab[p.t.o_h + i];
+    if (lane == 0) warp_syn_windows<NU>(p, wb, c << p.cb, (c + 1) << p.cb, vmp);
+    __syncthreads();  // filters (CTA-wide) and this warp's windows
+    const FiltSmem<NU> F{filt};
+    const Taps<NU> tp(F);
+    double* ob = p.out + v * p.out_vs;
+    warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) { ob[i] = val; });
 }
 
 // Coarse tail of an analysis pyramid launch: the last CTA of vector v to
@@ -1569,6 +1591,67 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
                 e -= CW;
                 ++ph;
             }
+        }
+    }
+}
+
+// Forward pass 1 fused with the top synthesis levels: the CTA's nw warps
+// synthesise the chunk's R1*B samples of xi (plus the H-sample halos of the
+// neighbouring chunks, computed redundantly by the first / last warp) straight
+// into the extended tile -- xi never goes through HBM -- then H over the low
+// kl bits of K and the G store as in k_large_fwd1.
+template <int NU>
+__global__ void __launch_bounds__(512, 1) k_large_fwd1_syn(LargeArgs a, PyrArgs p) {
+    using Gm = Geo<NU, kLogB>;
+    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS;
+    constexpr int FS = FiltSmem<NU>::SIZE;
+    extern __shared__ double sm[];
+    pdl_trigger();
+    pdl_wait();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+    const int j = a.j, M = 1 << j, A = 1 << (j - kLogB);
+    const int kl = a.kl, R1 = 1 << kl;
+    const int chunk = blockIdx.x, v = blockIdx.y;
+    const bool vmp = p.vmp != 0;
+    double* filt = sm;
+    double* T = sm + FS;
+    double* wb = T + R1 * RS + wid * (48 + 2 * p.wmax + p.dsum);
+    const int base = chunk * R1 * B, span = (R1 * B) / nw;
+    for (int i = tid; i < FS; i += nt) filt[i] = p.tab[p.t.o_h + i];
+    if (lane == 0) {
+        int lo = base + wid * span, hi = lo + span;
+        if (wid == 0) lo = max(0, lo - H);
+        if (wid == nw - 1) hi = min(M, hi + H);
+        warp_syn_windows<NU>(p, wb, lo, hi, vmp);
+    }
+    if (H > 0 && tid < H) {  // halo positions outside the vector are zero
+        if (chunk == 0) T[tid] = 0.0;                                                 // row 0, e < H
+        if (base + R1 * B >= M) T[(int)brev_bits((unsigned)(R1 - 1), kl) * RS + B + H + tid] = 0.0;
+    }
+    __syncthreads();
+    const FiltSmem<NU> F{filt};
+    const Taps<NU> tp(F);
+    warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) {
+        if (NU > 1 && (i < NU || i >= M - NU)) {  // raw edge values; the tile holds 0 there
+            a.ev[(long long)v * 2 * NU + (i < NU ? i : NU + i - (M - NU))] = val;
+            val = 0.0;
+        }
+        const int r = i - base + H;  // position in the chunk's extended range [0, R1 B + 2H)
+        const int rl = r >> kLogB, e = r & (B - 1);
+        if (rl < R1) T[(int)brev_bits((unsigned)rl, kl) * RS + e] = val;
+        if (e < 2 * H && rl >= 1) T[(int)brev_bits((unsigned)(rl - 1), kl) * RS + e + B] = val;
+    });
+    __syncthreads();
+    tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, nt);
+    double* g = a.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
+    int e = tid % CW, ph = tid / CW;
+    for (int f = tid; f < R1 * CW; f += nt) {
+        g[f] = T[ph * RS + e];
+        e += nt % CW;
+        ph += nt / CW;
+        if (e >= CW) {
+            e -= CW;
+            ++ph;
         }
     }
 }

@@ -139,6 +139,9 @@ struct PyrArgs {
 };
 
 cudaError_t launch_pyr(int nu, bool analysis, const PyrArgs& a, cudaStream_t st);
+// forward pass 1 fused with the last synthesis pyramid (top = j); smem query (-1: n/a)
+cudaError_t launch_fwd1_syn(int nu, const LargeArgs& a, const PyrArgs& p, cudaStream_t st);
+long long fwd1_syn_smem(int nu, int kl, const PyrArgs& p);
 
 // Normal form of the full-mask operator along one axis (SURVEY.md 8d "K10
 // normal-op form"): U* U = sum_s (D_s + E_s)^T H^T H (D_s + E_s) and H^T H =

@@ -184,6 +184,30 @@ cudaError_t CWW_FN(launch_normal_rows_reg_nu)(const NormArgs& a, cudaStream_t st
     }
 }
 
+// forward pass 1 fused with the top synthesis levels (warp cones of 512 samples)
+cudaError_t CWW_FN(launch_fwd1_syn_nu)(const LargeArgs& a, const PyrArgs& p, cudaStream_t st) {
+    using Gm = Geo<CWW_NU, kLogB>;
+    const int R1 = 1 << a.kl, kh = (a.j - kLogB) - a.kl;
+    const int nw = R1 * Gm::B / 512;
+    if (nw < 1 || nw > 16) return cudaErrorInvalidConfiguration;
+    const long long smem =
+        (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48 + 2ll * p.wmax + p.dsum)) * 8;
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    auto k = k_large_fwd1_syn<CWW_NU>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaError_t e = launch_k(k, dim3(1u << kh, (unsigned)a.nvec), dim3(32 * nw), (size_t)smem, st, a, p);
+        e != cudaSuccess)
+        return e;
+    return cudaGetLastError();
+}
+
+long long CWW_FN(fwd1_syn_smem_nu)(int kl, const PyrArgs& p) {
+    using Gm = Geo<CWW_NU, kLogB>;
+    const int R1 = 1 << kl, nw = R1 * Gm::B / 512;
+    if (nw < 1 || nw > 16) return -1;
+    return (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48 + 2ll * p.wmax + p.dsum)) * 8;
+}
+
 cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
     const int nt = 256;
     if (w.kind == 0) {
