@@ -82,6 +82,10 @@ typedef struct {
      * loaded instead of recomputing the table; otherwise the table is computed
      * and written back. */
     const char* cache_dir;
+    /* 1: run the kernel-table cascade (kernel.cpp:31-77) on the GPU; the
+     * table is bit-identical to the host computation (separately rounded
+     * products and sums in the host's order). */
+    int gpu_kernel_table;
 } cww_op_desc;
 
 typedef struct cww_op cww_op;

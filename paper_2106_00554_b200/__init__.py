@@ -68,7 +68,8 @@ class _Desc(C.Structure):
     _fields_ = [("family", C.c_int), ("nu", C.c_int), ("boundary", C.c_int), ("j", C.c_uint),
                 ("q", C.c_uint), ("dim", C.c_int), ("min_level", C.c_int), ("use_idwt", C.c_int),
                 ("kernel_resolution", C.c_int), ("device", C.c_int), ("data_dir", C.c_char_p),
-                ("mask", C.c_void_p), ("mask_len", C.c_size_t), ("cache_dir", C.c_char_p)]
+                ("mask", C.c_void_p), ("mask_len", C.c_size_t), ("cache_dir", C.c_char_p),
+                ("gpu_kernel_table", C.c_int)]
 
 
 _lib = None
@@ -243,13 +244,14 @@ class _Handle:
     def __init__(self, spec: WaveletSpec, j: int, q: int, dim: int, min_level: int, use_idwt: bool,
                  kernel_resolution: int = 0, device: Optional[int] = None,
                  data_dir: Optional[str] = None, mask: Optional[np.ndarray] = None,
-                 cache_dir: Optional[str] = None):
+                 cache_dir: Optional[str] = None, gpu_kernel_table: bool = False):
         L = _load()
         m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint64)
         d = _Desc(int(spec.family), spec.nu, int(spec.boundary), j, q, dim, min_level,
                   1 if use_idwt else 0, kernel_resolution, -1 if device is None else device,
                   (data_dir or DATA_DIR).encode(), None if m is None else m.ctypes.data,
-                  0 if m is None else m.size, None if cache_dir is None else cache_dir.encode())
+                  0 if m is None else m.size, None if cache_dir is None else cache_dir.encode(),
+                  1 if gpu_kernel_table else 0)
         h = C.c_void_p()
         _check(L.cww_op_create(C.byref(d), C.byref(h)))
         self.h = h
@@ -310,13 +312,14 @@ class FastOp:
 
     def __init__(self, spec: WaveletSpec, j: int, q: int, dim: int = 1, *,
                  kernel_resolution: int = 0, device: Optional[int] = None,
-                 data_dir: Optional[str] = None, cache_dir: Optional[str] = None):
+                 data_dir: Optional[str] = None, cache_dir: Optional[str] = None,
+                 gpu_kernel_table: bool = False):
         spec.validate()
         if spec.nu < 2:
             raise CwwError("FastOp requires nu >= 2; use HaarFullRankOp for Haar", 3)
         self._spec, self._j, self._q, self._dim = spec, int(j), int(q), int(dim)
         self._opts = dict(kernel_resolution=kernel_resolution, device=device, data_dir=data_dir,
-                          cache_dir=cache_dir)
+                          cache_dir=cache_dir, gpu_kernel_table=gpu_kernel_table)
         self._h = _Handle(spec, self._j, self._q, self._dim, -1, False, **self._opts)
 
     def M(self) -> int:

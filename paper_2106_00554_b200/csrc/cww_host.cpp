@@ -149,8 +149,10 @@ cww_status load_filters(int family, int nu, const char* dir_in, Filters& f) {
 }
 
 // ---------------------------------------------------------------------------
-// cascade and kernel table (host precompute, untimed)
+// cascade and kernel table (host precompute, untimed; the cascade optionally
+// on the GPU, bit-identical: cww_ktable.cu)
 // ---------------------------------------------------------------------------
+thread_local bool g_gpu_cascade = false;
 struct Samples {
     std::vector<double> v;
     long left = 0;  // support_left (integer)
@@ -187,8 +189,12 @@ std::vector<std::vector<double>> cascade_edges(const std::vector<double>& h,
                                                const std::vector<double>& B, int nu, int R) {
     const int a = -nu + 1, W = 2 * nu - 1;
     std::vector<std::vector<double>> lev(static_cast<size_t>(R) + 1);
-    lev[0] = phi;
-    for (int r = 1; r <= R; ++r) lev[size_t(r)] = refine(lev[size_t(r - 1)], r, a, nu, h, nu);
+    if (g_gpu_cascade) {
+        if (cww::cascade_gpu(h, phi, nu, R, lev) != cudaSuccess) return {};
+    } else {
+        lev[0] = phi;
+        for (int r = 1; r <= R; ++r) lev[size_t(r)] = refine(lev[size_t(r - 1)], r, a, nu, h, nu);
+    }
     std::vector<std::vector<double>> cur(static_cast<size_t>(nu));
     for (int m = 0; m < nu; ++m) {
         cur[size_t(m)].assign(size_t(nu + m + 1), 0.0);
@@ -200,6 +206,11 @@ std::vector<std::vector<double>> cascade_edges(const std::vector<double>& h,
             }
             cur[size_t(m)][size_t(k)] = acc;
         }
+    }
+    if (g_gpu_cascade) {
+        std::vector<std::vector<double>> out;
+        if (cww::cascade_edges_gpu(cur, lev, A, B, nu, R, out) != cudaSuccess) return {};
+        return out;
     }
     const double s2 = std::sqrt(2.0);
     for (int r = 1; r <= R; ++r) {
@@ -276,8 +287,15 @@ cww_status kernel_table(const Filters& f, int vmp, int q, int R, KernelTable& t)
     Samples in;
     in.R = R;
     in.left = -nu + 1;
-    in.v = f.phi;
-    for (int r = 1; r <= R; ++r) in.v = refine(in.v, r, -nu + 1, nu, f.h, nu);
+    if (g_gpu_cascade) {
+        std::vector<std::vector<double>> lev;
+        if (cww::cascade_gpu(f.h, f.phi, nu, R, lev) != cudaSuccess)
+            return fail(CWW_ERR_CUDA, "GPU kernel-table cascade failed");
+        in.v = std::move(lev[size_t(R)]);
+    } else {
+        in.v = f.phi;
+        for (int r = 1; r <= R; ++r) in.v = refine(in.v, r, -nu + 1, nu, f.h, nu);
+    }
     for (int l = -nu + 1; l <= nu - 1; ++l) {
         auto m = cell_masses(in, l, q);
         fwht_seq_host(m);
@@ -289,6 +307,8 @@ cww_status kernel_table(const Filters& f, int vmp, int q, int R, KernelTable& t)
     auto L = cascade_edges(f.h, f.phi, f.E[0], f.A[0], f.B[0], nu, R);
     std::vector<double> hr(f.h.rbegin(), f.h.rend()), pr(f.phi.rbegin(), f.phi.rend());
     auto Rt = cascade_edges(hr, pr, f.E[1], f.A[1], f.B[1], nu, R);
+    if (L.size() != size_t(nu) || Rt.size() != size_t(nu))
+        return fail(CWW_ERR_CUDA, "GPU kernel-table edge cascade failed");
     for (int m = 0; m < nu; ++m) {
         Samples sl;
         sl.R = R;
@@ -1171,6 +1191,7 @@ void cww_op_desc_init(cww_op_desc* d) {
     d->mask = nullptr;
     d->mask_len = 0;
     d->cache_dir = nullptr;
+    d->gpu_kernel_table = 0;
 }
 
 cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
@@ -1211,9 +1232,11 @@ cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
     CUDA_TRY(cudaSetDevice(op->device));
     if ((s = load_filters(desc->family, desc->nu, op->data_dir.c_str(), op->f)) != CWW_OK) return s;
     int R = desc->kernel_resolution > 0 ? desc->kernel_resolution : 14;
-    if ((s = cached_kernel_table(op->f, desc->family, desc->boundary, int(desc->q), R,
-                                 cache_dir_of(desc->cache_dir), op->kt)) != CWW_OK)
-        return s;
+    g_gpu_cascade = desc->gpu_kernel_table != 0;
+    s = cached_kernel_table(op->f, desc->family, desc->boundary, int(desc->q), R, cache_dir_of(desc->cache_dir),
+                            op->kt);
+    g_gpu_cascade = false;
+    if (s != CWW_OK) return s;
     build_edge_terms(*op);
     if ((s = build_tables(*op)) != CWW_OK) return s;
     op->full_out = op->dim == 2 ? op->N * op->N : op->N;

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <utility>
+#include <vector>
 
 #include "cww_device.cuh"
 
@@ -211,6 +212,13 @@ cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st);
 cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, double* scratch,
                         cudaStream_t st);
 cudaError_t launch_seq_perm(uint32_t* perm, int bits, cudaStream_t st);
+// GPU kernel-table cascades (cww_ktable.cu): interior levels 0..R of phi, and
+// the nu boundary functions from their start values cur0.
+cudaError_t cascade_gpu(const std::vector<double>& h, const std::vector<double>& phi, int nu, int R,
+                        std::vector<std::vector<double>>& lev);
+cudaError_t cascade_edges_gpu(const std::vector<std::vector<double>>& cur0,
+                              const std::vector<std::vector<double>>& lev, const std::vector<double>& A,
+                              const std::vector<double>& B, int nu, int R, std::vector<std::vector<double>>& out);
 // CGLS vector algebra (cww_solver.cu)
 int dot_nblk(long long n, long long batch);
 cudaError_t launch_dot(const double* a, const double* b, long long n, long long batch, double* part,

@@ -371,3 +371,18 @@ def test_op_uses_kernel_cache(orc, cuda, tmp_path):
     it2 = cw.FastOp(spec, 6, 2, cache_dir=str(tmp_path)).kernel_table()[0]
     assert np.array_equal(it2, it0)
     assert path.read_bytes() == open(gold, "rb").read()
+
+
+@pytest.mark.parametrize("fam,nu,bnd,q", [(0, 2, 1, 1), (0, 4, 1, 2), (1, 3, 0, 3), (0, 6, 1, 2), (1, 5, 1, 1),
+                                          (0, 3, 0, 2)])
+def test_gpu_kernel_table_bit_identical(orc, cuda, fam, nu, bnd, q):
+    """f4: the kernel-table cascade on the GPU (separately rounded products and
+    sums in the host's order) gives the same bits as the host / reference."""
+    cw = _cw()
+    spec = cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd))
+    host_t = cw.FastOp(spec, 6, q).kernel_table()
+    gpu_t = cw.FastOp(spec, 6, q, gpu_kernel_table=True).kernel_table()
+    for a, b in zip(host_t, gpu_t):
+        assert np.array_equal(a, b)
+    it, le, ri = orc.kernel_table(fam, nu, bnd, q)
+    assert np.array_equal(gpu_t[0], it)
