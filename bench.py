@@ -323,7 +323,23 @@ def main():
             op.forward(x_dev, fo_dev)
             op.adjoint(y_dev, ao_dev)
 
+    s_fwd, s_adj = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
     def step_e2e():
+        if not (rowpart or is5) and x_pin.numel() * 8 > (1 << 20):
+            # the public host API on pinned buffers (cww_*_host_async): chunk-pipelined H2D /
+            # compute / D2H; forward and adjoint are independent, so they run on two streams
+            # and the two PCIe directions overlap.  (Tiny inputs -- config 1 -- keep the
+            # single-stream copies below: measured 44k vs 36k matvec/s.)
+            s_fwd.wait_stream(stream)
+            s_adj.wait_stream(stream)
+            with torch.cuda.stream(s_fwd):
+                op.forward(x_pin, fo_pin)
+            with torch.cuda.stream(s_adj):
+                op.adjoint(y_pin, ao_pin)
+            stream.wait_stream(s_fwd)
+            stream.wait_stream(s_adj)
+            return
         x_dev.copy_(x_pin, non_blocking=True)
         if rowpart:
             xr = d2.normal(x_dev.view(1 << j, 1 << j)[rank * mr:(rank + 1) * mr], CFG5_ITERS)

@@ -142,6 +142,17 @@ cww_status cww_forward_host(const cww_op* op, const double* x, size_t x_len, dou
 cww_status cww_adjoint_host(const cww_op* op, const double* y, size_t y_len, double* x,
                             size_t x_len, size_t batch);
 
+/* Asynchronous host-pointer entry points for PINNED host buffers (cudaHostAlloc
+ * / cudaHostRegister; pageable buffers take the synchronous path): the batch
+ * is split into chunks whose host-to-device copy, compute and device-to-host
+ * copy run on three streams, so copies in both PCIe directions overlap the
+ * compute and each other.  Enqueued behind `stream`, which is made to wait
+ * for the last copy; returns without synchronising. */
+cww_status cww_forward_host_async(const cww_op* op, const double* x, size_t x_len, double* y,
+                                  size_t y_len, size_t batch, void* stream);
+cww_status cww_adjoint_host_async(const cww_op* op, const double* y, size_t y_len, double* x,
+                                  size_t x_len, size_t batch, void* stream);
+
 /* Multilevel DWT (dir = CWW_DWT_FORWARD, analysis) or IDWT (CWW_DWT_INVERSE)
  * of `batch` device vectors (dim 1: 2^j, dim 2: 2^j x 2^j row-major), in
  * place, using the op's filters, boundary and min_level (dwt_apply,

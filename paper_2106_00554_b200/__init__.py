@@ -97,6 +97,8 @@ def _load():
     for name in ("cww_forward_host", "cww_adjoint_host"):
         getattr(L, name).argtypes = [vp, dp, sz, dp, sz, sz]
     L.cww_normal.argtypes = [vp, dp, sz, dp, sz, sz, C.c_int, vp]
+    L.cww_forward_host_async.argtypes = [vp, dp, sz, dp, sz, sz, vp]
+    L.cww_adjoint_host_async.argtypes = [vp, dp, sz, dp, sz, sz, vp]
     L.cww_gs_solve.argtypes = [vp, dp, sz, dp, sz, sz, C.c_double, C.c_int, C.c_int,
                                C.POINTER(C.c_int), dp, vp]
     L.cww_dwt.argtypes = [vp, dp, sz, sz, C.c_int, vp]
@@ -271,6 +273,18 @@ class _Handle:
         nin, nout = (self.nout, self.nin) if adjoint else (self.nin, self.nout)
         if _is_tensor(inp):
             torch = _torch()
+            if (not inp.is_cuda and inp.is_pinned() and _is_tensor(out) and not out.is_cuda and out.is_pinned()
+                    and inp.dtype == torch.float64 and out.dtype == torch.float64 and inp.is_contiguous()
+                    and out.is_contiguous()):
+                # pinned host tensors: chunk-pipelined copies / compute, asynchronous on the
+                # current CUDA stream (cww_*_host_async); synchronise before reading `out`
+                if inp.numel() % nin or out.numel() != (inp.numel() // nin) * nout:
+                    raise CwwError(("adjoint" if adjoint else "forward") + ": dimension mismatch", 2)
+                batch = inp.numel() // nin
+                fn = self.L.cww_adjoint_host_async if adjoint else self.L.cww_forward_host_async
+                _check(fn(self.h, inp.data_ptr(), inp.numel(), out.data_ptr(), out.numel(), batch,
+                          torch.cuda.current_stream().cuda_stream))
+                return out
             if not inp.is_cuda:
                 inp = inp.detach().numpy()
             else:

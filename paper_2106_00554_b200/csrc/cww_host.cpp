@@ -1778,6 +1778,90 @@ cww_status cww_kernel_table_load(const char* path, int* header, double* interior
     return CWW_OK;
 }
 
+// Chunk-pipelined host staging for pinned buffers: H2D (side stream), compute
+// (caller stream), D2H (second side stream), one event per chunk and stage.
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+struct SideStreams {  // per host thread and device: created once
+    cudaStream_t in = nullptr, out = nullptr;
+    int device = -1;
+};
+
+static cww_status host_call_async(const cww_op* op, const double* in, size_t in_len, double* out,
+                                  size_t out_len, size_t batch, bool adj, cudaStream_t st) {
+    cww_status s = check_lens(op, in_len, out_len, batch, adj, adj ? "adjoint" : "forward");
+    if (s != CWW_OK) return s;
+    if (batch == 0) return CWW_OK;
+    if (!in || !out) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (!is_pinned(in) || !is_pinned(out)) return host_call(op, in, in_len, out, out_len, batch, adj);
+    CUDA_TRY(cudaSetDevice(op->device));
+    if ((in_len + out_len) * sizeof(double) <= (size_t(2) << 20)) {  // small: one stream, no pipeline
+        double *din = nullptr, *dout = nullptr;
+        CUDA_TRY(cudaMallocAsync(&din, in_len * sizeof(double), st));
+        CUDA_TRY(cudaMallocAsync(&dout, out_len * sizeof(double), st));
+        CUDA_TRY(cudaMemcpyAsync(din, in, in_len * sizeof(double), cudaMemcpyHostToDevice, st));
+        if ((s = run(op, din, dout, (long long)batch, adj, st)) != CWW_OK) return s;
+        CUDA_TRY(cudaMemcpyAsync(out, dout, out_len * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(din, st));
+        CUDA_TRY(cudaFreeAsync(dout, st));
+        return CWW_OK;
+    }
+    thread_local SideStreams ss;
+    if (ss.device != op->device) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ss.in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ss.out, cudaStreamNonBlocking));
+        ss.device = op->device;
+    }
+    const size_t ni = in_len / batch, no = out_len / batch;
+    const size_t target = size_t(8) << 20;  // ~8 MB of input+output per chunk
+    size_t cb = std::max<size_t>(1, target / ((ni + no) * sizeof(double)));
+    cb = std::min(cb, batch);
+    const size_t nch = (batch + cb - 1) / cb;
+    double *din = nullptr, *dout = nullptr;
+    CUDA_TRY(cudaMallocAsync(&din, in_len * sizeof(double), st));
+    CUDA_TRY(cudaMallocAsync(&dout, out_len * sizeof(double), st));
+    std::vector<cudaEvent_t> ev(2 * nch + 2, nullptr);
+    for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t e_start = ev[2 * nch], e_done = ev[2 * nch + 1];
+    CUDA_TRY(cudaEventRecord(e_start, st));  // buffers allocated, caller's prior work ordered
+    CUDA_TRY(cudaStreamWaitEvent(ss.in, e_start, 0));
+    for (size_t k = 0; k < nch; ++k) {
+        const size_t b0 = k * cb, nb = std::min(cb, batch - b0);
+        CUDA_TRY(cudaMemcpyAsync(din + b0 * ni, in + b0 * ni, nb * ni * sizeof(double), cudaMemcpyHostToDevice,
+                                 ss.in));
+        CUDA_TRY(cudaEventRecord(ev[2 * k], ss.in));
+        CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * k], 0));
+        if ((s = run(op, din + b0 * ni, dout + b0 * no, (long long)nb, adj, st)) != CWW_OK) return s;
+        CUDA_TRY(cudaEventRecord(ev[2 * k + 1], st));
+        CUDA_TRY(cudaStreamWaitEvent(ss.out, ev[2 * k + 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(out + b0 * no, dout + b0 * no, nb * no * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ss.out));
+    }
+    CUDA_TRY(cudaEventRecord(e_done, ss.out));
+    CUDA_TRY(cudaStreamWaitEvent(st, e_done, 0));  // the caller's stream sees the results
+    CUDA_TRY(cudaFreeAsync(din, st));
+    CUDA_TRY(cudaFreeAsync(dout, st));
+    for (auto& e : ev) cudaEventDestroy(e);  // destruction is deferred until the events complete
+    return CWW_OK;
+}
+
+cww_status cww_forward_host_async(const cww_op* op, const double* x, size_t x_len, double* y, size_t y_len,
+                                  size_t batch, void* stream) {
+    return host_call_async(op, x, x_len, y, y_len, batch, false, S_(stream));
+}
+
+cww_status cww_adjoint_host_async(const cww_op* op, const double* y, size_t y_len, double* x, size_t x_len,
+                                  size_t batch, void* stream) {
+    return host_call_async(op, y, y_len, x, x_len, batch, true, S_(stream));
+}
+
 cww_status cww_forward_host(const cww_op* op, const double* x, size_t x_len, double* y,
                             size_t y_len, size_t batch) {
     return host_call(op, x, x_len, y, y_len, batch, false);

@@ -386,3 +386,27 @@ def test_gpu_kernel_table_bit_identical(orc, cuda, fam, nu, bnd, q):
         assert np.array_equal(a, b)
     it, le, ri = orc.kernel_table(fam, nu, bnd, q)
     assert np.array_equal(gpu_t[0], it)
+
+
+def test_pinned_host_async_path(orc, cuda):
+    """cww_*_host_async on pinned host tensors (chunk-pipelined copies) gives
+    the same results as the device path, on two concurrent streams."""
+    import torch
+    cw = _cw()
+    spec = cw.WaveletSpec(cw.Family.Daubechies, 4, cw.Boundary.Vmp)
+    for j in (9, 14):
+        op = cw.ComposedOp(cw.FastOp(spec, j, 2), None, True, 4)
+        B = 37
+        x = torch.randn((B, op.cols()), dtype=torch.float64).pin_memory()
+        y = torch.randn((B, op.rows()), dtype=torch.float64).pin_memory()
+        fo = torch.empty((B, op.rows()), dtype=torch.float64).pin_memory()
+        ao = torch.empty((B, op.cols()), dtype=torch.float64).pin_memory()
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        with torch.cuda.stream(s1):
+            op.forward(x, fo)
+        with torch.cuda.stream(s2):
+            op.adjoint(y, ao)
+        torch.cuda.synchronize()
+        fd = op.forward(x.cuda()).cpu()
+        ad = op.adjoint(y.cuda()).cpu()
+        assert torch.equal(fo, fd) and torch.equal(ao, ad)
