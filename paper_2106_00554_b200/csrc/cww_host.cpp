@@ -1820,7 +1820,7 @@ static cww_status host_call_async(const cww_op* op, const double* in, size_t in_
         ss.device = op->device;
     }
     const size_t ni = in_len / batch, no = out_len / batch;
-    const size_t target = size_t(8) << 20;  // ~8 MB of input+output per chunk
+    static const size_t target = size_t(env_int("CWW_HOST_CHUNK_MB", 64)) << 20;  // input+output per chunk (tuned: 8-256 MB)
     size_t cb = std::max<size_t>(1, target / ((ni + no) * sizeof(double)));
     cb = std::min(cb, batch);
     const size_t nch = (batch + cb - 1) / cb;
