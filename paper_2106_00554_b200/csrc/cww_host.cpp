@@ -900,6 +900,8 @@ LargePlan large_plan(unsigned j) {
     int a = int(j) - cww::kLogB;
     int kl = (a + 1) / 2;
     if (kl > 8) kl = 8;
+    static const int kl_env = env_int("CWW_LARGE_KL", 0);  // tuning: low K bits of the contiguous pass
+    if (kl_env > 0 && kl_env < a) kl = kl_env;
     int kh = a - kl;
     int ng = 1;
     while (ng * (1 << kh) < 128 && ng * 2 <= (1 << kl)) ng *= 2;
