@@ -313,12 +313,26 @@ def main():
         mr = M_ // world
         x_rows0 = x_dev.view(M_, M_)[rank * mr:(rank + 1) * mr].contiguous()
 
-    def step_device():
+    conc = os.environ.get("CWW_BENCH_CONCURRENT", "0") == "1"  # measured: no gain (cfg2 0.273 vs 0.269 ms)
+    s_dev_f, s_dev_a = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def step_device(concurrent=conc):
         if rowpart:
             d2.normal(x_rows0, CFG5_ITERS)
         elif is5:
             ao_dev.copy_(x_dev)
             op.normal(ao_dev, iters=CFG5_ITERS, work=fo_dev)
+        elif concurrent:
+            # forward and adjoint of the batch are independent: two streams, so one
+            # chain's latency-bound phases and launch tails overlap the other's
+            s_dev_f.wait_stream(stream)
+            s_dev_a.wait_stream(stream)
+            with torch.cuda.stream(s_dev_f):
+                op.forward(x_dev, fo_dev)
+            with torch.cuda.stream(s_dev_a):
+                op.adjoint(y_dev, ao_dev)
+            stream.wait_stream(s_dev_f)
+            stream.wait_stream(s_dev_a)
         else:
             op.forward(x_dev, fo_dev)
             op.adjoint(y_dev, ao_dev)
@@ -390,7 +404,7 @@ def main():
         # per-kernel breakdown: the same steps again with CUDA events around every launch
         cw.profile_enable(True)
         cw.profile_dump()
-        ms_prof = timed(step_device, args.steps)
+        ms_prof = timed(lambda: step_device(False), args.steps)  # sequential: clean per-kernel events
         cw.profile_enable(False)
         prof = cw.profile_dump()
         t_end = time.time() + 1.0  # keep the same load running so nvidia-smi sees it
