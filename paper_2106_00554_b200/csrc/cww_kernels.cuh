@@ -596,7 +596,8 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
             row_load<LOGB>(ib0 + p.lin.eoff((long long)s * M), p.lin, a, rw, act, y);
             hadamard_reg<LOGB>(y);
             if (NU > 1) {  // transform-domain values at the 4nu-2 edge positions
-                const int slot = ((it * NT + (tid & ~31)) / (vf ? V : 1) / L) % nslot;
+                // V, L and nslot are powers of two: ((it*NT + warp base) / (vf ? V : 1) / L) % nslot
+                const int slot = ((it * NT + (tid & ~31)) >> ((vf ? lV : 0) + ilog2(L))) & (nslot - 1);
                 constexpr int R = 2 * NP <= 16 ? 16 : 32;
                 double ev[R];
 #pragma unroll
@@ -699,10 +700,20 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
     PHASE(4);
     const double* res = dwt ? T : X;
     const int rst = dwt ? tst : M;
-    for (int f = tid; f < V * M; f += NT) {
-        const int v = of ? f & (V - 1) : f >> j;
-        const int i = of ? f >> lV : f & (M - 1);
-        if (v < nv) p.out[p.lout.at(v0 + v, i)] = res[v * rst + i];
+    if (p.lout.vsh >= 62 && p.lout.esh >= 62) {  // plain strides: no tiling arithmetic per element
+        const long long vs = p.lout.vs, es = p.lout.es;
+        double* o0 = p.out + (v0 * vs);
+        for (int f = tid; f < V * M; f += NT) {
+            const int v = of ? f & (V - 1) : f >> j;
+            const int i = of ? f >> lV : f & (M - 1);
+            if (v < nv) o0[v * vs + i * es] = res[v * rst + i];
+        }
+    } else {
+        for (int f = tid; f < V * M; f += NT) {
+            const int v = of ? f & (V - 1) : f >> j;
+            const int i = of ? f >> lV : f & (M - 1);
+            if (v < nv) p.out[p.lout.at(v0 + v, i)] = res[v * rst + i];
+        }
     }
     __syncthreads();
     PHASE(5);
