@@ -119,6 +119,17 @@ public:
     void adjoint_device(const double* y, double* x, std::size_t batch, void* stream) const {
         check(cww_adjoint(h_.get(), y, batch * out_, x, batch * in_, batch, stream));
     }
+    // pinned host buffers: chunk-pipelined H2D / compute / D2H behind `stream` (no sync)
+    void forward_host_async(const double* x, double* y, std::size_t batch, void* stream) const {
+        check(cww_forward_host_async(h_.get(), x, batch * in_, y, batch * out_, batch, stream));
+    }
+    void adjoint_host_async(const double* y, double* x, std::size_t batch, void* stream) const {
+        check(cww_adjoint_host_async(h_.get(), y, batch * out_, x, batch * in_, batch, stream));
+    }
+    // x <- (A* A)^iters x on device memory (banded normal form for full masks)
+    void normal_device(double* x, std::size_t batch, int iters, void* stream) const {
+        check(cww_normal(h_.get(), x, batch * in_, nullptr, 0, batch, iters, stream));
+    }
     const cww_op* handle() const { return h_.get(); }
 
 private:
