@@ -881,6 +881,9 @@ const int kWpyrAnaLevels = env_int("CWW_WPYR_ANA_LEVELS", 3);  // analysis steps
 // B200 the fused kernel is no faster (cfg2 68 us vs 42 + 27 us; cfg3 slower) --
 // both halves are latency-bound, so the saved xi round trip does not show.
 const bool kFuseFwd1 = env_int("CWW_FUSE_FWD1", 0) != 0;
+// coarse synthesis levels r0+1..kPyrSynBot once per CTA inside the first warp pyramid
+// (instead of the one-CTA-per-vector k_wav_coarse launch)
+const bool kCtaCoarse = env_int("CWW_CTA_COARSE", 0) != 0;  // off: cfg2 idwt 66.9 vs 46.9 + 12.7 us
 
 cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     cww::PyrArgs y{};
@@ -889,6 +892,7 @@ cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     y.nvec = nvec;
     y.vmp = op->vmp;
     y.r0 = op->r0;
+    y.cbot = -1;  // no CTA coarse stage
     return y;
 }
 
@@ -961,7 +965,8 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
             int bot = std::max(op->r0, std::min(kPyrSynBot, j - 1));
             const double* src = nullptr;  // level-bot coarse vector (nullptr: the op input)
             long long src_vs = 0;
-            if (bot > op->r0) {
+            const bool cta_coarse = bot > op->r0 && kCtaCoarse;  // coarse levels inside the first pyramid
+            if (bot > op->r0 && !cta_coarse) {
                 cww::WavArgs w{};
                 w.tab = op->d_tab;
                 w.t = op->tabs;
@@ -1017,6 +1022,13 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
                 y.src_is_x = src ? 0 : 1;
                 y.src = src;
                 y.src_vs = src_vs;
+                if (cta_coarse && src == nullptr) {  // first pyramid: levels r0+1..bot per CTA
+                    const int nchunk = 1 << (top - y.cb), nw = nchunk < 8 ? nchunk : 8;
+                    int lnw = 0;
+                    while ((1 << lnw) < nw) ++lnw;
+                    y.cbot = op->r0;
+                    y.cwmax = cww::pyr_wmax_cta(nu, top, bot, op->r0, y.cb + lnw, op->vmp != 0, &y.cdsum);
+                }
                 ob = (src == w0.p) ? 1 : 0;  // never overwrite the level being read
                 y.out = bufs[ob];
                 y.out_vs = M;

@@ -923,7 +923,8 @@ __device__ __forceinline__ void warp_syn_windows(const PyrArgs& p, double* wb, i
 // level p.top and hand the top samples to put(i, value).
 template <int NU, class Put>
 __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU>& F, const Taps<NU>& tp,
-                                             double* wb, int v, int lane, bool vmp, Put&& put) {
+                                             double* wb, int v, int lane, bool vmp, Put&& put,
+                                             const double* cb_smem = nullptr, int cb_lo = 0) {
     const int* wlo = reinterpret_cast<const int*>(wb);
     const int* whi = wlo + 32;
     const int* doff = wlo + 64;
@@ -934,7 +935,11 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
     const double* cs = p.src_is_x ? xb : p.src + v * p.src_vs;
     {
         const int lo = wlo[p.bot], w = whi[p.bot] - lo, hb = 1 << p.bot;
-        for (int t = lane; t < w; t += 32) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
+        if (cb_smem) {  // the CTA stage's level-bot window (logical indices from cb_lo)
+            for (int t = lane; t < w; t += 32) P[t] = cb_smem[lo + t - cb_lo];
+        } else {
+            for (int t = lane; t < w; t += 32) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
+        }
     }
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {  // details of level lev (half = 2^(lev-1))
         const int lo = wlo[lev - 1], w = whi[lev - 1] - lo, hf = 1 << (lev - 1);
@@ -973,15 +978,71 @@ __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
     extern __shared__ double sm[];
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5, nt = blockDim.x;
     double* wb = sm + FS + wid * (48 + 2 * p.wmax + p.dsum);
     const int c = blockIdx.x * nw + wid, v = blockIdx.y;
     const bool vmp = p.vmp != 0;
-    for (int i = tid; i < FS; i += blockDim.x) filt[i] = p.tab[p.t.o_h + i];
+    const bool cta_stage = p.cbot >= 0 && p.cbot < p.bot;
+    // CTA stage scratch after the warps' areas: ints (48) | P | Q (cwmax) | D (cdsum)
+    double* cw = sm + FS + nw * (48 + 2 * p.wmax + p.dsum);
+    int* clo = reinterpret_cast<int*>(cw);
+    int* chi = clo + 32;
+    int* cdoff = clo + 64;
+    double* CP = cw + 48;
+    double* CQ = CP + p.cwmax;
+    double* CD = CQ + p.cwmax;
+    for (int i = tid; i < FS; i += nt) filt[i] = p.tab[p.t.o_h + i];
     if (lane == 0) warp_syn_windows<NU>(p, wb, c << p.cb, (c + 1) << p.cb, vmp);
-    __syncthreads();  // filters (CTA-wide) and this warp's windows
+    if (cta_stage && tid == (nw > 1 ? 32 : 0)) {  // the CTA's cone: top range of its warps, down to cbot
+        Win f{(blockIdx.x * nw) << p.cb, (blockIdx.x * nw + nw) << p.cb};
+        for (int lev = p.top; lev > p.bot; --lev) f = syn_need(NU, 1 << lev, f, vmp);
+        for (int lev = p.bot; lev >= p.cbot; --lev) {
+            clo[lev] = f.lo;
+            chi[lev] = f.hi;
+            if (lev > p.cbot) {
+                f = syn_need(NU, 1 << lev, f, vmp);
+                if (f.hi - f.lo > p.cwmax) __trap();
+            }
+        }
+        int off = 0;
+        for (int lev = p.cbot + 1; lev <= p.bot; ++lev) {
+            cdoff[lev] = off;
+            off += chi[lev - 1] - clo[lev - 1];
+        }
+        if (off > p.cdsum) __trap();
+    }
+    __syncthreads();  // filters (CTA-wide) and the windows
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
+    const double* xb = p.x + p.lx.vbase(p.xv0 + v);
+    if (cta_stage) {  // coarse levels cbot+1..bot once per CTA (shared by its warps' cones)
+        {
+            const int lo = clo[p.cbot], w = chi[p.cbot] - lo, hb = 1 << p.cbot;
+            for (int t = tid; t < w; t += nt) cp_async8(CP + t, xb + (vmp ? lo + t : ((lo + t) & (hb - 1))));
+        }
+        for (int lev = p.cbot + 1; lev <= p.bot; ++lev) {
+            const int lo = clo[lev - 1], w = chi[lev - 1] - lo, hf = 1 << (lev - 1);
+            for (int t = tid; t < w; t += nt)
+                cp_async8(CD + cdoff[lev] + t, xb + hf + (vmp ? lo + t : ((lo + t) & (hf - 1))));
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        double* P = CP;
+        double* Q = CQ;
+        for (int lev = p.cbot + 1; lev <= p.bot; ++lev) {
+            const int n = 1 << lev, lo = clo[lev], hi = chi[lev];
+            double* q = Q - lo;
+            idwt_window<NU>(F, tp, P, CD + cdoff[lev], clo[lev - 1], n, lo, hi, vmp, tid, nt,
+                            [&](int i, double val) { q[i] = val; });
+            __syncthreads();
+            double* t0 = P;
+            P = Q;
+            Q = t0;
+        }
+        double* ob = p.out + v * p.out_vs;
+        warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) { ob[i] = val; }, P, clo[p.bot]);
+        return;
+    }
     double* ob = p.out + v * p.out_vs;
     warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) { ob[i] = val; });
 }

@@ -123,6 +123,10 @@ struct PyrArgs {
     int vmp, top, bot, cb, r0, tail;
     int wmax;  // window buffer length (doubles), from pyr_wmax_*
     int dsum;  // synthesis: total detail-window length over all levels
+    // synthesis only: levels cbot+1..bot run once per CTA (its cone over the CTA's
+    // top range) before the warp cones start at level bot; cbot < 0 disables.
+    // cwmax / cdsum: the CTA stage's window and detail-window sizes.
+    int cbot, cwmax, cdsum;
     const double* x;
     Layout lx;
     long long xv0;
@@ -179,6 +183,26 @@ inline int pyr_wmax_syn(int nu, int top, int bot, int cb, bool vmp, int* dsum) {
         Win f{int(c << cb), int((c + 1) << cb)};
         int sum = 0;
         for (int lev = top; lev > bot; --lev) {
+            f = syn_need(nu, 1 << lev, f, vmp);
+            if (f.hi - f.lo > wm) wm = f.hi - f.lo;
+            sum += f.hi - f.lo;
+        }
+        if (sum > ds) ds = sum;
+    }
+    *dsum = ds;
+    return wm;
+}
+
+// CTA coarse stage of a synthesis pyramid: windows of levels cbot..bot for the
+// cone of top-level chunks of 2^ccb samples (ccb = cb + log2(warps per CTA)).
+inline int pyr_wmax_cta(int nu, int top, int bot, int cbot, int ccb, bool vmp, int* dsum) {
+    int wm = 1, ds = 1;
+    for (long long c = 0; c < (1ll << (top - ccb)); ++c) {
+        Win f{int(c << ccb), int((c + 1) << ccb)};
+        for (int lev = top; lev > bot; --lev) f = syn_need(nu, 1 << lev, f, vmp);
+        if (f.hi - f.lo > wm) wm = f.hi - f.lo;
+        int sum = 0;
+        for (int lev = bot; lev > cbot; --lev) {
             f = syn_need(nu, 1 << lev, f, vmp);
             if (f.hi - f.lo > wm) wm = f.hi - f.lo;
             sum += f.hi - f.lo;

@@ -118,7 +118,8 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     } else {
-        const long long smem = (FS + (long long)nw * (48 + 2ll * a.wmax + a.dsum)) * 8;
+        long long smem = (FS + (long long)nw * (48 + 2ll * a.wmax + a.dsum)) * 8;
+        if (a.cbot >= 0 && a.cbot < a.bot) smem += (48 + 2ll * a.cwmax + a.cdsum) * 8;  // CTA coarse stage
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_idwt_wpyr<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
