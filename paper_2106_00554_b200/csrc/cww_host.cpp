@@ -999,6 +999,7 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
                     y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum);
                     const int lev = j - bot, hh = nu - 1;  // halo-extended edge cones: margin
                     y.wmax += hh + 4;
+                    y.wmax2 = y.wmax;
                     y.dsum += lev * (hh + 4);
                     y.x = in;
                     y.lx = lin;
@@ -1016,7 +1017,7 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
                 y.top = top;
                 y.bot = bot;
                 y.cb = std::min(top, kWpyrLog);
-                y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum);
+                y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum, &y.wmax2);
                 y.x = in;
                 y.lx = lin;
                 y.src_is_x = src ? 0 : 1;
@@ -1095,7 +1096,7 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
         y.bot = bot;
         y.cb = cb;
         y.tail = tail ? 1 : 0;
-        y.wmax = cww::pyr_wmax_ana(nu, T, bot, cb, op->vmp != 0);
+        y.wmax = cww::pyr_wmax_ana(nu, T, bot, cb, op->vmp != 0, &y.wmax2);
         y.src = src;
         y.src_vs = M;
         y.y = out;

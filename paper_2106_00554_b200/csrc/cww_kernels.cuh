@@ -907,7 +907,7 @@ __device__ __forceinline__ void warp_syn_windows(const PyrArgs& p, double* wb, i
         whi[lev] = f.hi;
         if (lev > p.bot) {
             f = syn_need(NU, 1 << lev, f, vmp);
-            if (f.hi - f.lo > p.wmax) __trap();
+            if (f.hi - f.lo > (((p.top - lev) & 1) ? p.wmax2 : p.wmax)) __trap();  // slot size
         }
     }
     int off = 0;
@@ -928,9 +928,12 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
     const int* wlo = reinterpret_cast<const int*>(wb);
     const int* whi = wlo + 32;
     const int* doff = wlo + 64;
+    // level lev's window sits in buffer (lev - bot) & 1; the host sized slot 0 (wmax)
+    // for the level top-1 window and slot 1 (wmax2) for the other parity
+    const bool swap01 = ((p.top - 1 - p.bot) & 1) != 0;
     double* P = wb + 48;
-    double* Q = P + p.wmax;
-    double* D = Q + p.wmax;
+    double* Q = P + (swap01 ? p.wmax2 : p.wmax);
+    double* D = P + p.wmax + p.wmax2;
     const double* xb = p.x + p.lx.vbase(p.xv0 + v);
     const double* cs = p.src_is_x ? xb : p.src + v * p.src_vs;
     {
@@ -979,12 +982,12 @@ __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5, nt = blockDim.x;
-    double* wb = sm + FS + wid * (48 + 2 * p.wmax + p.dsum);
+    double* wb = sm + FS + wid * (48 + p.wmax + p.wmax2 + p.dsum);
     const int c = blockIdx.x * nw + wid, v = blockIdx.y;
     const bool vmp = p.vmp != 0;
     const bool cta_stage = p.cbot >= 0 && p.cbot < p.bot;
     // CTA stage scratch after the warps' areas: ints (48) | P | Q (cwmax) | D (cdsum)
-    double* cw = sm + FS + nw * (48 + 2 * p.wmax + p.dsum);
+    double* cw = sm + FS + nw * (48 + p.wmax + p.wmax2 + p.dsum);
     int* clo = reinterpret_cast<int*>(cw);
     int* chi = clo + 32;
     int* cdoff = clo + 64;
@@ -1096,7 +1099,7 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    const int per = 64 + 2 * p.wmax;
+    const int per = 64 + p.wmax + p.wmax2;  // slot 0: windows of steps top, top-2, ...; slot 1: the others
     double* wb = sm + FS + wid * per;
     int* rlo = reinterpret_cast<int*>(wb);
     int* rhi = rlo + 32;
@@ -1116,7 +1119,7 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
             rhi[s] = r.hi;
             xlo[s] = w.lo;
             xhi[s] = w.hi;
-            if (w.hi - w.lo > p.wmax) __trap();
+            if (w.hi - w.lo > (((p.top - s) & 1) ? p.wmax2 : p.wmax)) __trap();  // slot size
             r = w;
         }
     }
@@ -1687,7 +1690,7 @@ __global__ void __launch_bounds__(512, 1) k_large_fwd1_syn(LargeArgs a, PyrArgs 
     const bool vmp = p.vmp != 0;
     double* filt = sm;
     double* T = sm + FS;
-    double* wb = T + R1 * RS + wid * (48 + 2 * p.wmax + p.dsum);
+    double* wb = T + R1 * RS + wid * (48 + p.wmax + p.wmax2 + p.dsum);
     const int base = chunk * R1 * B, span = (R1 * B) / nw;
     for (int i = tid; i < FS; i += nt) filt[i] = p.tab[p.t.o_h + i];
     if (lane == 0) {

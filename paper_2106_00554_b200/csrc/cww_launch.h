@@ -121,7 +121,8 @@ struct PyrArgs {
     Tables t;
     long long nvec;
     int vmp, top, bot, cb, r0, tail;
-    int wmax;  // window buffer length (doubles), from pyr_wmax_*
+    int wmax;  // window buffer length (doubles), from pyr_wmax_*: the larger ping-pong slot
+    int wmax2; // the other ping-pong slot (levels alternate: about half of wmax)
     int dsum;  // synthesis: total detail-window length over all levels
     // synthesis only: levels cbot+1..bot run once per CTA (its cone over the CTA's
     // top range) before the warp cones start at level bot; cbot < 0 disables.
@@ -176,21 +177,28 @@ cudaError_t launch_transpose(const double* in, double* out, long long n, long lo
 
 // Largest window (over all CTAs and levels) of a synthesis pyramid producing
 // chunks of 2^cb samples of level top from level bot.
-// Also returns the largest total detail-window length of one CTA (dsum).
-inline int pyr_wmax_syn(int nu, int top, int bot, int cb, bool vmp, int* dsum) {
-    int wm = 1, ds = 1;
+// Also returns the largest total detail-window length of one CTA (dsum) and,
+// in *wm2, the largest window of the other ping-pong slot: level lev's window
+// lives in slot (top-1-lev) & 1 (slot 0 = the level top-1 window, the largest).
+inline int pyr_wmax_syn(int nu, int top, int bot, int cb, bool vmp, int* dsum, int* wm2 = nullptr) {
+    int wm[2] = {1, 1}, ds = 1;
     for (long long c = 0; c < (1ll << (top - cb)); ++c) {
         Win f{int(c << cb), int((c + 1) << cb)};
         int sum = 0;
         for (int lev = top; lev > bot; --lev) {
-            f = syn_need(nu, 1 << lev, f, vmp);
-            if (f.hi - f.lo > wm) wm = f.hi - f.lo;
+            f = syn_need(nu, 1 << lev, f, vmp);  // window of level lev-1
+            const int slot = (top - lev) & 1;
+            if (f.hi - f.lo > wm[slot]) wm[slot] = f.hi - f.lo;
             sum += f.hi - f.lo;
         }
         if (sum > ds) ds = sum;
     }
     *dsum = ds;
-    return wm;
+    if (wm2) {
+        *wm2 = wm[1];
+        return wm[0];
+    }
+    return wm[0] > wm[1] ? wm[0] : wm[1];
 }
 
 // CTA coarse stage of a synthesis pyramid: windows of levels cbot..bot for the
@@ -213,18 +221,24 @@ inline int pyr_wmax_cta(int nu, int top, int bot, int cbot, int ccb, bool vmp, i
     return wm;
 }
 
-// Same for an analysis pyramid (steps top..bot+1, chunks of 2^cb at level top).
-inline int pyr_wmax_ana(int nu, int top, int bot, int cb, bool vmp) {
-    int wm = 1;
+// Same for an analysis pyramid (steps top..bot+1, chunks of 2^cb at level top);
+// the input window of step s lives in slot (top - s) & 1, *wm2 = slot 1's max.
+inline int pyr_wmax_ana(int nu, int top, int bot, int cb, bool vmp, int* wm2 = nullptr) {
+    int wm[2] = {1, 1};
     const int lnc = top - cb;
     for (long long c = 0; c < (1ll << lnc); ++c) {
         Win r{int(c << (bot - lnc)), int((c + 1) << (bot - lnc))};
         for (int s = bot + 1; s <= top; ++s) {
-            r = ana_need(nu, 1 << s, r, vmp);
-            if (r.hi - r.lo > wm) wm = r.hi - r.lo;
+            r = ana_need(nu, 1 << s, r, vmp);  // input window of step s
+            const int slot = (top - s) & 1;
+            if (r.hi - r.lo > wm[slot]) wm[slot] = r.hi - r.lo;
         }
     }
-    return wm;
+    if (wm2) {
+        *wm2 = wm[1];
+        return wm[0];
+    }
+    return wm[0] > wm[1] ? wm[0] : wm[1];
 }
 cudaError_t launch_small(int nu, const SmallArgs& a, bool adj, cudaStream_t st);
 long long small_smem_query(int nu, int V, int j, int q, bool adj, bool vf);

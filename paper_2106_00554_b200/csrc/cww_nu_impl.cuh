@@ -110,7 +110,7 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
     const int nw = nchunk < 8 ? nchunk : 8;
     const dim3 grid((unsigned)(nchunk / nw), (unsigned)a.nvec);
     if (analysis) {
-        long long nb = (long long)nw * (64 + 2ll * a.wmax);
+        long long nb = (long long)nw * (64ll + a.wmax + a.wmax2);
         if (a.tail && nb < (2ll << a.bot)) nb = 2ll << a.bot;
         const long long smem = (FS + nb) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -118,7 +118,7 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     } else {
-        long long smem = (FS + (long long)nw * (48 + 2ll * a.wmax + a.dsum)) * 8;
+        long long smem = (FS + (long long)nw * (48ll + a.wmax + a.wmax2 + a.dsum)) * 8;
         if (a.cbot >= 0 && a.cbot < a.bot) smem += (48 + 2ll * a.cwmax + a.cdsum) * 8;  // CTA coarse stage
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_idwt_wpyr<CWW_NU>;
@@ -192,7 +192,7 @@ cudaError_t CWW_FN(launch_fwd1_syn_nu)(const LargeArgs& a, const PyrArgs& p, cud
     const int nw = R1 * Gm::B / 512;
     if (nw < 1 || nw > 16) return cudaErrorInvalidConfiguration;
     const long long smem =
-        (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48 + 2ll * p.wmax + p.dsum)) * 8;
+        (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48ll + p.wmax + p.wmax2 + p.dsum)) * 8;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto k = k_large_fwd1_syn<CWW_NU>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -206,7 +206,7 @@ long long CWW_FN(fwd1_syn_smem_nu)(int kl, const PyrArgs& p) {
     using Gm = Geo<CWW_NU, kLogB>;
     const int R1 = 1 << kl, nw = R1 * Gm::B / 512;
     if (nw < 1 || nw > 16) return -1;
-    return (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48 + 2ll * p.wmax + p.dsum)) * 8;
+    return (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48ll + p.wmax + p.wmax2 + p.dsum)) * 8;
 }
 
 cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
