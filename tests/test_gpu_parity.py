@@ -97,7 +97,9 @@ LARGE = [(0, 4, 1, 14, 1, 1, 4), (0, 2, 1, 15, 2, 1, 3), (0, 4, 1, 16, 2, 1, 4),
          (1, 6, 1, 15, 1, 1, -1), (0, 1, 0, 14, 1, 1, 1), (0, 5, 1, 17, 1, 1, -1),
          # edge sums in per-warp slots (2(2nu-1)2^q > 256); multi-launch analysis pyramids;
          # periodic cones down to level 0
-         (0, 6, 1, 13, 4, 1, -1), (0, 4, 1, 18, 1, 1, 4), (0, 2, 0, 18, 1, 1, 0), (1, 3, 0, 20, 1, 1, -1)]
+         (0, 6, 1, 13, 4, 1, -1), (0, 4, 1, 18, 1, 1, 4), (0, 2, 0, 18, 1, 1, 0), (1, 3, 0, 20, 1, 1, -1),
+         # Haar q = 0 (HaarFullRankOp), coarsest level near the top, r0 above the coarse split
+         (0, 1, 0, 15, 0, 1, 0), (0, 4, 1, 13, 1, 1, 12), (0, 3, 1, 16, 2, 1, 11)]
 
 
 @pytest.mark.parametrize("case", LARGE, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
