@@ -6,7 +6,7 @@
  * /root/reference/proj paths).  Parity is pinned two ways ("Oracle"):
  *   - against the compiled reference itself (oracle/_ref/libcwwref.so, built
  *     by oracle/Makefile from the unmodified sources), and
- *   - against committed golden vectors tests/golden/*.npz produced by that
+ *   - against committed golden vectors tests/golden/ (npz files) produced by that
  *     reference (tests/golden/make_golden.py), plus the known-answer checks
  *     of the reference's own suites (proj/tests/test_walsh.cpp,
  *     proj/tests/test_wavelet.cpp) restated in tests/test_oracle.py.

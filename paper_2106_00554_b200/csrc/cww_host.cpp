@@ -811,6 +811,8 @@ cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
 Layout lay_contig(long long len) { return Layout{0, len, 0, 1, 62, 62}; }
 
 // largest power of two V <= cap with V*M <= 4096 (one small-path CTA)
+int env_int(const char* name, int dflt);
+
 int small_V(long long M, long long nvec, int cap = 32) {
     int V = 1;
     while (V * 2 <= cap && (V * 2) * M <= 4096 && V * 2 <= nvec) V *= 2;
@@ -849,7 +851,7 @@ cww::SmallArgs small_args(const cww_op* op, const double* in, Layout lin, double
 }
 
 cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
-                     long long nvec, bool adj, cudaStream_t st) {
+                     long long nvec, bool adj, cudaStream_t st, bool wav = true) {
     if (nvec == 0) return CWW_OK;
     int V = small_V(op->M, nvec);
     const bool vf = adj ? lin.vfast() : lout.vfast();
@@ -857,6 +859,7 @@ cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out
     if (cww::small_smem_query(op->nu, V, int(op->j), int(op->q), adj, vf) > 227 * 1024)
         return fail(CWW_ERR_UNSUPPORTED, "shared-memory footprint too large for nu=%d j=%u q=%u", op->nu, op->j, op->q);
     auto a = small_args(op, in, lin, out, lout, nvec, V);
+    if (!wav) a.use_idwt = 0;  // 2D: the wavelet transform of this axis runs as a separate panel pass
     // block-contiguous inputs allow a plain 16-byte copy (forward kernel)
     const long long M = op->M;
     if (lin.contig() && (V == 1 || (lin.vsh >= 62 && lin.vs == M))) a.in_block = 1;
@@ -894,6 +897,35 @@ cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     y.r0 = op->r0;
     y.cbot = -1;  // no CTA coarse stage
     return y;
+}
+
+// 2D: column wavelet transforms as a separate panel pass (see run_2d).  Off:
+// measured no faster on B200 (cfg4 1.997 vs 1.994 ms per step: the panel
+// passes cost 2 x 0.21 ms, about what the N-column passes save); read per
+// call so tests can exercise it.
+bool hoist_col_wav() { return env_int("CWW_HOIST_COLWAV", 0) != 0; }
+
+// Multilevel IDWT (inverse) / DWT of nvec vectors through layouts, V per CTA.
+cww_status run_panel_wav(const cww_op* op, const double* src, Layout ls, double* dst, Layout ld,
+                         long long nvec, bool inverse, cudaStream_t st) {
+    if (nvec == 0) return CWW_OK;
+    cww::WavArgs w{};
+    w.kind = 1;
+    w.V = small_V(op->M, nvec, 16);
+    w.tab = op->d_tab;
+    w.t = op->tabs;
+    w.nvec = nvec;
+    w.lev = int(op->j);
+    w.r0 = op->r0;
+    w.inverse = inverse ? 1 : 0;
+    w.vmp = op->vmp;
+    w.src = src;
+    w.ls = ls;
+    w.dst = dst;
+    w.ld = ld;
+    Prof pr(inverse ? "panel_idwt" : "panel_dwt", st);
+    CUDA_TRY(cww::launch_wav(op->nu, w, st));
+    return CWW_OK;
 }
 
 // ---- large path (1D, M > 2^13) ----
@@ -1135,10 +1167,29 @@ cww_status run_2d(const cww_op* op, const double* in, double* out, long long bat
     CUDA_TRY(T.alloc(size_t(batch * M * N), st));
     // row vectors: v = b*M + m ; column vectors: v = b*N + n
     Layout x_rows{0, M, 0, 1, 62, 62};                     // x[v*M + i]
+    Layout x_cols{M * M, 1, 0, M, j, 62};                  // x: (v>>j)*M^2 + (v&(M-1)) + i*M
     Layout t_rows{M * N, VC, M * VC, 1, j, lvc};           // T: (v>>j)*MN + (v&(M-1))*VC + (i>>lvc)*M*VC + (i&(VC-1))
     Layout t_cols{M * VC, 1, 0, VC, lvc, 62};              // T: (v>>lvc)*M*VC + (v&(VC-1)) + i*VC
     Layout y_cols{N * N, 1, 0, N, jq, 62};                 // y: (v>>jq)*N^2 + (v&(N-1)) + i*N
     cww_status s;
+    // Column wavelet transforms hoisted onto the M columns of the coefficient
+    // image: G = U W^-1 along columns and W^-1 acts on a different axis than
+    // the row pass, so  G X G^T = U ((W^-1 X) W^-T U^T)  -- the N-column pass
+    // runs U alone (M instead of N column wavelet transforms; exact algebra,
+    // only the rounding order changes).  Adjoint: W (U^T Y U W^T) by symmetry.
+    const bool hoist = hoist_col_wav() && op->d.use_idwt && op->r0 < j && j >= 8;
+    if (hoist) {
+        DevBuf Xw;
+        CUDA_TRY(Xw.alloc(size_t(batch * M * M), st));
+        if (!adj) {
+            if ((s = run_panel_wav(op, in, x_cols, Xw.p, x_cols, batch * M, true, st)) != CWW_OK) return s;
+            if ((s = run_small(op, Xw.p, x_rows, T.p, t_rows, batch * M, false, st)) != CWW_OK) return s;
+            return run_small(op, T.p, t_cols, out, y_cols, batch * N, false, st, false);
+        }
+        if ((s = run_small(op, in, y_cols, T.p, t_cols, batch * N, true, st, false)) != CWW_OK) return s;
+        if ((s = run_small(op, T.p, t_rows, Xw.p, x_rows, batch * M, true, st)) != CWW_OK) return s;
+        return run_panel_wav(op, Xw.p, x_cols, out, x_cols, batch * M, false, st);
+    }
     if (!adj) {
         if ((s = run_small(op, in, x_rows, T.p, t_rows, batch * M, false, st)) != CWW_OK) return s;
         return run_small(op, T.p, t_cols, out, y_cols, batch * N, false, st);

@@ -720,6 +720,151 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
 }
 
 // ---------------------------------------------------------------------------
+// panel wavelet pass (2D driver): the full multilevel IDWT / DWT of V vectors
+// per CTA through arbitrary layouts -- used for the column transforms of the
+// 2D operator, hoisted out of the N-column U pass onto the M columns of the
+// coefficient image (W^-1 along columns commutes with the row pass).
+// smem per vector: X [M] (input; analysis ping), Wb [M] (synthesis ping-pong
+// halves; output staging), C [M/2] (last coarse level / analysis pong).
+// ---------------------------------------------------------------------------
+__host__ __device__ inline long long panel_wav_smem_bytes(int fs, int V, int j) {
+    return ((long long)fs + (long long)V * ((5ll << j) / 2)) * 8;
+}
+
+template <int NU, int NT>
+__global__ void __launch_bounds__(NT, 2) k_panel_wav(WavArgs p) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x;
+    const int j = p.lev, M = 1 << j, hM = M >> 1;
+    const int V = p.V, lV = ilog2(V);
+    const long long v0 = (long long)blockIdx.x * V;
+    const int nv = (int)((p.nvec - v0) < V ? (p.nvec - v0) : V);
+    double* filt = sm;
+    double* X = filt + FiltSmem<NU>::SIZE;
+    double* Wb = X + V * M;
+    double* C = Wb + V * M;
+    const int Gs = NT / V, gid = tid / Gs, gt = tid % Gs;
+    stage_filters<NU>(filt, p.tab, p.t, tid, NT);
+    {
+        const bool vf = p.ls.vfast();  // lanes vary the vector first (column panels)
+        constexpr int U = 8;           // loads in flight per thread
+        if (vf && p.ls.esh >= 62 && p.ls.vsh >= lV && nv == V) {
+            // the CTA's V vectors are adjacent columns of one image: pointer stepping
+            const int v = tid & (V - 1), i0 = tid >> lV, di = NT >> lV;
+            const long long es = p.ls.es;
+            const double* b = p.src + p.ls.vbase(v0) + v + (long long)i0 * es;
+            double* xd = X + v * M + i0;
+            for (int i = 0; i < M; i += U * di) {
+                double r[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) r[u] = (i + u * di + i0 < M) ? __ldg(b + (long long)(i + u * di) * es) : 0.0;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (i + u * di + i0 < M) xd[i + u * di] = r[u];
+            }
+        } else
+        for (int f0 = tid; f0 < V * M; f0 += U * NT) {
+            double r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int f = f0 + u * NT;
+                const int v = vf ? f & (V - 1) : f >> j;
+                const int i = vf ? f >> lV : f & (M - 1);
+                r[u] = (f < V * M && v < nv) ? __ldg(p.src + p.ls.at(v0 + v, i)) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int f = f0 + u * NT;
+                const int v = vf ? f & (V - 1) : f >> j;
+                const int i = vf ? f >> lV : f & (M - 1);
+                if (f < V * M) X[v * M + i] = r[u];
+            }
+        }
+    }
+    __syncthreads();
+    const FiltSmem<NU> F{filt};
+    double* const ov = Wb;  // output staging (both directions)
+    if (gid < nv) {
+        const int v = gid;
+        double* xv = X + v * M;
+        double* wv = Wb + v * M;
+        double* cv = C + v * hM;
+        if (p.inverse) {  // synthesis levels r0+1 .. j (wavelet.cpp:505-513)
+            const double* cfin = idwt_group<NU, NT>(F, xv, wv, wv + hM, cv, j, p.r0, p.vmp, gt, Gs, gid, nv,
+                                                    p.tab + p.t.o_csyn, p.t.nc);
+            double* o = ov + v * M;  // the final level reads cfin (C or X) and X: Wb is free
+            constexpr int EL = FiltSmem<NU>::EL;
+            const int mlo = p.vmp ? (EL + 1) >> 1 : 0;
+            const int mhi = p.vmp ? (M - EL) >> 1 : hM;
+            const Taps<NU> tp(F);
+            for (int m = mlo + gt; m < mhi; m += Gs) {
+                double o0, o1;
+                idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, p.vmp, o0, o1);
+                o[2 * m] = o0;
+                o[2 * m + 1] = o1;
+            }
+            if (p.vmp) {
+                const int nl = 2 * mlo, nr = M - 2 * mhi;
+                for (int k2 = Gs - 1 - gt; k2 < nl + nr; k2 += Gs) {
+                    const int i = k2 < nl ? k2 : 2 * mhi + (k2 - nl);
+                    o[i] = idwt_one<NU>(F, cfin, xv + hM, M, i, true);
+                }
+            }
+        } else {  // analysis levels j .. r0+1 (wavelet.cpp:497-504)
+            double* o = ov + v * M;  // [c_r0 | d_r0 | ... | d_(j-1)]
+            const double* src = xv;
+            const int nc = p.t.nc;
+            const int lstop = nc > 0 ? 31 - __clz(nc) : p.r0;
+            for (int lev = j; lev > lstop; --lev) {
+                const int t = j - lev, n = 1 << lev, half = n >> 1;
+                const bool last = lev == p.r0 + 1;
+                double* dst = last ? o : ((t & 1) ? xv : cv);
+                for (int mm = gt; mm < half; mm += Gs) {
+                    double c, d;
+                    dwt_pair<NU>(F, src, n, mm, p.vmp, c, d);
+                    o[half + mm] = d;
+                    dst[mm] = c;
+                }
+                group_sync<NT>(gid, Gs, nv);
+                src = dst;
+            }
+            if (nc > 0) {
+                const double* cana = p.tab + p.t.o_cana;
+                for (int oo = gt; oo < kNc; oo += Gs) {
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 16
+                    for (int i = 0; i < kNc; i += 4) {
+                        a0 += __ldg(cana + i * kNc + oo) * src[i];
+                        a1 += __ldg(cana + (i + 1) * kNc + oo) * src[i + 1];
+                        a2 += __ldg(cana + (i + 2) * kNc + oo) * src[i + 2];
+                        a3 += __ldg(cana + (i + 3) * kNc + oo) * src[i + 3];
+                    }
+                    o[oo] = (a0 + a1) + (a2 + a3);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const bool vf = p.ld.vfast();
+    if (vf && p.ld.esh >= 62 && p.ld.vsh >= lV && nv == V) {
+        const int v = tid & (V - 1), i0 = tid >> lV, di = NT >> lV;
+        const long long es = p.ld.es;
+        double* b = p.dst + p.ld.vbase(v0) + v + (long long)i0 * es;
+        const double* od = ov + v * M + i0;
+#pragma unroll 4
+        for (int i = 0; i + i0 < M; i += di) b[(long long)i * es] = od[i];
+        return;
+    }
+    for (int f = tid; f < V * M; f += NT) {
+        const int v = vf ? f & (V - 1) : f >> j;
+        const int i = vf ? f >> lV : f & (M - 1);
+        if (v < nv) p.dst[p.ld.at(v0 + v, i)] = ov[v * M + i];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // wavelet levels in global memory (large path)
 // ---------------------------------------------------------------------------
 

@@ -88,7 +88,8 @@ struct LargeArgs {
 };
 
 struct WavArgs {
-    int kind;  // 0: coarse levels (one CTA per vector, shared memory)
+    int kind;  // 0: coarse levels (one CTA per vector, shared memory); 1: panel (V vectors per CTA, all levels)
+    int V;     // kind 1: vectors per CTA
     const double* tab;
     Tables t;
     long long nvec;

@@ -211,7 +211,14 @@ long long CWW_FN(fwd1_syn_smem_nu)(int kl, const PyrArgs& p) {
 
 cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
     const int nt = 256;
-    if (w.kind == 0) {
+    if (w.kind == 1) {
+        const long long smem = panel_wav_smem_bytes(FiltSmem<CWW_NU>::SIZE, w.V, w.lev);
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+        auto k = k_panel_wav<CWW_NU, 256>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const unsigned grid = (unsigned)((w.nvec + w.V - 1) / w.V);
+        if (cudaError_t e = launch_k(k, dim3(grid), dim3(256), (size_t)smem, st, w); e != cudaSuccess) return e;
+    } else if (w.kind == 0) {
         long long smem = (FiltSmem<CWW_NU>::SIZE + 3 * (1ll << w.lev)) * 8;
         auto k = k_wav_coarse<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -75,7 +75,10 @@ def test_parity_1d(orc, cuda, case, use_idwt):
 
 
 TWO_D = [(0, 2, 1, 3, 1, 2, -1), (0, 4, 1, 4, 1, 2, 4), (0, 2, 1, 6, 1, 2, 3), (0, 3, 0, 5, 2, 2, -1),
-         (0, 4, 1, 7, 1, 2, 4), (1, 5, 1, 5, 1, 2, -1), (0, 6, 0, 6, 1, 2, -1)]
+         (0, 4, 1, 7, 1, 2, 4), (1, 5, 1, 5, 1, 2, -1), (0, 6, 0, 6, 1, 2, -1),
+         # j >= 8: column wavelet transforms run as a separate panel pass on the M columns
+         (0, 4, 1, 8, 1, 2, 4), (0, 2, 0, 8, 2, 2, -1), (1, 3, 1, 9, 1, 2, 5), (0, 6, 1, 8, 1, 2, -1),
+         (0, 2, 1, 10, 1, 2, 3)]
 
 
 @pytest.mark.parametrize("case", TWO_D, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
@@ -90,6 +93,13 @@ def test_parity_2d(orc, cuda, case, use_idwt):
     for b in range(2):
         assert rel(fx[b], ref.forward(x[b], use_idwt)) <= TOL
         assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL
+
+
+@pytest.mark.parametrize("case", [c for c in TWO_D if c[3] >= 8], ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
+def test_parity_2d_panel_wavelets(orc, cuda, case, monkeypatch):
+    # column wavelet transforms hoisted into a separate panel pass (CWW_HOIST_COLWAV=1)
+    monkeypatch.setenv("CWW_HOIST_COLWAV", "1")
+    test_parity_2d(orc, cuda, case, 1)
 
 
 # large-M path (two-pass Hadamard with the L2-resident intermediate)
