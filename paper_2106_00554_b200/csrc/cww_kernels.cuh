@@ -103,6 +103,32 @@ __device__ __forceinline__ void row_adj_accum(double* trow, int sw, const double
     }
 }
 
+// Adjoint row with software pipelining: as the correlation stream passes
+// column e, y[e - 2H] is dead and its register receives the next block's
+// element (nxt: that block's base pointer, or null on the last block), so the
+// next block's 32 loads are in flight while this block is consumed.
+template <int NU, int LOGB>
+__device__ __forceinline__ void row_adj_accum_pf(double* trow, const double* kp, int S, double* y, bool first,
+                                                 const double* nxt, int a, unsigned rwn) {
+    using G = Geo<NU, LOGB>;
+    constexpr int B = G::B, H = G::H, CW = G::CW;
+    double kap[2 * H + 1];
+#pragma unroll
+    for (int l = 0; l <= 2 * H; ++l) kap[l] = kp[l * S];
+#pragma unroll
+    for (int e = 0; e < CW; ++e) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = -H; l <= H; ++l) {
+            const int k = e - H + l;
+            if (k >= 0 && k < B) acc += kap[l + H] * y[k];
+        }
+        trow[e] = first ? acc : trow[e] + acc;
+        const int kd = e - 2 * H;  // last use of y[kd] was this column
+        if (kd >= 0 && kd < B && nxt) y[kd] = __ldg(nxt + (gray_inv_hi(kd, LOGB, a) ^ rwn));
+    }
+}
+
 // Store / load one row's B sequency-ordered values: element index
 // s*M + (gray^-1(bitrev_b(nl) << a) ^ rw), specialised by layout kind.
 template <int LOGB>
@@ -1963,12 +1989,16 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
         const int rho = rho0 + (act ? ng : 0);
         const double sg = ((__popc(wlo) + __popc(rho)) & 1) ? -1.0 : 1.0;
         const unsigned glo = ((unsigned)rho << kh) | (unsigned)wlo;
-        for (int s = 0; s < S; ++s) {
-            double y[B];
-            const unsigned rw = gray_inv(glo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
-            const double* is = ib + (long long)s * M;  // large path: contiguous 1D input
+        const unsigned gi = gray_inv(glo);
+        double y[B];
+        if (act) {  // block s = 0; later blocks are prefetched by the row stage (large path: contiguous input)
 #pragma unroll
-            for (int nl = 0; nl < B; ++nl) y[nl] = act ? __ldg(is + (gray_inv_hi(nl, kLogB, a) ^ rw)) : 0.0;
+            for (int nl = 0; nl < B; ++nl) y[nl] = __ldg(ib + (gray_inv_hi(nl, kLogB, a) ^ gi));
+        } else {
+#pragma unroll
+            for (int nl = 0; nl < B; ++nl) y[nl] = 0.0;
+        }
+        for (int s = 0; s < S; ++s) {
             hadamard_reg<kLogB>(y);
             if (NU > 1) {  // per-warp partial sums, one slot per (CTA, iteration, warp)
                 constexpr int R = 2 * NP <= 16 ? 16 : 32;
@@ -1983,7 +2013,12 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
                     seg_reduce_store<R, 31u>(ev, lane, 2 * NP, true, p.epw + (((long long)v * p.nslot + slot) * S + s) * 2 * NP);
                 }
             }
-            if (act) row_adj_accum<NU, kLogB>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S, y, s == 0);
+            if (act) {
+                const double* nxt = s + 1 < S ? ib + (long long)(s + 1) * M : nullptr;
+                const unsigned rwn = gi ^ (((s + 1) & 1) ? (unsigned)(M - 1) : 0u);
+                row_adj_accum_pf<NU, kLogB>(T + ng * tst + wlo * RS, p.tab + p.t.o_kap + s, S, y, s == 0, nxt, a,
+                                            rwn);
+            }
         }
     }
     __syncthreads();
