@@ -653,6 +653,37 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
         __syncthreads();
     }
     // overlap-add + interior mask + edge columns -> X
+    if constexpr (B == 32) {  // one tile row per warp, lane = column: row indices are warp-uniform
+        const int lane = tid & 31;
+        const int hside = lane < H ? -1 : (lane >= B - H ? 1 : 0);
+        const int hcol = lane < H ? B + H + lane : lane - (B - H);
+        for (int r = tid >> 5; r < nv * A; r += NT / 32) {
+            const int v = r >> a, K = r & (A - 1);
+            const double* t = T + v * tst;
+            double val = t[(int)brev_bits((unsigned)K, a) * RS + lane + H];
+            if (hside != 0) {
+                const int Kn = K + hside;
+                if (Kn >= 0 && Kn < A) val += t[(int)brev_bits((unsigned)Kn, a) * RS + hcol];
+            }
+            const int i = K * B + lane;
+            if (NU > 1 && (K == 0 || K == A - 1) && (i < NU || i >= M - NU)) {
+                const int c = i < NU ? i : NU + i - (M - NU);
+                const double* wv = W + v * S * 2 * NP;
+                double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+                const int nsp = S * 2 * NP;
+                int sp = 0;
+                for (; sp + 4 <= nsp; sp += 4) {
+                    e0 += EM[sp * 2 * NU + c] * wv[sp];
+                    e1 += EM[(sp + 1) * 2 * NU + c] * wv[sp + 1];
+                    e2 += EM[(sp + 2) * 2 * NU + c] * wv[sp + 2];
+                    e3 += EM[(sp + 3) * 2 * NU + c] * wv[sp + 3];
+                }
+                for (; sp < nsp; ++sp) e0 += EM[sp * 2 * NU + c] * wv[sp];
+                val = (e0 + e1) + (e2 + e3);
+            }
+            X[v * M + i] = val;
+        }
+    } else
     for (int o = tid; o < nv * M; o += NT) {
         const int v = o >> j, i = o & (M - 1);
         const double* t = T + v * tst;
@@ -726,9 +757,10 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
     PHASE(4);
     const double* res = dwt ? T : X;
     const int rst = dwt ? tst : M;
-    if (p.lout.vsh >= 62 && p.lout.esh >= 62) {  // plain strides: no tiling arithmetic per element
+    if (p.lout.esh >= 62 && (p.lout.vsh >= 62 || (p.lout.vsh >= lV && nv == V))) {
+        // plain strides within the CTA's V vectors: no tiling arithmetic per element
         const long long vs = p.lout.vs, es = p.lout.es;
-        double* o0 = p.out + (v0 * vs);
+        double* o0 = p.out + p.lout.vbase(v0);
         for (int f = tid; f < V * M; f += NT) {
             const int v = of ? f & (V - 1) : f >> j;
             const int i = of ? f >> lV : f & (M - 1);
@@ -2108,8 +2140,13 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
         }
     }
     const bool has_edge = NU > 1 && (chunk == 0 || (chunk + 1) * R1 >= A);
-    double* red2 = red + (NT / 32) * 2 * NU;
     const int nr = FE <= NT ? NT / FE : 1;  // slot lanes per edge sum
+    // edge-sum scratch: the tile's pad column (RS = CW + 1; cp.async never
+    // writes it, the Hadamard never reads it) when it is long enough -- keeps
+    // the CTA inside the 3-per-SM shared-memory budget
+    const bool padred = nr * FE <= R1;
+    const int r2s = padred ? RS : 1;
+    double* red2 = padred ? T + CW : red + (NT / 32) * 2 * NU;
     for (int idx = tid; has_edge && idx < nr * FE; idx += NT) {
         const int f = idx % FE, r = idx / FE;
         const double* e0 = p.epw + (long long)v * p.nslot * FE + f;
@@ -2122,7 +2159,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
             a3 += e0[(sl + 3 * nr) * FE];
         }
         for (; sl < p.nslot; sl += nr) a0 += e0[sl * FE];
-        red2[r * FE + f] = (a0 + a1) + (a2 + a3);
+        red2[(r * FE + f) * r2s] = (a0 + a1) + (a2 + a3);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -2134,7 +2171,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     }
     for (int f = tid; has_edge && f < FE; f += NT) {
         double acc = 0.0;
-        for (int r = 0; r < nr; ++r) acc += red2[r * FE + f];
+        for (int r = 0; r < nr; ++r) acc += red2[(r * FE + f) * r2s];
         Wv[f] = acc;
     }
     __syncthreads();
@@ -2143,46 +2180,40 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     double* ob = p.out + p.lout.vbase(p.v0 + v);
     static_assert(B == 32, "one tile row per warp");
     const int lane = tid & 31;
+    // per lane: which halo (if any) it adds, and from which column of the neighbour row
+    const int hside = lane < H ? -1 : (lane >= B - H ? 1 : 0);
+    const int hcol = lane < H ? B + H + lane : lane - (B - H);
+    const double nbv = hside < 0 ? nb[lane] : (hside > 0 ? nb[H + lane - (B - H)] : 0.0);
+    const long long base = (long long)chunk * R1 * B;
+    double* xw = p.xo_is_output ? nullptr : xo + base + lane;
     for (int rl = tid >> 5; rl < R1; rl += NT / 32) {  // logical local row K_lo, lane = column
-        const int k = lane;
-        const long long pos = ((long long)chunk * R1 + rl) * B + k;
         const int ph = (int)brev_bits((unsigned)rl, kl);
-        double val = T[tile_idx(ph, k + H, RS, ph)];
-        if (k < H) {  // overlap-add of the previous row's right halo
-            if (rl > 0) {
-                const int pq = (int)brev_bits((unsigned)(rl - 1), kl);
-                val += T[tile_idx(pq, B + H + k, RS, pq)];
-            } else {
-                val += nb[k];
+        double val = T[ph * RS + lane + H];
+        if (hside != 0) {  // overlap-add of the previous row's right / the next row's left halo
+            const int rn = rl + hside;
+            val += (rn >= 0 && rn < R1) ? T[(int)brev_bits((unsigned)rn, kl) * RS + hcol] : nbv;
+        }
+        if (has_edge) {
+            const long long pos = base + (long long)rl * B + lane;
+            const long long rpos = pos - lane;  // warp-uniform: does this row hold an edge position?
+            if ((rpos < NU || rpos + B > M - NU) && (pos < NU || pos >= M - NU)) {
+                const int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
+                const double* em = p.tab + p.t.o_em + c;
+                double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+                const int nsp = S * 2 * NP;
+                int sp = 0;
+                for (; sp + 4 <= nsp; sp += 4) {
+                    e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
+                    e1 += __ldg(em + (sp + 1) * 2 * NU) * Wv[sp + 1];
+                    e2 += __ldg(em + (sp + 2) * 2 * NU) * Wv[sp + 2];
+                    e3 += __ldg(em + (sp + 3) * 2 * NU) * Wv[sp + 3];
+                }
+                for (; sp < nsp; ++sp) e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
+                val = (e0 + e1) + (e2 + e3);
             }
         }
-        if (k >= B - H) {  // and of the next row's left halo
-            const int kk = k - (B - H);
-            if (rl < R1 - 1) {
-                const int pq = (int)brev_bits((unsigned)(rl + 1), kl);
-                val += T[tile_idx(pq, kk, RS, pq)];
-            } else {
-                val += nb[H + kk];
-            }
-        }
-        const long long rpos = pos - k;  // warp-uniform: does this row hold an edge position?
-        if (NU > 1 && (rpos < NU || rpos + B > M - NU) && (pos < NU || pos >= M - NU)) {
-            const int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
-            const double* em = p.tab + p.t.o_em + c;
-            double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-            const int nsp = S * 2 * NP;
-            int sp = 0;
-            for (; sp + 4 <= nsp; sp += 4) {
-                e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
-                e1 += __ldg(em + (sp + 1) * 2 * NU) * Wv[sp + 1];
-                e2 += __ldg(em + (sp + 2) * 2 * NU) * Wv[sp + 2];
-                e3 += __ldg(em + (sp + 3) * 2 * NU) * Wv[sp + 3];
-            }
-            for (; sp < nsp; ++sp) e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
-            val = (e0 + e1) + (e2 + e3);
-        }
-        if (p.xo_is_output) ob[p.lout.eoff(pos)] = val;
-        else xo[pos] = val;
+        if (xw) xw[rl * B] = val;
+        else ob[p.lout.eoff(base + (long long)rl * B + lane)] = val;
     }
 }
 
