@@ -1831,22 +1831,26 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     const int chunk = blockIdx.x, v = blockIdx.y;
     const double* xi = p.xi + (long long)v * p.xi_vs;
     double* T = sm;
+    const double* src = p.xi_is_input ? p.in + p.lin.vbase(p.v0 + v) : xi;  // large path: contiguous
+    const long long cbase = (long long)chunk * R1 * B;
+    const bool echunk = NU > 1 && (chunk == 0 || cbase + R1 * B >= M);  // holds edge positions
     {
-        const double* src = p.xi_is_input ? p.in + p.lin.vbase(p.v0 + v) : xi;  // large path: contiguous
-        int e = tid % CW, rl = tid / CW;  // (f % CW, f / CW), stepped without division
-        for (int f = tid; f < R1 * CW; f += NT) {
-            const long long pos = (long long)(chunk * R1 + rl) * B + e - H;  // logical local row K_lo = rl
-            double* dst = T + (int)brev_bits((unsigned)rl, kl) * RS + e;
-            if (pos >= 0 && pos < M && !(NU > 1 && (pos < NU || pos >= M - NU)))
-                cp_async8(dst, src + pos);
-            else
-                *dst = 0.0;  // outside the vector, or an edge position (edge terms)
-            e += NT % CW;
-            rl += NT / CW;
-            if (e >= CW) {
-                e -= CW;
-                ++rl;
-            }
+        // each source sample once, into its row's own columns [H, B + H): one
+        // warp per logical row, lane = column (coalesced, warp-uniform row math)
+        const int lane = tid & 31;
+        for (int rl = tid >> 5; rl < R1; rl += NT / 32) {
+            const long long pos = cbase + (long long)rl * B + lane;
+            double* dst = T + (int)brev_bits((unsigned)rl, kl) * RS + H + lane;
+            if (echunk && (pos < NU || pos >= M - NU)) *dst = 0.0;  // edge position (edge terms)
+            else cp_async8(dst, src + pos);
+        }
+        if (H > 0 && tid < 2 * H) {  // the chunk's outer halos come from the neighbouring chunks
+            const bool left = tid < H;
+            const int c = left ? tid : tid - H;
+            const long long pos = left ? cbase - H + c : cbase + (long long)R1 * B + c;
+            double* dst = left ? T + c : T + (int)brev_bits((unsigned)(R1 - 1), kl) * RS + B + H + c;
+            if (pos >= 0 && pos < M && !(NU > 1 && (pos < NU || pos >= M - NU))) cp_async8(dst, src + pos);
+            else *dst = 0.0;
         }
     }
     if (NU > 1 && tid < 2 * NU) {  // raw edge values (first / last chunk)
@@ -1857,14 +1861,25 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     }
     cp_async_wait_all();
     __syncthreads();
+    if (H > 0) {  // inner halos: copies of the neighbouring rows' own columns
+        for (int f = tid; f < (R1 - 1) * 2 * H; f += NT) {
+            const int K = f / (2 * H), c = f % (2 * H);  // boundary between logical rows K and K + 1
+            const int p0 = (int)brev_bits((unsigned)K, kl) * RS, p1 = (int)brev_bits((unsigned)(K + 1), kl) * RS;
+            if (c < H) T[p0 + B + H + c] = T[p1 + H + c];  // right halo of K <- own column c of K + 1
+            else T[p1 + (c - H)] = T[p0 + B + (c - H)];    // left halo of K + 1 <- own column B - H + c' of K
+        }
+        __syncthreads();
+    }
     tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
     {
-        int e = tid % CW, ph = tid / CW;
-        for (int f = tid; f < R1 * CW; f += NT) {
-            g[f] = T[ph * RS + e];
-            e += NT % CW;
-            ph += NT / CW;
+        static_assert(CW % 2 == 0, "16-byte G stores");
+        int e = (2 * tid) % CW, ph = (2 * tid) / CW;  // (2f % CW, 2f / CW), stepped without division
+        double2* g2 = reinterpret_cast<double2*>(g);
+        for (int f = tid; f < R1 * CW / 2; f += NT) {
+            g2[f] = make_double2(T[ph * RS + e], T[ph * RS + e + 1]);
+            e += (2 * NT) % CW;
+            ph += (2 * NT) / CW;
             if (e >= CW) {
                 e -= CW;
                 ++ph;
