@@ -552,6 +552,14 @@ __host__ __device__ inline Win ana_need(int nu, int n, Win r, bool vmp) {
 
 // gray^-1(bitrev_5(nl) << a): gray^-1 is linear over XOR and
 // gray^-1(x << a) = (gray^-1(x) << a) | (parity(x) ? 2^a - 1 : 0).
+// compile-time friendly (constexpr) 5-bit reversal and inverse Gray code
+__host__ __device__ constexpr unsigned brev_c5(int v) {
+    return ((v & 1) << 4) | ((v & 2) << 2) | (v & 4) | ((v & 8) >> 2) | ((v & 16) >> 4);
+}
+__host__ __device__ constexpr unsigned gray_inv_c(unsigned g) {
+    return g ^ (g >> 1) ^ (g >> 2) ^ (g >> 3) ^ (g >> 4) ^ (g >> 5) ^ (g >> 6) ^ (g >> 7);
+}
+
 __device__ __forceinline__ unsigned gray_inv_hi(int nl, int logb, int a) {
     const unsigned x = brev_bits((unsigned)nl, logb);
     const unsigned gx = gray_inv(x);

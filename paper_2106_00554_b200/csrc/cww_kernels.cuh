@@ -2002,11 +2002,22 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
         row_fwd<NU, kLogB>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S,
                            NU > 1 ? ES + s * 2 * NP : nullptr, sg, z);
         // g = bitrev_j(N*B + n_lo) = bitrev5(n_lo)*A + bitrev_kl(N_lo)*R2 + bitrev_kh(N_hi)
+        // element index gray_inv_hi(nl) ^ rw = (gx ^ rh) * A + (low a bits), with
+        // rw = gray_inv(glo) ^ (odd s ? M - 1 : 0): rh = 0 or 31, and the low
+        // part rl or rl ^ (A - 1) by the parity of bitrev5(nl) -- two base
+        // pointers and a compile-time multiple of +-A per store
         const unsigned glo = ((unsigned)rho << kh) | (unsigned)wlo;
-        const unsigned rw = gray_inv(glo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
+        const unsigned rl = gray_inv(glo) ^ ((s & 1) ? (unsigned)(A - 1) : 0u);
         double* os = ob + (long long)s * M;  // large path: contiguous 1D output
+        const int stp = (s & 1) ? -A : A;
+        double* pe = os + rl + ((s & 1) ? 31ll * A : 0ll);
+        double* po = os + (rl ^ (unsigned)(A - 1)) + ((s & 1) ? 31ll * A : 0ll);
 #pragma unroll
-        for (int nl = 0; nl < B; ++nl) os[gray_inv_hi(nl, kLogB, a) ^ rw] = z[nl];
+        for (int nl = 0; nl < B; ++nl) {
+            const unsigned x = brev_c5(nl);
+            const int gx = (int)gray_inv_c(x);
+            ((__popc(x) & 1) ? po : pe)[(long long)gx * stp] = z[nl];
+        }
     }
 }
 
