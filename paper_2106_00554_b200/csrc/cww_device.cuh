@@ -552,10 +552,13 @@ __host__ __device__ inline Win ana_need(int nu, int n, Win r, bool vmp) {
 
 // gray^-1(bitrev_5(nl) << a): gray^-1 is linear over XOR and
 // gray^-1(x << a) = (gray^-1(x) << a) | (parity(x) ? 2^a - 1 : 0).
-// compile-time friendly (constexpr) 5-bit reversal and inverse Gray code
-__host__ __device__ constexpr unsigned brev_c5(int v) {
-    return ((v & 1) << 4) | ((v & 2) << 2) | (v & 4) | ((v & 8) >> 2) | ((v & 16) >> 4);
+// compile-time friendly (constexpr) bit reversal and inverse Gray code
+__host__ __device__ constexpr unsigned brev_c(int v, int bits) {
+    unsigned r = 0;
+    for (int b = 0; b < bits; ++b) r |= (unsigned)((v >> b) & 1) << (bits - 1 - b);
+    return r;
 }
+__host__ __device__ constexpr unsigned brev_c5(int v) { return brev_c(v, 5); }
 __host__ __device__ constexpr unsigned gray_inv_c(unsigned g) {
     return g ^ (g >> 1) ^ (g >> 2) ^ (g >> 3) ^ (g >> 4) ^ (g >> 5) ^ (g >> 6) ^ (g >> 7);
 }
@@ -564,6 +567,28 @@ __device__ __forceinline__ unsigned gray_inv_hi(int nl, int logb, int a) {
     const unsigned x = brev_bits((unsigned)nl, logb);
     const unsigned gx = gray_inv(x);
     return (gx << a) | ((__popc(x) & 1) ? ((1u << a) - 1u) : 0u);
+}
+
+// Sequency-ordered row access (row_store / row_load / the large adjoint):
+// element nl of a row sits at gray_inv_hi(nl) ^ rw, rw = gray_inv(w) ^ (odd
+// block ? M - 1 : 0) with gray_inv(w) < A.  Since gray_inv_hi(nl) = gx * A |
+// (parity(bitrev(nl)) ? A - 1 : 0), the address is pe/po + gx * step: two
+// base pointers by parity and a compile-time multiple of one stride, valid
+// whenever the layout is affine over multiples of A (plain strides, or a
+// tiled layout whose tile width divides A).
+__device__ __forceinline__ bool seq_linear(const Layout& L, int a) { return L.esh >= 62 || a >= L.esh; }
+
+template <int LOGB, class P>
+__device__ __forceinline__ void seq_ptrs(P* ob, const Layout& L, int a, unsigned rw, P*& pe, P*& po,
+                                         long long& step) {
+    const long long A = 1ll << a;
+    const bool odd = (rw >> a) != 0u;
+    const unsigned rl = rw & (unsigned)(A - 1);
+    const long long ea = L.eoff(A);
+    const long long base = odd ? (long long)((1 << LOGB) - 1) * ea : 0ll;
+    pe = ob + L.eoff(rl) + base;
+    po = ob + L.eoff(rl ^ (unsigned)(A - 1)) + base;
+    step = odd ? -ea : ea;
 }
 
 }  // namespace cww

@@ -109,7 +109,7 @@ __device__ __forceinline__ void row_adj_accum(double* trow, int sw, const double
 // next block's 32 loads are in flight while this block is consumed.
 template <int NU, int LOGB>
 __device__ __forceinline__ void row_adj_accum_pf(double* trow, const double* kp, int S, double* y, bool first,
-                                                 const double* nxt, int a, unsigned rwn) {
+                                                 const double* pe, const double* po, long long step) {
     using G = Geo<NU, LOGB>;
     constexpr int B = G::B, H = G::H, CW = G::CW;
     double kap[2 * H + 1];
@@ -125,7 +125,10 @@ __device__ __forceinline__ void row_adj_accum_pf(double* trow, const double* kp,
         }
         trow[e] = first ? acc : trow[e] + acc;
         const int kd = e - 2 * H;  // last use of y[kd] was this column
-        if (kd >= 0 && kd < B && nxt) y[kd] = __ldg(nxt + (gray_inv_hi(kd, LOGB, a) ^ rwn));
+        if (kd >= 0 && kd < B && pe) {
+            const unsigned xb = brev_c(kd, LOGB);
+            y[kd] = __ldg(((__popc(xb) & 1) ? po : pe) + (long long)gray_inv_c(xb) * step);
+        }
     }
 }
 
@@ -133,7 +136,16 @@ __device__ __forceinline__ void row_adj_accum_pf(double* trow, const double* kp,
 // s*M + (gray^-1(bitrev_b(nl) << a) ^ rw), specialised by layout kind.
 template <int LOGB>
 __device__ __forceinline__ void row_store(double* ob, const Layout& L, int a, unsigned rw, const double* z) {
-    if (L.contig()) {
+    if (seq_linear(L, a)) {
+        double *pe, *po;
+        long long step;
+        seq_ptrs<LOGB>(ob, L, a, rw, pe, po, step);
+#pragma unroll
+        for (int nl = 0; nl < (1 << LOGB); ++nl) {
+            const unsigned x = brev_c(nl, LOGB);
+            ((__popc(x) & 1) ? po : pe)[(long long)gray_inv_c(x) * step] = z[nl];
+        }
+    } else if (L.contig()) {
 #pragma unroll
         for (int nl = 0; nl < (1 << LOGB); ++nl) ob[gray_inv_hi(nl, LOGB, a) ^ rw] = z[nl];
     } else if (L.esh >= 62) {
@@ -152,6 +164,15 @@ __device__ __forceinline__ void row_load(const double* ib, const Layout& L, int 
     if (!act) {
 #pragma unroll
         for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = 0.0;
+    } else if (seq_linear(L, a)) {
+        const double *pe, *po;
+        long long step;
+        seq_ptrs<LOGB>(ib, L, a, rw, pe, po, step);
+#pragma unroll
+        for (int nl = 0; nl < (1 << LOGB); ++nl) {
+            const unsigned x = brev_c(nl, LOGB);
+            y[nl] = __ldg(((__popc(x) & 1) ? po : pe) + (long long)gray_inv_c(x) * step);
+        }
     } else if (L.contig()) {
 #pragma unroll
         for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = __ldg(ib + (gray_inv_hi(nl, LOGB, a) ^ rw));
@@ -2049,9 +2070,16 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
         const unsigned glo = ((unsigned)rho << kh) | (unsigned)wlo;
         const unsigned gi = gray_inv(glo);
         double y[B];
-        if (act) {  // block s = 0; later blocks are prefetched by the row stage (large path: contiguous input)
+        const Layout lc{0, 0, 0, 1, 62, 62};  // large path: contiguous 1D input
+        if (act) {  // block s = 0; later blocks are prefetched by the row stage
+            const double *pe, *po;
+            long long step;
+            seq_ptrs<kLogB>(ib, lc, a, gi, pe, po, step);
 #pragma unroll
-            for (int nl = 0; nl < B; ++nl) y[nl] = __ldg(ib + (gray_inv_hi(nl, kLogB, a) ^ gi));
+            for (int nl = 0; nl < B; ++nl) {
+                const unsigned x = brev_c(nl, kLogB);
+                y[nl] = __ldg(((__popc(x) & 1) ? po : pe) + (long long)gray_inv_c(x) * step);
+            }
         } else {
 #pragma unroll
             for (int nl = 0; nl < B; ++nl) y[nl] = 0.0;
@@ -2072,10 +2100,13 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
                 }
             }
             if (act) {
-                const double* nxt = s + 1 < S ? ib + (long long)(s + 1) * M : nullptr;
-                const unsigned rwn = gi ^ (((s + 1) & 1) ? (unsigned)(M - 1) : 0u);
-                row_adj_accum_pf<NU, kLogB>(T + ng * tst + wlo * RS, p.tab + p.t.o_kap + s, S, y, s == 0, nxt, a,
-                                            rwn);
+                const double *pe = nullptr, *po = nullptr;
+                long long step = 0;
+                if (s + 1 < S)
+                    seq_ptrs<kLogB>(ib + (long long)(s + 1) * M, lc, a, gi ^ (((s + 1) & 1) ? (unsigned)(M - 1) : 0u),
+                                    pe, po, step);
+                row_adj_accum_pf<NU, kLogB>(T + ng * tst + wlo * RS, p.tab + p.t.o_kap + s, S, y, s == 0, pe, po,
+                                            step);
             }
         }
     }
