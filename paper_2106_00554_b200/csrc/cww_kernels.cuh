@@ -145,13 +145,6 @@ __device__ __forceinline__ void row_store(double* ob, const Layout& L, int a, un
             const unsigned x = brev_c(nl, LOGB);
             ((__popc(x) & 1) ? po : pe)[(long long)gray_inv_c(x) * step] = z[nl];
         }
-    } else if (L.contig()) {
-#pragma unroll
-        for (int nl = 0; nl < (1 << LOGB); ++nl) ob[gray_inv_hi(nl, LOGB, a) ^ rw] = z[nl];
-    } else if (L.esh >= 62) {
-        const long long es = L.es;
-#pragma unroll
-        for (int nl = 0; nl < (1 << LOGB); ++nl) ob[(long long)(gray_inv_hi(nl, LOGB, a) ^ rw) * es] = z[nl];
     } else {
 #pragma unroll
         for (int nl = 0; nl < (1 << LOGB); ++nl) ob[L.eoff(gray_inv_hi(nl, LOGB, a) ^ rw)] = z[nl];
@@ -173,13 +166,6 @@ __device__ __forceinline__ void row_load(const double* ib, const Layout& L, int 
             const unsigned x = brev_c(nl, LOGB);
             y[nl] = __ldg(((__popc(x) & 1) ? po : pe) + (long long)gray_inv_c(x) * step);
         }
-    } else if (L.contig()) {
-#pragma unroll
-        for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = __ldg(ib + (gray_inv_hi(nl, LOGB, a) ^ rw));
-    } else if (L.esh >= 62) {
-        const long long es = L.es;
-#pragma unroll
-        for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = __ldg(ib + (long long)(gray_inv_hi(nl, LOGB, a) ^ rw) * es);
     } else {
 #pragma unroll
         for (int nl = 0; nl < (1 << LOGB); ++nl) y[nl] = __ldg(ib + L.eoff(gray_inv_hi(nl, LOGB, a) ^ rw));
