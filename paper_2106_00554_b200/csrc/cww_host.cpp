@@ -1920,6 +1920,18 @@ static cww_status host_call_async(const cww_op* op, const double* in, size_t in_
     if (!in || !out) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     if (!is_pinned(in) || !is_pinned(out)) return host_call(op, in, in_len, out, out_len, batch, adj);
     CUDA_TRY(cudaSetDevice(op->device));
+    static const size_t zc_max = size_t(env_int("CWW_ZERO_COPY_KB", 256)) << 10;
+    if ((in_len + out_len) * sizeof(double) <= zc_max && op->M <= (1ll << cww::kSmallMaxLog)) {
+        // tiny transforms (small path: each input read once, each output written
+        // once): the kernels read / write the pinned buffers over PCIe directly
+        // (zero-copy) -- no copy launches on the latency-bound path
+        cudaPointerAttributes ai{}, ao{};
+        if (cudaPointerGetAttributes(&ai, in) == cudaSuccess && cudaPointerGetAttributes(&ao, out) == cudaSuccess &&
+            ai.devicePointer && ao.devicePointer)
+            return run(op, static_cast<const double*>(ai.devicePointer), static_cast<double*>(ao.devicePointer),
+                       (long long)batch, adj, st);
+        cudaGetLastError();
+    }
     if ((in_len + out_len) * sizeof(double) <= (size_t(2) << 20)) {  // small: one stream, no pipeline
         double *din = nullptr, *dout = nullptr;
         CUDA_TRY(cudaMallocAsync(&din, in_len * sizeof(double), st));

@@ -406,9 +406,12 @@ def test_pinned_host_async_path(orc, cuda):
     import torch
     cw = _cw()
     spec = cw.WaveletSpec(cw.Family.Daubechies, 4, cw.Boundary.Vmp)
-    for j in (9, 14):
-        op = cw.ComposedOp(cw.FastOp(spec, j, 2), None, True, 4)
-        B = 37
+    # (9, 37) / (14, 37): chunk-pipelined copies; the tiny ones (<= 256 KB) run
+    # zero-copy on the pinned buffers, including 2D and the Haar op (config 1)
+    cases = [(cw.ComposedOp(cw.FastOp(spec, j, 2), None, True, 4), B) for j, B in ((9, 37), (14, 37), (10, 1), (6, 5))]
+    cases.append((cw.ComposedOp(cw.FastOp(spec, 5, 1, 2), None, True, 4), 2))
+    cases.append((cw.HaarFullRankOp(10, 1, 1), 1))
+    for op, B in cases:
         x = torch.randn((B, op.cols()), dtype=torch.float64).pin_memory()
         y = torch.randn((B, op.rows()), dtype=torch.float64).pin_memory()
         fo = torch.empty((B, op.rows()), dtype=torch.float64).pin_memory()
