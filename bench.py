@@ -127,14 +127,14 @@ def algorithmic_bytes(cfg, kernel: str, batch: int) -> float:
         return 8.0 * batch * mats * (M * M + 2 * M * N + N * N)
     CW = 32 + 2 * (nu - 1)
     A = M // 32
-    lc = min(j - 1, 13)
+    lc = min(j - 1, 10)  # coarse levels <= 10 run in k_wav_coarse / the analysis tail (CWW_PYR_SYN_BOT)
     per = {
         "small_fwd": M + N, "small_adj": M + N,
         "large_fwd1": M + A * CW, "large_fwd1_syn": M + A * CW, "large_fwd2": A * CW + N,
         "large_adj2": N + A * CW, "large_adj1": A * CW + M,
-        "idwt_level": sum(2 * (1 << lev) for lev in range(lc + 1, j + 1)),
-        "dwt_level": sum(2 * (1 << lev) for lev in range(lc + 1, j + 1)),
-        "wav_coarse": 2 * 2 * (1 << lc),
+        # all launches of a step together: every coefficient read once, every sample written once
+        "idwt_pyr": 2 * M, "dwt_pyr": 2 * M,
+        "wav_coarse": 2 * (1 << lc),
     }
     return 8.0 * batch * per.get(kernel, 0)
 

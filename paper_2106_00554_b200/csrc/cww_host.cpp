@@ -883,6 +883,8 @@ const int kPyrSynBot = env_int("CWW_PYR_SYN_BOT", 10);  // coarse levels <= this
 const int kWpyrLog = env_int("CWW_WPYR_LOG", 9);       // warp pyramid: 2^9 fine samples per warp
 const int kWpyrLevels = env_int("CWW_WPYR_LEVELS", 0);  // synthesis levels per launch (0: 6 if j <= 17, else 4)
 const int kWpyrAnaLevels = env_int("CWW_WPYR_ANA_LEVELS", 3);  // analysis steps per launch
+const int kWpyrMinLog = env_int("CWW_WPYR_MIN_LOG", 9);      // narrowest analysis warp chunk (9: off)
+const long long kWpyrMinWarps = env_int("CWW_WPYR_MIN_WARPS", 148 * 16);  // warps wanted per launch
 // last synthesis pyramid inside forward pass 1 (xi never written).  Off: on
 // B200 the fused kernel is no faster (cfg2 68 us vs 42 + 27 us; cfg3 slower) --
 // both halves are latency-bound, so the saved xi round trip does not show.
@@ -1134,7 +1136,10 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     const double* src = w0.p;
     double* sink[2] = {w1.p, w0.p};
     for (int it = 0;; ++it) {
-        const int cb = std::min(T, kWpyrLog);
+        int cb = std::min(T, kWpyrLog);
+        // small grids (the last launches of short vectors): narrower warp chunks so
+        // at least ~2 CTAs of 8 warps per SM get work (halo overhead grows instead)
+        while (cb > kWpyrMinLog && nvec * (1ll << (T - cb)) < kWpyrMinWarps) --cb;
         const int bot = std::max({op->r0, T - kWpyrAnaLevels, T - cb});
         const bool tail = bot > op->r0 && bot <= std::max(kPyrSynBot, op->r0);
         cww::PyrArgs y = pyr_args(op, nvec);

@@ -441,23 +441,41 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
     PHASE(0);
     stage_filters<NU>(filt, p.tab, p.t, tid, NT);
     stage_ke<NU>(KE, p.tab, p.t, S, tid, NT);
+    constexpr int U = 4;  // 16-byte loads in flight per thread
     if (p.in_block == 1 && M >= 2) {  // V vectors back to back: 16-byte copy
         const double2* blk = reinterpret_cast<const double2*>(p.in + p.lin.vbase(v0));
         const int tot2 = (nv * M) >> 1;
-        for (int f = tid; f < tot2; f += NT) {
-            const double2 val = __ldg(blk + f);
-            X[2 * f] = val.x;
-            X[2 * f + 1] = val.y;
+        for (int f0 = tid; f0 < tot2; f0 += U * NT) {
+            double2 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = f0 + u * NT < tot2 ? __ldg(blk + f0 + u * NT) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int f = f0 + u * NT;
+                if (f < tot2) {
+                    X[2 * f] = r[u].x;
+                    X[2 * f + 1] = r[u].y;
+                }
+            }
         }
     } else if (p.in_block == 2 && V >= 2) {  // [M][V] interleaved block (column panel)
         const double2* blk = reinterpret_cast<const double2*>(p.in + p.lin.vbase(v0));
         const int tot2 = (V * M) >> 1;
-        for (int f = tid; f < tot2; f += NT) {
-            const int v = (2 * f) & (V - 1), i = (2 * f) >> lV;
-            if (v < nv) {
-                const double2 val = __ldg(blk + f);
-                X[v * M + i] = val.x;
-                X[(v + 1) * M + i] = val.y;
+        for (int f0 = tid; f0 < tot2; f0 += U * NT) {
+            double2 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int f = f0 + u * NT;
+                r[u] = (f < tot2 && ((2 * f) & (V - 1)) < nv) ? __ldg(blk + f) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int f = f0 + u * NT;
+                const int v = (2 * f) & (V - 1), i = (2 * f) >> lV;
+                if (f < tot2 && v < nv) {
+                    X[v * M + i] = r[u].x;
+                    X[(v + 1) * M + i] = r[u].y;
+                }
             }
         }
     } else {
@@ -500,17 +518,32 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
             const int mlo = p.vmp ? (EL + 1) >> 1 : 0;
             const int mhi = p.vmp ? (M - EL) >> 1 : hM;
             const Taps<NU> tp(F);
-            for (int m = mlo + gt; m < mhi; m += Gs) {
-                double o0, o1;
-                idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, p.vmp, o0, o1);
-                put(2 * m, o0);
-                put(2 * m + 1, o1);
-            }
-            if (p.vmp) {
+            if (p.vmp && B >= 2) {  // interior pairs hold no edge position: both samples in one tile row
+                for (int m = mlo + gt; m < mhi; m += Gs) {
+                    double o0, o1;
+                    idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, true, o0, o1);
+                    double* d = tv + (int)brev_bits((unsigned)((2 * m) >> LOGB), a) * RS + ((2 * m) & (B - 1)) + H;
+                    d[0] = o0;
+                    d[1] = o1;
+                }
                 const int nl = 2 * mlo, nr = M - 2 * mhi;
                 for (int k2 = Gs - 1 - gt; k2 < nl + nr; k2 += Gs) {
                     const int i = k2 < nl ? k2 : 2 * mhi + (k2 - nl);
                     put(i, idwt_one<NU>(F, cfin, xv + hM, M, i, true));
+                }
+            } else {
+                for (int m = mlo + gt; m < mhi; m += Gs) {
+                    double o0, o1;
+                    idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, p.vmp, o0, o1);
+                    put(2 * m, o0);
+                    put(2 * m + 1, o1);
+                }
+                if (p.vmp) {
+                    const int nl = 2 * mlo, nr = M - 2 * mhi;
+                    for (int k2 = Gs - 1 - gt; k2 < nl + nr; k2 += Gs) {
+                        const int i = k2 < nl ? k2 : 2 * mhi + (k2 - nl);
+                        put(i, idwt_one<NU>(F, cfin, xv + hM, M, i, true));
+                    }
                 }
             }
         }
