@@ -308,14 +308,15 @@ __device__ __forceinline__ double idwt_one(const FiltSmem<NU>& F, const double* 
     const int half = n >> 1;
     const int par = (i + NU + 1) & 1;
     if (!vmp) {
-        double acc = 0.0;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
         for (int k = 0; k < NU; ++k) {
             const int u = -NU + 1 + 2 * k + par;
             const int mm = ((i - u) & (n - 1)) >> 1;
-            acc += F.h(u) * cv[mm] + F.g(u) * dv[mm];
+            a0 = fma(F.h(u), cv[mm], a0);
+            a1 = fma(F.g(u), dv[mm], a1);
         }
-        return acc;
+        return a0 + a1;
     }
     constexpr int EL = FiltSmem<NU>::EL, CI = FiltSmem<NU>::CI;
     if (n < 8 * NU) return idwt_sample_full2<NU>(F, cv, dv, n, i, vmp);
@@ -324,22 +325,29 @@ __device__ __forceinline__ double idwt_one(const FiltSmem<NU>& F, const double* 
         const int ii = side ? n - 1 - i : i;
         const double* sc = F.syn(side, ii, 0);
         const double* sd = F.syn(side, ii, 1);
-        double acc = 0.0;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;  // four short chains (latency)
 #pragma unroll
         for (int k = 0; k < CI; ++k) {
             const int idx = side ? half - 1 - k : k;
-            acc += sc[k * EL] * cv[idx] + sd[k * EL] * dv[idx];
+            if (k & 1) {
+                a1 = fma(sc[k * EL], cv[idx], a1);
+                b1 = fma(sd[k * EL], dv[idx], b1);
+            } else {
+                a0 = fma(sc[k * EL], cv[idx], a0);
+                b0 = fma(sd[k * EL], dv[idx], b0);
+            }
         }
-        return acc;
+        return (a0 + a1) + (b0 + b1);
     }
-    double acc = 0.0;
+    double a0 = 0.0, a1 = 0.0;
 #pragma unroll
     for (int k = 0; k < NU; ++k) {
         const int u = -NU + 1 + 2 * k + par;
         const int mm = (i - u) >> 1;
-        acc += F.h(u) * cv[mm] + F.g(u) * dv[mm];
+        a0 = fma(F.h(u), cv[mm], a0);
+        a1 = fma(F.g(u), dv[mm], a1);
     }
-    return acc;
+    return a0 + a1;
 }
 
 // Paired synthesis: fine samples 2m and 2m+1 share one window of nu+1 coarse
@@ -451,20 +459,30 @@ template <int NU>
 __device__ __forceinline__ void dwt_pair(const FiltSmem<NU>& F, const double* x, int n, int mm,
                                          bool vmp, double& c, double& d) {
     const int half = n >> 1;
-    double a = 0.0, b = 0.0;
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;  // two chains per output (latency)
     if (!vmp) {
 #pragma unroll
         for (int u = -NU + 1; u <= NU; ++u) {
             const double xv = x[(2 * mm + u) & (n - 1)];
-            a += F.h(u) * xv;
-            b += F.g(u) * xv;
+            if (u & 1) {
+                a1 = fma(F.h(u), xv, a1);
+                b1 = fma(F.g(u), xv, b1);
+            } else {
+                a0 = fma(F.h(u), xv, a0);
+                b0 = fma(F.g(u), xv, b0);
+            }
         }
     } else if (mm >= NU && mm < half - NU) {
 #pragma unroll
         for (int u = -NU + 1; u <= NU; ++u) {
             const double xv = x[2 * mm + u];
-            a += F.h(u) * xv;
-            b += F.g(u) * xv;
+            if (u & 1) {
+                a1 = fma(F.h(u), xv, a1);
+                b1 = fma(F.g(u), xv, b1);
+            } else {
+                a0 = fma(F.h(u), xv, a0);
+                b0 = fma(F.g(u), xv, b0);
+            }
         }
     } else {
         constexpr int EL = FiltSmem<NU>::EL;
@@ -475,12 +493,17 @@ __device__ __forceinline__ void dwt_pair(const FiltSmem<NU>& F, const double* x,
 #pragma unroll
         for (int k = 0; k < EL; ++k) {
             const double xv = x[side ? n - 1 - k : k];
-            a += ra[k] * xv;
-            b += rb[k] * xv;
+            if (k & 1) {
+                a1 = fma(ra[k], xv, a1);
+                b1 = fma(rb[k], xv, b1);
+            } else {
+                a0 = fma(ra[k], xv, a0);
+                b0 = fma(rb[k], xv, b0);
+            }
         }
     }
-    c = a;
-    d = b;
+    c = a0 + a1;
+    d = b0 + b1;
 }
 
 // Programmatic dependent launch (PDL): every kernel triggers its dependents

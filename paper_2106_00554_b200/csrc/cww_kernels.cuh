@@ -1117,15 +1117,20 @@ __device__ __forceinline__ void dwt_pair_log(const FiltSmem<NU>& F, const Taps<N
     const int m = side ? half - 1 - mm : mm;
     const double* ra = F.ana(side, 0, m);
     const double* rb = F.ana(side, 1, m);
-    double a = 0.0, b = 0.0;
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;  // two chains per output (latency)
 #pragma unroll
     for (int k = 0; k < EL; ++k) {
         const double xv = x[side ? n - 1 - k : k];
-        a += ra[k] * xv;
-        b += rb[k] * xv;
+        if (k & 1) {
+            a1 = fma(ra[k], xv, a1);
+            b1 = fma(rb[k], xv, b1);
+        } else {
+            a0 = fma(ra[k], xv, a0);
+            b0 = fma(rb[k], xv, b0);
+        }
     }
-    c = a;
-    d = b;
+    c = a0 + a1;
+    d = b0 + b1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1659,14 +1664,15 @@ __device__ __forceinline__ void syn_up(const FiltSmem<NU>& F, const Taps<NU>& tp
         const int side = tid < EL ? 0 : 1, ii = side ? tid - EL : tid, i = side ? n - 1 - ii : ii;
         const double* sc = F.syn(side, ii, 0);
         const double* sd = F.syn(side, ii, 1);
-        double acc = 0.0;
+        double a0 = 0.0, a1 = 0.0;  // two chains (this helper warp gates the barrier)
 #pragma unroll
         for (int k = 0; k < CI; ++k) {
             const int idx = side ? half - 1 - k : k;
             const double cv = PADIN ? cs[pidx(idx)] : cs[idx];
-            acc += sc[k * EL] * cv + sd[k * EL] * ds[pidx(idx)];
+            a0 = fma(sc[k * EL], cv, a0);
+            a1 = fma(sd[k * EL], ds[pidx(idx)], a1);
         }
-        dst[pidx(i)] = acc;
+        dst[pidx(i)] = a0 + a1;
     }
     __syncthreads();
     if (edge) {
@@ -1705,13 +1711,19 @@ __device__ __forceinline__ void ana_down(const FiltSmem<NU>& F, const Taps<NU>& 
         const int side = tid < NU ? 0 : 1, m = side ? tid - NU : tid, k = side ? half - 1 - m : m;
         const double* ra = F.ana(side, 0, m);
         const double* rb = F.ana(side, 1, m);
-        double a = 0.0, b = 0.0;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
         for (int q = 0; q < EL; ++q) {
             const double xv = xs[pidx(side ? n - 1 - q : q)];
-            a += ra[q] * xv;
-            b += rb[q] * xv;
+            if (q & 1) {
+                a1 = fma(ra[q], xv, a1);
+                b1 = fma(rb[q], xv, b1);
+            } else {
+                a0 = fma(ra[q], xv, a0);
+                b0 = fma(rb[q], xv, b0);
+            }
         }
+        const double a = a0 + a1, b = b0 + b1;
         out[(half + k) * es] = b;
         if (K == 1) low[k] = a;
         else other[pidx(k)] = a;
