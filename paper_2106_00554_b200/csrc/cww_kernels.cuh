@@ -1865,6 +1865,333 @@ __global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
 }
 
 // ---------------------------------------------------------------------------
+// compact-halo register rows (k_normal_rows_x): k_normal_rows_reg without the
+// shared-memory copies of the register levels.  Every level publishes only
+//   * its segment boundaries -- the first / last HH values of each thread's
+//     segment (Ex: [thread][2 HH + 1], odd stride: conflict free), from which
+//     the neighbours take their window halos, and
+//   * its edge zones -- the first / last EW values of the level (Z: [2][EW]),
+//     from which the threads that OWN the VMP edge samples / rows / band edge
+//     rows compute them (no helper threads, no re-reads after the barrier).
+// Exchange and zone buffers are double-buffered across the one barrier per
+// level.  ~56 KB of shared memory instead of ~110 KB: 3 CTAs per SM.
+// ---------------------------------------------------------------------------
+template <int NU>
+struct NxGeo {
+    static constexpr int OFF = (NU + 1) / 2;       // synthesis window: left reach (coarse)
+    static constexpr int SR = NU + 1 - OFF;        // synthesis window: right reach
+    static constexpr int Bw = 2 * NU - 2;          // band half width
+    static constexpr int WL = NU - 1;              // analysis window reach (fine), both sides
+    static constexpr int m1 = OFF > SR ? OFF : SR;
+    static constexpr int m2 = Bw > WL ? Bw : WL;
+    static constexpr int HH = (m1 > m2 ? m1 : m2) > 0 ? (m1 > m2 ? m1 : m2) : 1;  // halo depth
+    static constexpr int XS = 2 * HH + 1;          // exchange stride per thread
+    static constexpr int EW = 64;                  // edge-zone width (>= 3nu-1, 2nu, E + Bw)
+};
+
+// value g (0 <= g < K * RNT) of a level published with K values per thread
+template <int HH>
+__device__ __forceinline__ double nx_get(const double* ex, int XS, int g, int lk, int K) {
+    const int u = g >> lk, o = g & (K - 1);
+    if (K <= HH || o < HH) return ex[u * XS + o];
+    return ex[u * XS + HH + o - (K - HH)];
+}
+
+// publish this thread's segment v[K] (first / last HH, edge zones of a level of n values)
+template <int HH, int K>
+__device__ __forceinline__ void nx_put(double* ex, int XS, double* z, int EW, int n, const double (&v)[K]) {
+    const int tid = threadIdx.x, g0 = tid * K;
+#pragma unroll
+    for (int o = 0; o < (K < HH ? K : HH); ++o) ex[tid * XS + o] = v[o];
+    if (K > HH) {
+#pragma unroll
+        for (int o = 0; o < HH; ++o) ex[tid * XS + HH + o] = v[K - HH + o];
+    }
+    if (g0 < EW) {
+#pragma unroll
+        for (int o = 0; o < K; ++o)
+            if (g0 + o < EW) z[g0 + o] = v[o];
+    }
+    if (g0 + K > n - EW) {
+#pragma unroll
+        for (int o = 0; o < K; ++o)
+            if (g0 + o >= n - EW) z[EW + g0 + o - (n - EW)] = v[o];
+    }
+}
+
+template <int NU, int J, int RNT>
+__global__ void __launch_bounds__(RNT, 3) k_normal_rows_x(NormArgs p) {
+    constexpr int RLOG = 8;  // levels <= 2^RLOG: plain shared memory (one value per thread at RLOG)
+    static_assert(RNT == (1 << RLOG), "one level-RLOG value per thread");
+    constexpr int M = 1 << J, KT = M / (2 * RNT), FT = 2 * KT;
+    constexpr int FS = FiltSmem<NU>::SIZE, W = 4 * NU - 3, PM = M + M / 32, NL = 1 << RLOG;
+    using X_ = NxGeo<NU>;
+    constexpr int HH = X_::HH, XS = X_::XS, EW = X_::EW, OFF = X_::OFF, Bw = X_::Bw, WL = X_::WL;
+    constexpr int EL = FiltSmem<NU>::EL, CI = FiltSmem<NU>::CI;
+    extern __shared__ double sm[];
+    double* filt = sm;
+    double* gE = sm + FS;
+    double* X = gE + 2 * p.E * W;  // staged input row, padded (coarse + every level's details)
+    double* Ex0 = X + PM;          // boundary exchange, double-buffered
+    double* Ex1 = Ex0 + RNT * XS;
+    double* Z0 = Ex1 + RNT * XS;   // edge zones [2][EW], double-buffered
+    double* Z1 = Z0 + 2 * EW;
+    double* L0 = Z1 + 2 * EW;      // plain buffers of the coarse (<= 2^RLOG) levels
+    double* L1 = L0 + NL;
+    double* XL = L1 + NL;          // plain copy of the input's first 2^RLOG values
+    pdl_trigger();
+    pdl_wait();
+    const int tid = threadIdx.x;
+    const bool vmp = p.vmp != 0;
+    for (int i = tid; i < FS; i += RNT) filt[i] = p.tab[p.t.o_h + i];
+    for (int i = tid; i < 2 * p.E * W; i += RNT) gE[i] = p.band[i];
+    double gI[W];
+#pragma unroll
+    for (int d = 0; d < W; ++d) gI[d] = __ldg(p.band + 2 * p.E * W + d);
+    const long long v = blockIdx.x;
+    const long long es = p.es > 0 ? p.es : 1;
+    const long long vb = p.es > 0 ? (v / p.vpi) * p.ivs + (v % p.vpi) * p.in_vs : v * p.in_vs;
+    const double* xg = p.in + vb;
+    double* out = p.out + (p.es > 0 ? vb : v * p.out_vs);
+#pragma unroll
+    for (int r = 0; r < M / RNT; ++r) cp_async8(X + pidx(tid + r * RNT), xg + (tid + r * RNT) * es);
+    cp_async8(XL + tid, xg + tid * es);
+    cp_async_wait_all();
+    __syncthreads();
+    const FiltSmem<NU> F{filt};
+    const Taps<NU> tp(F);
+    // coarse synthesis levels r0+1 .. RLOG (plain shared memory)
+    const int nc = 1 << p.r0;
+    {
+        const double* src = XL;
+        double* dst = L0;
+        for (int lev = p.r0 + 1; lev <= RLOG; ++lev) {
+            const int n = 1 << lev;
+            idwt_level_vec<NU>(F, src, XL + (n >> 1), dst, n, vmp, tid, RNT);
+            __syncthreads();
+            src = dst;
+            dst = (dst == L0) ? L1 : L0;
+        }
+        // the level-RLOG values, one per thread, published as a register level
+        const double c1[1] = {src[tid]};
+        nx_put<HH, 1>(Ex0, XS, Z0, EW, NL, c1);
+    }
+    __syncthreads();
+    double* exc = Ex0;  // published coarse level (read side)
+    double* zc = Z0;
+    double* exn = Ex1;  // next level (write side)
+    double* zn = Z1;
+    // ---- register synthesis levels RLOG+1 .. J: K coarse values -> 2K fine ----
+    double fine[FT];
+    {
+        double cbuf[KT];  // coarse values of the current level (K of them used)
+        cbuf[0] = exc[tid * XS];  // level RLOG: the thread's own value
+        // unrolled over K = 1, 2, 4, .., KT
+#define NX_SYN_LEVEL(K)                                                                                   \
+        {                                                                                                 \
+            constexpr int kK = (K);                                                                       \
+            constexpr int lk = (kK == 1 ? 0 : kK == 2 ? 1 : kK == 4 ? 2 : kK == 8 ? 3 : kK == 16 ? 4 : 5); \
+            const int half = kK * RNT, n = 2 * half, m0 = tid * kK;                                       \
+            const double* ds = X + pidx(half);                                                            \
+            constexpr int WN = kK + NU + 1;                                                               \
+            double cw[WN], dw[WN];                                                                        \
+            _Pragma("unroll") for (int w = 0; w < WN; ++w) {                                              \
+                int idx = m0 - OFF + w;                                                                   \
+                const bool ok = !vmp || (idx >= 0 && idx < half);                                         \
+                idx &= half - 1;                                                                          \
+                if (w >= OFF && w < OFF + kK) cw[w] = cbuf[w - OFF];                                      \
+                else cw[w] = ok ? nx_get<HH>(exc, XS, idx, lk, kK) : 0.0;                                 \
+                dw[w] = ok ? ds[pidx(idx)] : 0.0;                                                         \
+            }                                                                                             \
+            double f[2 * kK];                                                                             \
+            _Pragma("unroll") for (int q = 0; q < kK; ++q) {                                              \
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;                                            \
+                _Pragma("unroll") for (int u = -NU + 1; u <= NU; ++u) {                                   \
+                    if ((u & 1) == 0) {                                                                   \
+                        const int ix = OFF - u / 2 + q;                                                   \
+                        a0 = fma(tp.h[u + NU - 1], cw[ix], a0);                                           \
+                        b0 = fma(tp.g[u + NU - 1], dw[ix], b0);                                           \
+                    } else {                                                                              \
+                        const int ix = OFF - (u - 1) / 2 + q;                                             \
+                        a1 = fma(tp.h[u + NU - 1], cw[ix], a1);                                           \
+                        b1 = fma(tp.g[u + NU - 1], dw[ix], b1);                                           \
+                    }                                                                                     \
+                }                                                                                         \
+                f[2 * q] = a0 + b0;                                                                       \
+                f[2 * q + 1] = a1 + b1;                                                                   \
+            }                                                                                             \
+            if (vmp && (2 * m0 < EL || 2 * m0 + 2 * kK > n - EL)) {  /* owned VMP edge samples */        \
+                _Pragma("unroll") for (int q = 0; q < 2 * kK; ++q) {                                      \
+                    const int i = 2 * m0 + q;                                                             \
+                    if (i < EL || i >= n - EL) {                                                          \
+                        const int side = i < EL ? 0 : 1, ii = side ? n - 1 - i : i;                       \
+                        const double* sc = F.syn(side, ii, 0);                                            \
+                        const double* sd = F.syn(side, ii, 1);                                            \
+                        double e0 = 0.0, e1 = 0.0;                                                        \
+                        _Pragma("unroll") for (int k = 0; k < CI; ++k) {                                  \
+                            const int idx = side ? half - 1 - k : k;                                      \
+                            const double cv = side ? zc[EW + EW - 1 - k] : zc[k];                         \
+                            e0 = fma(sc[k * EL], cv, e0);                                                 \
+                            e1 = fma(sd[k * EL], ds[pidx(idx)], e1);                                      \
+                        }                                                                                 \
+                        f[q] = e0 + e1;                                                                   \
+                    }                                                                                     \
+                }                                                                                         \
+            }                                                                                             \
+            if constexpr (kK < KT) {                                                                      \
+                nx_put<HH, 2 * kK>(exn, XS, zn, EW, n, f);                                                \
+                _Pragma("unroll") for (int q = 0; q < 2 * kK; ++q) cbuf[q] = f[q];                        \
+            } else {                                                                                      \
+                nx_put<HH, 2 * kK>(exn, XS, zn, EW, n, f);                                                \
+                _Pragma("unroll") for (int q = 0; q < 2 * kK; ++q) fine[q] = f[q];                        \
+            }                                                                                             \
+            __syncthreads();                                                                              \
+            { double* t_ = exc; exc = exn; exn = t_; t_ = zc; zc = zn; zn = t_; }                         \
+        }
+        if constexpr (KT >= 1) NX_SYN_LEVEL(1)
+        if constexpr (KT >= 2) NX_SYN_LEVEL(2)
+        if constexpr (KT >= 4) NX_SYN_LEVEL(4)
+        if constexpr (KT >= 8) NX_SYN_LEVEL(8)
+        if constexpr (KT >= 16) NX_SYN_LEVEL(16)
+#undef NX_SYN_LEVEL
+    }
+    // ---- band product in registers (halos and edge rows from the published top level) ----
+    double y[FT];
+    {
+        const int i0 = tid * FT;
+        constexpr int WN = FT + 2 * Bw;
+        constexpr int lk = (FT == 2 ? 1 : FT == 4 ? 2 : FT == 8 ? 3 : FT == 16 ? 4 : 5);
+        double xw[WN];
+#pragma unroll
+        for (int w = 0; w < WN; ++w) {
+            const int idx = i0 - Bw + w;
+            if (w >= Bw && w < Bw + FT) xw[w] = fine[w - Bw];
+            else xw[w] = (!vmp || (idx >= 0 && idx < M)) ? nx_get<HH>(exc, XS, idx & (M - 1), lk, FT) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < FT; ++r) {
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int d = 0; d < W; ++d) {
+                if (d & 1) a1 = fma(gI[d], xw[r + d], a1);
+                else a0 = fma(gI[d], xw[r + d], a0);
+            }
+            y[r] = a0 + a1;
+        }
+        const int E = p.E;
+        if (i0 < E || i0 + FT > M - E) {  // owned band edge rows: tabulated, inputs from the edge zones
+#pragma unroll
+            for (int r = 0; r < FT; ++r) {
+                const int i = i0 + r;
+                if (i < E || i >= M - E) {
+                    const double* g = gE + (i < E ? i : i - (M - 2 * E)) * W;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int d = 0; d < W; ++d) {
+                        int k = i + d - Bw;
+                        if (!vmp) k &= M - 1;
+                        if (k >= 0 && k < M) acc = fma(g[d], k < EW ? zc[k] : zc[EW + k - (M - EW)], acc);
+                    }
+                    y[r] = acc;
+                }
+            }
+        }
+        nx_put<HH, FT>(exn, XS, zn, EW, M, y);
+        __syncthreads();
+        { double* t_ = exc; exc = exn; exn = t_; t_ = zc; zc = zn; zn = t_; }
+    }
+    // ---- register analysis levels J .. RLOG+1: 2K fine values -> K coarse + K details ----
+    {
+        double xb[FT];
+#pragma unroll
+        for (int q = 0; q < FT; ++q) xb[q] = y[q];
+#define NX_ANA_LEVEL(K)                                                                                   \
+        {                                                                                                 \
+            constexpr int kK = (K);                                                                       \
+            constexpr int l2 = (kK == 1 ? 1 : kK == 2 ? 2 : kK == 4 ? 3 : kK == 8 ? 4 : kK == 16 ? 5 : 6); \
+            const int half = kK * RNT, n = 2 * half, k0 = tid * kK;                                       \
+            constexpr int WN = 2 * kK + 2 * NU - 2;                                                       \
+            double xw[WN];                                                                                \
+            _Pragma("unroll") for (int w = 0; w < WN; ++w) {                                              \
+                int idx = 2 * k0 - WL + w;                                                                \
+                const bool ok = !vmp || (idx >= 0 && idx < n);                                            \
+                idx &= n - 1;                                                                             \
+                if (w >= WL && w < WL + 2 * kK) xw[w] = xb[w - WL];                                       \
+                else xw[w] = ok ? nx_get<HH>(exc, XS, idx, l2, 2 * kK) : 0.0;                             \
+            }                                                                                             \
+            double c[kK], d[kK];                                                                          \
+            _Pragma("unroll") for (int r = 0; r < kK; ++r) {                                              \
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;                                            \
+                _Pragma("unroll") for (int u = -NU + 1; u <= NU; ++u) {                                   \
+                    const double xv = xw[2 * r + u + WL];                                                 \
+                    if (u & 1) {                                                                          \
+                        a1 = fma(tp.h[u + NU - 1], xv, a1);                                               \
+                        b1 = fma(tp.g[u + NU - 1], xv, b1);                                               \
+                    } else {                                                                              \
+                        a0 = fma(tp.h[u + NU - 1], xv, a0);                                               \
+                        b0 = fma(tp.g[u + NU - 1], xv, b0);                                               \
+                    }                                                                                     \
+                }                                                                                         \
+                c[r] = a0 + a1;                                                                           \
+                d[r] = b0 + b1;                                                                           \
+            }                                                                                             \
+            if (vmp && (k0 < NU || k0 + kK > half - NU)) {  /* owned VMP edge rows (wavelet.cpp:403-445) */ \
+                _Pragma("unroll") for (int r = 0; r < kK; ++r) {                                          \
+                    const int k = k0 + r;                                                                 \
+                    if (k < NU || k >= half - NU) {                                                       \
+                        const int side = k < NU ? 0 : 1, m = side ? half - 1 - k : k;                     \
+                        const double* ra = F.ana(side, 0, m);                                             \
+                        const double* rb = F.ana(side, 1, m);                                             \
+                        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;                                    \
+                        _Pragma("unroll") for (int q = 0; q < EL; ++q) {                                  \
+                            const double xv = side ? zc[EW + EW - 1 - q] : zc[q];                         \
+                            if (q & 1) {                                                                  \
+                                a1 = fma(ra[q], xv, a1);                                                  \
+                                b1 = fma(rb[q], xv, b1);                                                  \
+                            } else {                                                                      \
+                                a0 = fma(ra[q], xv, a0);                                                  \
+                                b0 = fma(rb[q], xv, b0);                                                  \
+                            }                                                                             \
+                        }                                                                                 \
+                        c[r] = a0 + a1;                                                                   \
+                        d[r] = b0 + b1;                                                                   \
+                    }                                                                                     \
+                }                                                                                         \
+            }                                                                                             \
+            double* od = out + (half + k0) * es;                                                          \
+            _Pragma("unroll") for (int r = 0; r < kK; ++r) od[r * es] = d[r];                             \
+            if constexpr (kK > 1) {                                                                       \
+                nx_put<HH, kK>(exn, XS, zn, EW, half, c);                                                 \
+                _Pragma("unroll") for (int r = 0; r < kK; ++r) xb[r] = c[r];                              \
+                __syncthreads();                                                                          \
+                { double* t_ = exc; exc = exn; exn = t_; t_ = zc; zc = zn; zn = t_; }                     \
+            } else {                                                                                      \
+                L0[tid] = c[0];                                                                           \
+                __syncthreads();                                                                          \
+            }                                                                                             \
+        }
+        if constexpr (KT >= 16) NX_ANA_LEVEL(16)
+        if constexpr (KT >= 8) NX_ANA_LEVEL(8)
+        if constexpr (KT >= 4) NX_ANA_LEVEL(4)
+        if constexpr (KT >= 2) NX_ANA_LEVEL(2)
+        NX_ANA_LEVEL(1)
+#undef NX_ANA_LEVEL
+    }
+    // coarse analysis levels RLOG .. r0+1 (plain shared memory)
+    double* cur = L0;
+    double* nxt = L1;
+    for (int lev = RLOG; lev > p.r0; --lev) {
+        const int n = 1 << lev, half = n >> 1;
+        dwt_level_vec<NU>(F, tp, cur, nxt, out + half * es, n, vmp, tid, RNT, es);
+        __syncthreads();
+        double* t0 = cur;
+        cur = nxt;
+        nxt = t0;
+    }
+    for (int i = tid; i < nc; i += RNT) out[i * es] = cur[i];
+}
+
+// ---------------------------------------------------------------------------
 // large path: two-pass Hadamard over K with an L2-resident intermediate
 // ---------------------------------------------------------------------------
 // G per vector: [2^kh chunks][R1 physical rows][CW]; chunk c = K_hi (forward

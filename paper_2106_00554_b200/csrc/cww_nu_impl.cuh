@@ -163,8 +163,34 @@ cudaError_t normal_reg_t(const NormArgs& a, cudaStream_t st) {
 }
 }  // namespace
 
+namespace {
+template <int J>
+cudaError_t normal_x_t(const NormArgs& a, cudaStream_t st) {
+    using X_ = NxGeo<CWW_NU>;
+    const long long smem = (FiltSmem<CWW_NU>::SIZE + 2ll * a.E * (4 * CWW_NU - 3) + ((1 << J) + (1 << J) / 32) +
+                            2ll * 256 * X_::XS + 4ll * X_::EW + 3ll * 256) * 8;
+    auto k = k_normal_rows_x<CWW_NU, J, 256>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaError_t e = launch_k(k, dim3((unsigned)a.nvec), dim3(256), (size_t)smem, st, a); e != cudaSuccess)
+        return e;
+    return cudaGetLastError();
+}
+}  // namespace
+
 // register-resident variant: use_idwt, 2^9 <= M <= 2^12, r0 < kRegLog
 cudaError_t CWW_FN(launch_normal_rows_reg_nu)(const NormArgs& a, cudaStream_t st) {
+    static const bool nx = [] {  // compact-halo variant (k_normal_rows_x, opt-in: measured even)
+        const char* e = std::getenv("CWW_NORMAL_X");
+        return e && e[0] == '1';
+    }();
+    if (nx && a.E + NxGeo<CWW_NU>::Bw <= NxGeo<CWW_NU>::EW && a.j >= 9 && a.j <= 12) {
+        switch (a.j) {
+            case 9: return normal_x_t<9>(a, st);
+            case 10: return normal_x_t<10>(a, st);
+            case 11: return normal_x_t<11>(a, st);
+            default: return normal_x_t<12>(a, st);
+        }
+    }
     static const int rnt = [] {
         const char* e = std::getenv("CWW_NORMAL_RNT");
         return e && std::atoi(e) == 512 ? 512 : 256;

@@ -11,6 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def rel(a, b):
@@ -272,6 +273,28 @@ def test_normal_form_matches_forward_adjoint(orc, cuda, case, use_idwt, iters):
     for b in range(2):
         assert rel(host(got)[b], host(want)[b]) <= 1e-12
     assert rel(host(got)[0], z) <= 1e-12
+
+
+def test_normal_form_compact_halo_kernel(cuda):
+    """The opt-in compact-halo normal-rows kernel (CWW_NORMAL_X=1, read once per
+    process) against repeated adjoint(forward(x)): run in a child process."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import torch, paper_2106_00554_b200 as cw\n"
+        "for fam, nu, bnd, j, q, dim, r0 in [(0, 2, 1, 12, 1, 2, 3), (0, 4, 1, 10, 2, 1, 4), (1, 3, 0, 9, 1, 1, -1),\n"
+        "                                   (0, 6, 1, 11, 1, 1, 5), (0, 2, 0, 12, 1, 1, 2)]:\n"
+        "    op = cw.ComposedOp(cw.FastOp(cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd)), j, q, dim), None, True, r0)\n"
+        "    x = torch.randn((2, op.cols()), dtype=torch.float64, device='cuda')\n"
+        "    want = op.adjoint(op.forward(op.adjoint(op.forward(x))))\n"
+        "    got = op.normal(x.clone(), iters=2)\n"
+        "    e = float(torch.linalg.norm(got - want) / torch.linalg.norm(want))\n"
+        "    assert e <= 1e-12, (fam, nu, bnd, j, e)\n"
+        "print('ok')\n") % REPO
+    env = dict(os.environ, CWW_NORMAL_X="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_host_pointer_path(orc, cuda):
