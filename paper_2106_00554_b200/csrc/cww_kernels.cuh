@@ -414,6 +414,7 @@ __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 
 template <int NU, int LOGB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
+    const bool vmp_ = NU > 1 && p.vmp != 0;  // VMP needs nu >= 2: no VMP code in the Haar kernels
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using G = Geo<NU, LOGB>;
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         const double* xv = X + v * M;
         double* tv = T + v * tst;
         const double* cfin = xv;
-        if (idwt) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, p.vmp, gt, Gs, gid, nv,
+        if (idwt) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, vmp_, gt, Gs, gid, nv,
                                                  p.tab + p.t.o_csyn, p.t.nc);
         PHASE(2);
         auto put = [&](int i, double val) {
@@ -511,14 +512,14 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         };
         if (!idwt) {
             for (int i = gt; i < M; i += Gs) put(i, xv[i]);
-        } else if (p.vmp && M < 8 * NU) {
+        } else if (vmp_ && M < 8 * NU) {
             for (int i = gt; i < M; i += Gs) put(i, idwt_sample_full2<NU>(F, cfin, xv + hM, M, i, true));
         } else {
             constexpr int EL = FiltSmem<NU>::EL;
-            const int mlo = p.vmp ? (EL + 1) >> 1 : 0;
-            const int mhi = p.vmp ? (M - EL) >> 1 : hM;
+            const int mlo = vmp_ ? (EL + 1) >> 1 : 0;
+            const int mhi = vmp_ ? (M - EL) >> 1 : hM;
             const Taps<NU> tp(F);
-            if (p.vmp && B >= 2) {  // interior pairs hold no edge position: both samples in one tile row
+            if (NU > 1 && vmp_ && B >= 2) {  // interior pairs hold no edge position: both samples in one tile row
                 for (int m = mlo + gt; m < mhi; m += Gs) {
                     double o0, o1;
                     idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, true, o0, o1);
@@ -534,11 +535,11 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
             } else {
                 for (int m = mlo + gt; m < mhi; m += Gs) {
                     double o0, o1;
-                    idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, p.vmp, o0, o1);
+                    idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, vmp_, o0, o1);
                     put(2 * m, o0);
                     put(2 * m + 1, o1);
                 }
-                if (p.vmp) {
+                if (vmp_) {
                     const int nl = 2 * mlo, nr = M - 2 * mhi;
                     for (int k2 = Gs - 1 - gt; k2 < nl + nr; k2 += Gs) {
                         const int i = k2 < nl ? k2 : 2 * mhi + (k2 - nl);
@@ -609,6 +610,7 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
 
 template <int NU, int LOGB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
+    const bool vmp_ = NU > 1 && p.vmp != 0;  // VMP needs nu >= 2: no VMP code in the Haar kernels
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using G = Geo<NU, LOGB>;
@@ -769,11 +771,35 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
             const bool last = lev == p.r0 + 1;
             double* dst = last ? ov : ((t & 1) ? xv : cv);  // coarse rows ping-pong C <-> X
             const double* s2 = src;
-            for (int mm = gt; mm < half; mm += Gs) {
-                double c, d;
-                dwt_pair<NU>(F, s2, n, mm, p.vmp, c, d);
-                ov[half + mm] = d;
-                dst[mm] = c;
+            if (NU > 1 && vmp_ && half >= 2 * NU + 2) {  // (VMP needs nu >= 2: no code for Haar)
+                // interior rows [NU, half - NU) two per thread (shared window), then
+                // the odd leftover and the 2 NU edge rows on the last threads
+                const Taps<NU> tp(F);
+                const int nq = (half - 2 * NU) >> 1;
+                for (int qi = gt; qi < nq; qi += Gs) {
+                    const int mm = NU + 2 * qi;
+                    double c0, d0, c1, d1;
+                    dwt_quad_inner<NU>(tp, s2, mm, c0, d0, c1, d1);
+                    ov[half + mm] = d0;
+                    ov[half + mm + 1] = d1;
+                    dst[mm] = c0;
+                    dst[mm + 1] = c1;
+                }
+                const int odd = (half - 2 * NU) & 1;
+                for (int k2 = Gs - 1 - gt; k2 < 2 * NU + odd; k2 += Gs) {
+                    const int mm = k2 < NU ? k2 : (k2 < 2 * NU ? half - 2 * NU + k2 : half - NU - 1);
+                    double c, d;
+                    dwt_pair<NU>(F, s2, n, mm, true, c, d);
+                    ov[half + mm] = d;
+                    dst[mm] = c;
+                }
+            } else {
+                for (int mm = gt; mm < half; mm += Gs) {
+                    double c, d;
+                    dwt_pair<NU>(F, s2, n, mm, vmp_, c, d);
+                    ov[half + mm] = d;
+                    dst[mm] = c;
+                }
             }
             group_sync<NT>(gid, Gs, nv);
             src = dst;
