@@ -433,10 +433,11 @@ def main():
         steps_bytes = algorithmic_bytes(cfg, kname, batch) * args.steps
         achieved = steps_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
         traffic, tnote = None, None
-        try:  # committed ncu capture of this config's dominant kernel (profiles/r01_traffic.json)
-            tr = json.load(open(os.path.join(REPO, "profiles", "r01_traffic.json")))[str(args.config)]
-            if tr["kernel"] == kname:
-                traffic, tnote = tr["bytes"], tr["launch"] + " (ncu dram__bytes_read+write, profiles/)"
+        try:  # committed ncu captures of this config's leading kernels (profiles/r01_traffic.json)
+            trs = json.load(open(os.path.join(REPO, "profiles", "r01_traffic.json")))[str(args.config)]
+            for tr in (trs if isinstance(trs, list) else [trs]):
+                if tr["kernel"] == kname:
+                    traffic, tnote = tr["bytes"], tr["launch"] + " (ncu dram__bytes_read+write, profiles/)"
         except (OSError, KeyError, ValueError):
             pass
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,

@@ -17,9 +17,10 @@ for _ in range(2):
         op.forward(x); op.adjoint(y)
 torch.cuda.synchronize()
 PY
-for spec in "1:small_fwd" "2:large_adj2" "3:large_adj2" "4:small_adj" "5:normal_rows"; do
-  c=${spec%%:*}; k=${spec##*:}
+# spec = config:kernel[:launches per call] -- the second call's launches are captured
+for spec in "1:small_fwd" "1:small_adj" "2:large_adj2" "2:dwt_wpyr:2" "3:large_adj2" "4:small_adj:2" "5:normal_rows"; do
+  c=$(echo $spec | cut -d: -f1); k=$(echo $spec | cut -d: -f2); n=$(echo $spec | cut -d: -f3); n=${n:-1}
   python /tmp/dom.py $c
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
-      -k regex:"$k" -s 1 -c 1 python /tmp/dom.py $c 2>/dev/null | grep -E "dram__|gpu__" | sed "s/^/cfg$c,/"
+      -k regex:"$k" -s $n -c $n python /tmp/dom.py $c 2>/dev/null | grep -E "dram__|gpu__" | sed "s/^/cfg$c,/"
 done
