@@ -545,6 +545,12 @@ __device__ __forceinline__ void dwt_quad_inner(const Taps<NU>& tp, const double*
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// Asynchronous 16-byte global -> shared copy (both addresses 16-byte aligned).
+__device__ __forceinline__ void cp_async16(double* sdst, const double* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
 // Asynchronous 8-byte global -> shared copy (LDGSTS): many loads in flight
 // per thread without register staging.
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
@@ -645,6 +651,21 @@ __device__ __forceinline__ void seq_ptrs(P* ob, const Layout& L, int a, unsigned
     pe = ob + L.eoff(rl) + base;
     po = ob + L.eoff(rl ^ (unsigned)(A - 1)) + base;
     step = odd ? -ea : ea;
+}
+
+// One warp copies w contiguous doubles global -> shared asynchronously; when
+// source and destination share their 16-byte phase the body moves in 16-byte
+// pieces (half the copy instructions), an unaligned head / odd tail singly.
+__device__ __forceinline__ void warp_copy_span(double* dst, const double* src, int w, int lane) {
+    if (((reinterpret_cast<uintptr_t>(dst) ^ reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        const int head = (reinterpret_cast<uintptr_t>(src) & 15) ? 1 : 0;
+        if (lane == 0 && head && w > 0) cp_async8(dst, src);
+        const int body = (w - head) >> 1;
+        for (int t = lane; t < body; t += 32) cp_async16(dst + head + 2 * t, src + head + 2 * t);
+        if (lane == 0 && w > head && ((w - head) & 1)) cp_async8(dst + w - 1, src + w - 1);
+    } else {
+        for (int t = lane; t < w; t += 32) cp_async8(dst + t, src + t);
+    }
 }
 
 }  // namespace cww

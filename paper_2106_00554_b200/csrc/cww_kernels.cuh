@@ -1222,6 +1222,7 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
         const int lo = wlo[lev - 1], w = whi[lev - 1] - lo, hf = 1 << (lev - 1);
         const double* ds = xb + hf;
         double* dd = D + doff[lev];
+        // (16-byte window copies measured slower here: cfg2 49.8 vs 47.3 us)
         for (int t = lane; t < w; t += 32) cp_async8(dd + t, ds + (vmp ? lo + t : ((lo + t) & (hf - 1))));
     }
     cp_async_wait_all();
@@ -1401,7 +1402,12 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
     {
         const double* src = p.src + v * p.src_vs;
         const int lo = xlo[p.top], w = xhi[p.top] - lo, n = 1 << p.top;
-        for (int t = lane; t < w; t += 32) cp_async8(X + t, src + (vmp ? lo + t : ((lo + t) & (n - 1))));
+        if (vmp) {  // window start shifted to the source's 16-byte phase (host slack: +1 in slot 0)
+            if ((reinterpret_cast<uintptr_t>(X) ^ reinterpret_cast<uintptr_t>(src + lo)) & 8) ++X;
+            warp_copy_span(X, src + lo, w, lane);
+        } else {
+            for (int t = lane; t < w; t += 32) cp_async8(X + t, src + ((lo + t) & (n - 1)));
+        }
     }
     cp_async_wait_all();
     __syncwarp();
