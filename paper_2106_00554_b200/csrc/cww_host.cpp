@@ -883,6 +883,9 @@ const int kPyrSynBot = env_int("CWW_PYR_SYN_BOT", 10);  // coarse levels <= this
 const int kWpyrLog = env_int("CWW_WPYR_LOG", 9);       // warp pyramid: 2^9 fine samples per warp
 const int kWpyrLevels = env_int("CWW_WPYR_LEVELS", 0);  // synthesis levels per launch (0: 6 if j <= 17, else 4)
 const int kWpyrAnaLevels = env_int("CWW_WPYR_ANA_LEVELS", 3);  // analysis steps per launch
+// analysis levels <= this: one CTA per vector (k_wav_coarse).  Off: measured even
+// (cfg2 0.2584 vs 0.2600 ms at 12, worse at 13; cfg3 2.512 vs 2.514 ms)
+const int kAnaCtaTail = env_int("CWW_ANA_CTA_TAIL", 0);
 const int kWpyrMinLog = env_int("CWW_WPYR_MIN_LOG", 9);      // narrowest analysis warp chunk (9: off)
 const long long kWpyrMinWarps = env_int("CWW_WPYR_MIN_WARPS", 148 * 16);  // warps wanted per launch
 // last synthesis pyramid inside forward pass 1 (xi never written).  Off: on
@@ -1136,6 +1139,27 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     const double* src = w0.p;
     double* sink[2] = {w1.p, w0.p};
     for (int it = 0;; ++it) {
+        if (T > op->r0 && T <= kAnaCtaTail && it > 0) {
+            // the remaining levels T .. r0+1 (2^T samples) in one CTA per vector,
+            // shared-memory ping-pong (k_wav_coarse, analysis direction)
+            cww::WavArgs w{};
+            w.kind = 0;
+            w.tab = op->d_tab;
+            w.t = op->tabs;
+            w.nvec = nvec;
+            w.lev = T;
+            w.r0 = op->r0;
+            w.inverse = 0;
+            w.vmp = op->vmp;
+            w.src = src;
+            w.src_vs = M;
+            w.dst = out;
+            w.ld = lout;
+            w.dv0 = 0;
+            Prof pr("dwt_pyr", st);
+            CUDA_TRY(cww::launch_wav(nu, w, st));
+            break;
+        }
         int cb = std::min(T, kWpyrLog);
         // small grids (the last launches of short vectors): narrower warp chunks so
         // at least ~2 CTAs of 8 warps per SM get work (halo overhead grows instead)
