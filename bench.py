@@ -471,7 +471,10 @@ def main():
         "kernels": {k: [round(v[0] / args.steps, 4), v[1] // args.steps] for k, v in prof.items()},
         "gpu_launches": launches,
         "e2e": {"value": round(e2e, 3), "unit": "matvec/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 4)},
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 4),
+                # host link throughput of the e2e step (PCIe Gen5 x16 on this box: ~55 GB/s per
+                # direction, ~99 GB/s both directions at once, tools/pcie_bw.py)
+                "link_gbs": round((h2d + d2h) / (ms_e2e / args.steps / 1e3) / 1e9, 1)},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
