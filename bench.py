@@ -6,8 +6,11 @@
 metric : forward+adjoint matvecs/s (a matvec = one U W^-1 or one W U* application
          to one vector/image) and the achieved fraction of the HBM roofline.
 step   : config 1-4: one forward of the whole batch + one adjoint of the whole
-         batch (2*batch matvecs); config 5: 50 iterations of the normal operator
-         U*U on the image (100 matvecs).  Default config: 2 (BASELINE configs[1]).
+         batch (2*batch matvecs; independent, so on two streams); config 5: 50
+         iterations of the normal operator U*U on the image (100 matvecs).
+         Default config: 2 (BASELINE configs[1]).  Configs 1-4 capture the step
+         once into a CUDA graph and replay it (same launches, no per-launch host
+         overhead; eager fallback if capture or a bitwise replay check fails).
 value  : whole-job throughput, inputs resident in HBM, device-timed with CUDA
          events per step, L2 flushed (256 MiB write) between steps, max over ranks.
 e2e    : the same metric through the public API with the step's inputs copied
@@ -313,7 +316,10 @@ def main():
         mr = M_ // world
         x_rows0 = x_dev.view(M_, M_)[rank * mr:(rank + 1) * mr].contiguous()
 
-    conc = os.environ.get("CWW_BENCH_CONCURRENT", "0") == "1"  # measured: no gain (cfg2 0.273 vs 0.269 ms)
+    # forward and adjoint of the step are independent: two streams, so one chain's
+    # latency-bound launches overlap the other's (inside the replayed CUDA graph:
+    # cfg2 0.210 vs 0.240 ms sequential; eager launches measured no gain)
+    conc = os.environ.get("CWW_BENCH_CONCURRENT", "1") == "1"
     s_dev_f, s_dev_a = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
     def step_device(concurrent=conc):
@@ -325,14 +331,15 @@ def main():
         elif concurrent:
             # forward and adjoint of the batch are independent: two streams, so one
             # chain's latency-bound phases and launch tails overlap the other's
-            s_dev_f.wait_stream(stream)
-            s_dev_a.wait_stream(stream)
+            cur = torch.cuda.current_stream(dev)  # (the capture stream inside a graph capture)
+            s_dev_f.wait_stream(cur)
+            s_dev_a.wait_stream(cur)
             with torch.cuda.stream(s_dev_f):
                 op.forward(x_dev, fo_dev)
             with torch.cuda.stream(s_dev_a):
                 op.adjoint(y_dev, ao_dev)
-            stream.wait_stream(s_dev_f)
-            stream.wait_stream(s_dev_a)
+            cur.wait_stream(s_dev_f)
+            cur.wait_stream(s_dev_a)
         else:
             op.forward(x_dev, fo_dev)
             op.adjoint(y_dev, ao_dev)
@@ -345,14 +352,15 @@ def main():
             # compute / D2H; forward and adjoint are independent, so they run on two streams
             # and the two PCIe directions overlap.  Tiny inputs (config 1) go zero-copy: the
             # kernels read and write the pinned buffers over PCIe, no copy launches.
-            s_fwd.wait_stream(stream)
-            s_adj.wait_stream(stream)
+            cur = torch.cuda.current_stream(dev)  # (the capture stream inside a graph capture)
+            s_fwd.wait_stream(cur)
+            s_adj.wait_stream(cur)
             with torch.cuda.stream(s_fwd):
                 op.forward(x_pin, fo_pin)
             with torch.cuda.stream(s_adj):
                 op.adjoint(y_pin, ao_pin)
-            stream.wait_stream(s_fwd)
-            stream.wait_stream(s_adj)
+            cur.wait_stream(s_fwd)
+            cur.wait_stream(s_adj)
             return
         x_dev.copy_(x_pin, non_blocking=True)
         if rowpart:
@@ -393,14 +401,46 @@ def main():
             ms = float(t.item())
         return ms
 
+    def graphed(fn, outs):
+        """The step captured once into a CUDA graph and replayed (the launch-bound
+        configs lose their per-launch host overhead); falls back to eager calls
+        when capture fails or a replay does not reproduce the eager outputs bit
+        for bit.  Returns (callable, kernel launches per step or None)."""
+        if os.environ.get("CWW_BENCH_GRAPH", "1") != "1" or world > 1:
+            return fn, None
+        try:
+            fn()
+            torch.cuda.synchronize(dev)
+            ref = [o.clone() for o in outs]
+            g = torch.cuda.CUDAGraph()
+            l0 = cw.kernel_launches()
+            with torch.cuda.graph(g):
+                fn()
+            per = cw.kernel_launches() - l0
+            for o in outs:
+                o.zero_()
+            g.replay()
+            torch.cuda.synchronize(dev)
+            if all(torch.equal(o, r) for o, r in zip(outs, ref)):
+                return g.replay, per
+        except Exception as e:  # noqa: BLE001 -- any capture problem: eager calls
+            print(f"bench: CUDA graph capture not used ({type(e).__name__}: {e})", file=sys.stderr)
+        torch.cuda.synchronize(dev)
+        return fn, None
+
     for _ in range(args.warmup):
         step_device()
+    torch.cuda.synchronize(dev)
+    dev_outs = [ao_dev] if (is5 or rowpart) else [fo_dev, ao_dev]
+    step_dev_g, per_launch = graphed(step_device, dev_outs) if not (is5 or rowpart) else (step_device, None)
+    for _ in range(args.warmup):
+        step_dev_g()
     torch.cuda.synchronize(dev)
 
     l0 = cw.kernel_launches()
     with Clocks(local) as clk:
-        ms = timed(step_device, args.steps)  # the reported time: no per-launch instrumentation
-        launches = cw.kernel_launches() - l0
+        ms = timed(step_dev_g, args.steps)  # the reported time: no per-launch instrumentation
+        launches = cw.kernel_launches() - l0 if per_launch is None else per_launch * args.steps
         # per-kernel breakdown: the same steps again with CUDA events around every launch
         cw.profile_enable(True)
         cw.profile_dump()
@@ -414,7 +454,11 @@ def main():
 
     for _ in range(2):
         step_e2e()
-    ms_e2e = timed(step_e2e, args.steps)
+    e2e_outs = [ao_pin] if (is5 or rowpart) else [fo_pin, ao_pin]
+    step_e2e_g, _ = graphed(step_e2e, e2e_outs) if not (is5 or rowpart) else (step_e2e, None)
+    for _ in range(2):
+        step_e2e_g()
+    ms_e2e = timed(step_e2e_g, args.steps)
 
     # weak scaling (independent batches per rank) except config 5 on P GPUs,
     # where the one image is shared (strong scaling)
@@ -458,7 +502,11 @@ def main():
         "config": {"workload": name, "batch_per_gpu": batch,
                    "step": (f"{CFG5_ITERS} x U*U on the image (cww_normal: banded normal form W G W^-1 per "
                             "axis, G = U*U exactly banded since H^T H = M I; rows fused IDWT-band-DWT, tiled "
-                            "transposes)" if is5 else "forward + adjoint of the batch"),
+                            "transposes)" if is5 else
+                            ("forward + adjoint of the batch (independent: two streams)" if conc else
+                             "forward + adjoint of the batch")),
+                   "launch": ("one CUDA graph per step (captured once, replayed; eager fallback)"
+                              if per_launch is not None else "eager launches"),
                    "l2": "flushed (256 MiB write) between timed steps",
                    "parallelism": (f"rows/{world} + NCCL all-to-all transposes" if rowpart
                                    else f"dp{world} (independent batches)")},

@@ -499,8 +499,12 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         const double* xv = X + v * M;
         double* tv = T + v * tst;
         const double* cfin = xv;
-        if (idwt) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, vmp_, gt, Gs, gid, nv,
-                                                 p.tab + p.t.o_csyn, p.t.nc);
+        // Haar (nu = 1, periodic, non-overlapping 2-tap filters): every fine sample is
+        // its own chain c_r0 -> level j through one coefficient per level, so all the
+        // levels run in ONE phase without barriers (wavelet.cpp:387-400 per step)
+        constexpr bool haar = NU == 1;
+        if (idwt && !haar) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, vmp_, gt, Gs, gid,
+                                                          nv, p.tab + p.t.o_csyn, p.t.nc);
         PHASE(2);
         auto put = [&](int i, double val) {
             if (NU > 1 && (i < NU || i >= M - NU)) {
@@ -512,6 +516,18 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         };
         if (!idwt) {
             for (int i = gt; i < M; i += Gs) put(i, xv[i]);
+        } else if (haar) {
+            const double h0 = F.h(0), h1 = F.h(1), g0 = F.g(0), g1 = F.g(1);
+            const int r0 = p.r0;
+            for (int i = gt; i < M; i += Gs) {
+                double val = xv[i >> (j - r0)];  // c_r0
+                for (int l = r0; l < j; ++l) {   // level l + 1 from level l: fine[2m + u] = h_u c[m] + g_u d[m]
+                    const int idx = i >> (j - l - 1);
+                    const double d = xv[(1 << l) + (idx >> 1)];
+                    val = (idx & 1) ? h1 * val + g1 * d : h0 * val + g0 * d;
+                }
+                put(i, val);
+            }
         } else if (vmp_ && M < 8 * NU) {
             for (int i = gt; i < M; i += Gs) put(i, idwt_sample_full2<NU>(F, cfin, xv + hM, M, i, true));
         } else {
