@@ -8,8 +8,8 @@ metric : forward+adjoint matvecs/s (a matvec = one U W^-1 or one W U* applicatio
 step   : config 1-4: one forward of the whole batch + one adjoint of the whole
          batch (2*batch matvecs; independent, so on two streams); config 5: 50
          iterations of the normal operator U*U on the image (100 matvecs).
-         Default config: 2 (BASELINE configs[1]).  Configs 1-4 capture the step
-         once into a CUDA graph and replay it (same launches, no per-launch host
+         Default config: 2 (BASELINE configs[1]).  On one GPU the step is captured
+         once into a CUDA graph and replayed (same launches, no per-launch host
          overhead; eager fallback if capture or a bitwise replay check fails).
 value  : whole-job throughput, inputs resident in HBM, device-timed with CUDA
          events per step, L2 flushed (256 MiB write) between steps, max over ranks.
@@ -432,7 +432,7 @@ def main():
         step_device()
     torch.cuda.synchronize(dev)
     dev_outs = [ao_dev] if (is5 or rowpart) else [fo_dev, ao_dev]
-    step_dev_g, per_launch = graphed(step_device, dev_outs) if not (is5 or rowpart) else (step_device, None)
+    step_dev_g, per_launch = graphed(step_device, dev_outs) if not rowpart else (step_device, None)
     for _ in range(args.warmup):
         step_dev_g()
     torch.cuda.synchronize(dev)
@@ -455,7 +455,7 @@ def main():
     for _ in range(2):
         step_e2e()
     e2e_outs = [ao_pin] if (is5 or rowpart) else [fo_pin, ao_pin]
-    step_e2e_g, _ = graphed(step_e2e, e2e_outs) if not (is5 or rowpart) else (step_e2e, None)
+    step_e2e_g, _ = graphed(step_e2e, e2e_outs) if not rowpart else (step_e2e, None)
     for _ in range(2):
         step_e2e_g()
     ms_e2e = timed(step_e2e_g, args.steps)
