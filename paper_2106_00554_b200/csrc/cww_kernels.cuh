@@ -2649,6 +2649,18 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     const double nbv = hside < 0 ? nb[lane] : (hside > 0 ? nb[H + lane - (B - H)] : 0.0);
     const long long base = (long long)chunk * R1 * B;
     double* xw = p.xo_is_output ? nullptr : xo + base + lane;
+    if (!has_edge && xw) {  // interior chunks: four rows in flight per warp (independent chains)
+#pragma unroll 4
+        for (int rl = tid >> 5; rl < R1; rl += NT / 32) {
+            double val = T[(int)brev_bits((unsigned)rl, kl) * RS + lane + H];
+            if (hside != 0) {
+                const int rn = rl + hside;
+                val += (rn >= 0 && rn < R1) ? T[(int)brev_bits((unsigned)rn, kl) * RS + hcol] : nbv;
+            }
+            xw[rl * B] = val;
+        }
+        return;
+    }
     for (int rl = tid >> 5; rl < R1; rl += NT / 32) {  // logical local row K_lo, lane = column
         const int ph = (int)brev_bits((unsigned)rl, kl);
         double val = T[ph * RS + lane + H];
