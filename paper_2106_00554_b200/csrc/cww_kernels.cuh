@@ -2250,7 +2250,9 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
-    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS;
+    // the contiguous pass's tile rows are unpadded (RS = CW): its lane patterns walk
+    // columns only, and the tile is then byte-for-byte the chunk's G block
+    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = CW;
     extern __shared__ double sm[];
     const int tid = threadIdx.x;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a;
@@ -2299,19 +2301,11 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
     }
     tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
-    {
+    {  // tile == G block: 16-byte copy
         static_assert(CW % 2 == 0, "16-byte G stores");
-        int e = (2 * tid) % CW, ph = (2 * tid) / CW;  // (2f % CW, 2f / CW), stepped without division
+        const double2* t2 = reinterpret_cast<const double2*>(T);
         double2* g2 = reinterpret_cast<double2*>(g);
-        for (int f = tid; f < R1 * CW / 2; f += NT) {
-            g2[f] = make_double2(T[ph * RS + e], T[ph * RS + e + 1]);
-            e += (2 * NT) % CW;
-            ph += (2 * NT) / CW;
-            if (e >= CW) {
-                e -= CW;
-                ++ph;
-            }
-        }
+        for (int f = tid; f < R1 * CW / 2; f += NT) g2[f] = t2[f];
     }
 }
 
@@ -2547,7 +2541,8 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
-    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
+    // unpadded tile rows (RS = CW): the chunk's G block loads as one 16-byte copy
+    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = CW, NP = Gm::NP;
     extern __shared__ double sm[];
     const int tid = threadIdx.x;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
@@ -2560,17 +2555,9 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     double* red = T + R1 * RS;       // reduction scratch: [NT/32][2H] and [NT/FE][FE]
     const double* g = p.G + (long long)v * A * CW;
     {
+        static_assert(CW % 2 == 0, "16-byte G loads");
         const double* gc = g + (long long)chunk * R1 * CW;
-        int e = tid % CW, ph = tid / CW;
-        for (int f = tid; f < R1 * CW; f += NT) {
-            cp_async8(T + ph * RS + e, gc + f);
-            e += NT % CW;
-            ph += NT / CW;
-            if (e >= CW) {
-                e -= CW;
-                ++ph;
-            }
-        }
+        for (int f = tid; f < R1 * CW / 2; f += NT) cp_async16(T + 2 * f, gc + 2 * f);
     }
     // halo contributions from the neighbouring chunks' boundary rows (sums over
     // the physical rows rho of their Hadamard rows; popc is bit-reversal invariant):
@@ -2604,12 +2591,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     }
     const bool has_edge = NU > 1 && (chunk == 0 || (chunk + 1) * R1 >= A);
     const int nr = FE <= NT ? NT / FE : 1;  // slot lanes per edge sum
-    // edge-sum scratch: the tile's pad column (RS = CW + 1; cp.async never
-    // writes it, the Hadamard never reads it) when it is long enough -- keeps
-    // the CTA inside the 3-per-SM shared-memory budget
-    const bool padred = nr * FE <= R1;
-    const int r2s = padred ? RS : 1;
-    double* red2 = padred ? T + CW : red + (NT / 32) * 2 * NU;
+    double* red2 = red + (NT / 32) * 2 * NU;  // [nr][FE]
     for (int idx = tid; has_edge && idx < nr * FE; idx += NT) {
         const int f = idx % FE, r = idx / FE;
         const double* e0 = p.epw + (long long)v * p.nslot * FE + f;
@@ -2622,7 +2604,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
             a3 += e0[(sl + 3 * nr) * FE];
         }
         for (; sl < p.nslot; sl += nr) a0 += e0[sl * FE];
-        red2[(r * FE + f) * r2s] = (a0 + a1) + (a2 + a3);
+        red2[r * FE + f] = (a0 + a1) + (a2 + a3);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -2634,7 +2616,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
     }
     for (int f = tid; has_edge && f < FE; f += NT) {
         double acc = 0.0;
-        for (int r = 0; r < nr; ++r) acc += red2[(r * FE + f) * r2s];
+        for (int r = 0; r < nr; ++r) acc += red2[r * FE + f];
         Wv[f] = acc;
     }
     __syncthreads();
