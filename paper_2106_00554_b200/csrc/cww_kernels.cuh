@@ -2520,19 +2520,16 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
         }
     }
     tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
-    // physical row ph of sub-tile ng is logical K_hi = bitrev_kh(ph)
+    // physical row ph of sub-tile ng is logical K_hi = bitrev_kh(ph); one warp
+    // per row, lane = column
     double* g = p.G + (long long)v * A * CW;
-    int e = tid % CW, rest = tid / CW;  // (f % CW, f / CW), stepped without division
-    for (int f = tid; f < NG * R2 * CW; f += NT) {
-        const int ng = rest & (NG - 1), khi = rest >> lng;  // NG = 2^lng
-        const int ph = (int)brev_bits((unsigned)khi, kh);
-        g[((long long)khi * R1 + rho0 + ng) * CW + e] = T[ng * tst + ph * RS + e];
-        e += NT % CW;
-        rest += NT / CW;
-        if (e >= CW) {
-            e -= CW;
-            ++rest;
-        }
+    const int lane2 = tid & 31;
+    for (int rr = tid >> 5; rr < NG * R2; rr += NT / 32) {
+        const int ng = rr & (NG - 1), khi = rr >> lng;  // NG = 2^lng
+        const double* t = T + ng * tst + (int)brev_bits((unsigned)khi, kh) * RS;
+        double* gr = g + ((long long)khi * R1 + rho0 + ng) * CW;
+        gr[lane2] = t[lane2];
+        if (lane2 < CW - 32) gr[32 + lane2] = t[32 + lane2];
     }
 }
 
