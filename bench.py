@@ -8,9 +8,10 @@ metric : forward+adjoint matvecs/s (a matvec = one U W^-1 or one W U* applicatio
 step   : config 1-4: one forward of the whole batch + one adjoint of the whole
          batch (2*batch matvecs; independent, so on two streams); config 5: 50
          iterations of the normal operator U*U on the image (100 matvecs).
-         Default config: 2 (BASELINE configs[1]).  On one GPU the step is captured
-         once into a CUDA graph and replayed (same launches, no per-launch host
-         overhead; eager fallback if capture or a bitwise replay check fails).
+         Default config: 2 (BASELINE configs[1]).  The step is captured once into
+         a CUDA graph per rank and replayed (same launches, no per-launch host
+         overhead; eager fallback if capture or a bitwise replay check fails;
+         config 5 on P > 1 GPUs, whose step holds NCCL all-to-alls, stays eager).
 value  : whole-job throughput, inputs resident in HBM, device-timed with CUDA
          events per step, L2 flushed (256 MiB write) between steps, max over ranks.
 e2e    : the same metric through the public API with the step's inputs copied
@@ -406,7 +407,7 @@ def main():
         configs lose their per-launch host overhead); falls back to eager calls
         when capture fails or a replay does not reproduce the eager outputs bit
         for bit.  Returns (callable, kernel launches per step or None)."""
-        if os.environ.get("CWW_BENCH_GRAPH", "1") != "1" or world > 1:
+        if os.environ.get("CWW_BENCH_GRAPH", "1") != "1":
             return fn, None
         try:
             fn()
