@@ -147,7 +147,25 @@ __device__ __forceinline__ void tile_hadamard_pass(double* T, int V, int a, int 
 }
 
 // H_A restricted to row bits [lo, hi), passes of <= MAXR bits (registers:
-// 2^MAXR doubles per thread), __syncthreads after each.
+// 2^MAXR doubles per thread), __syncthreads after each.  Inlined variant
+// (no call frame) for kernels whose register budget is tight.
+template <int CW, int RS, int MAXR = 5>
+__device__ __forceinline__ void tile_hadamard_inl(double* T, int V, int a, int lo, int hi, int tstride,
+                                                  int tid, int nt) {
+    while (lo < hi) {
+        const int r = hi - lo < MAXR ? hi - lo : MAXR;
+        switch (r) {
+            case 1: tile_hadamard_pass<1, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            case 2: tile_hadamard_pass<2, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            case 3: tile_hadamard_pass<3, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            case 4: tile_hadamard_pass<4, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+            default: tile_hadamard_pass<5, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
+        }
+        __syncthreads();
+        lo += r;
+    }
+}
+
 template <int CW, int RS, int MAXR = 5>
 __device__ __noinline__ void tile_hadamard(double* T, int V, int a, int lo, int hi, int tstride,
                                            int tid, int nt) {

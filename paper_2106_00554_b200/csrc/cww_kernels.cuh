@@ -2246,7 +2246,7 @@ __global__ void __launch_bounds__(RNT, 3) k_normal_rows_x(NormArgs p) {
 // pass 1 output) and physical row rho = bitrev_kl(N_lo).
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 3) k_large_fwd1(LargeArgs p) {  // 3: the tile caps residency at 3 anyway
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
@@ -2299,7 +2299,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_fwd1(LargeArgs p) {
         }
         __syncthreads();
     }
-    tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
+    tile_hadamard_inl<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
     {  // tile == G block: 16-byte copy
         static_assert(CW % 2 == 0, "16-byte G stores");
@@ -2534,7 +2534,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 }
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
+__global__ void __launch_bounds__(NT, 3) k_large_adj1(LargeArgs p) {  // (64 registers spilled)
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
@@ -2617,7 +2617,7 @@ __global__ void __launch_bounds__(NT, 4) k_large_adj1(LargeArgs p) {
         Wv[f] = acc;
     }
     __syncthreads();
-    tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
+    tile_hadamard_inl<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
     double* xo = p.xo + (long long)v * p.xo_vs;
     double* ob = p.out + p.lout.vbase(p.v0 + v);
     static_assert(B == 32, "one tile row per warp");
