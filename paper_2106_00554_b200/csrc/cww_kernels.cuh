@@ -32,6 +32,11 @@ namespace cww {
 constexpr int kSmallNT = 256;  // threads per small-path CTA (2 CTAs per SM)
 constexpr int kNc = 64;        // dense coarse wavelet block (levels r0+1..6)
 constexpr int kWarpLev = 8;  // wavelet levels of <= 256 samples run warp-private
+#ifndef CWW_CONTIG_MINB
+#define CWW_CONTIG_MINB 3  // large contiguous passes: CTAs per SM (the 76 KB tile allows 3;
+                           // 4 forced 64 registers with spills; 2: cfg3 adj1 0.335 vs 0.354 ms
+                           // but fwd1 and every config-2 launch slower)
+#endif
 
 // Optional per-phase cycle stamps (build with -DCWW_PHASE_TIMING): thread 0 of
 // each CTA records clock64() at phase boundaries into cww_phase_buf.
@@ -2246,7 +2251,7 @@ __global__ void __launch_bounds__(RNT, 3) k_normal_rows_x(NormArgs p) {
 // pass 1 output) and physical row rho = bitrev_kl(N_lo).
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT, 3) k_large_fwd1(LargeArgs p) {  // 3: the tile caps residency at 3 anyway
+__global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p) {
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
@@ -2534,7 +2539,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 }
 
 template <int NU, int NT>
-__global__ void __launch_bounds__(NT, 3) k_large_adj1(LargeArgs p) {  // (64 registers spilled)
+__global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p) {
     pdl_trigger();  // let the next launch in the stream get resident during our tail
     pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
