@@ -152,15 +152,15 @@ __device__ __forceinline__ void tile_hadamard_pass(double* T, int V, int a, int 
 template <int CW, int RS, int MAXR = 5>
 __device__ __forceinline__ void tile_hadamard_inl(double* T, int V, int a, int lo, int hi, int tstride,
                                                   int tid, int nt) {
+    static_assert(MAXR >= 1 && MAXR <= 5, "pass width");
     while (lo < hi) {
         const int r = hi - lo < MAXR ? hi - lo : MAXR;
-        switch (r) {
-            case 1: tile_hadamard_pass<1, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
-            case 2: tile_hadamard_pass<2, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
-            case 3: tile_hadamard_pass<3, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
-            case 4: tile_hadamard_pass<4, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
-            default: tile_hadamard_pass<5, CW, RS>(T, V, a, lo, tstride, tid, nt); break;
-        }
+        // only passes of <= MAXR bits are instantiated (register budget)
+        if (r == 1) tile_hadamard_pass<1, CW, RS>(T, V, a, lo, tstride, tid, nt);
+        else if (MAXR >= 2 && r == 2) tile_hadamard_pass<(MAXR >= 2 ? 2 : 1), CW, RS>(T, V, a, lo, tstride, tid, nt);
+        else if (MAXR >= 3 && r == 3) tile_hadamard_pass<(MAXR >= 3 ? 3 : 1), CW, RS>(T, V, a, lo, tstride, tid, nt);
+        else if (MAXR >= 4 && r == 4) tile_hadamard_pass<(MAXR >= 4 ? 4 : 1), CW, RS>(T, V, a, lo, tstride, tid, nt);
+        else tile_hadamard_pass<MAXR, CW, RS>(T, V, a, lo, tstride, tid, nt);
         __syncthreads();
         lo += r;
     }

@@ -32,6 +32,9 @@ namespace cww {
 constexpr int kSmallNT = 256;  // threads per small-path CTA (2 CTAs per SM)
 constexpr int kNc = 64;        // dense coarse wavelet block (levels r0+1..6)
 constexpr int kWarpLev = 8;  // wavelet levels of <= 256 samples run warp-private
+#ifndef CWW_CONTIG_MAXR
+#define CWW_CONTIG_MAXR 4  // large contiguous passes: widest in-register Hadamard pass (bits)
+#endif
 #ifndef CWW_CONTIG_MINB
 #define CWW_CONTIG_MINB 3  // large contiguous passes: CTAs per SM (the 76 KB tile allows 3;
                            // 4 forced 64 registers with spills; 2: cfg3 adj1 0.335 vs 0.354 ms
@@ -2304,7 +2307,7 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p)
         }
         __syncthreads();
     }
-    tile_hadamard_inl<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
+    tile_hadamard_inl<CW, RS, CWW_CONTIG_MAXR>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
     {  // tile == G block: 16-byte copy
         static_assert(CW % 2 == 0, "16-byte G stores");
@@ -2622,7 +2625,7 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
         Wv[f] = acc;
     }
     __syncthreads();
-    tile_hadamard_inl<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, NT);
+    tile_hadamard_inl<CW, RS, CWW_CONTIG_MAXR>(T, 1, kl, 0, kl, 0, tid, NT);
     double* xo = p.xo + (long long)v * p.xo_vs;
     double* ob = p.out + p.lout.vbase(p.v0 + v);
     static_assert(B == 32, "one tile row per warp");
