@@ -1172,6 +1172,7 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
         y.cb = cb;
         y.tail = tail ? 1 : 0;
         y.wmax = cww::pyr_wmax_ana(nu, T, bot, cb, op->vmp != 0, &y.wmax2) + 1;  // +1: 16-byte phase shift
+        y.wmax2 += 1;
         y.src = src;
         y.src_vs = M;
         y.y = out;

@@ -1423,31 +1423,56 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
         }
     }
     __syncthreads();
+    // Every window is stored so that sample 2mm - nu + 1 of each row mm sits at a
+    // 16-byte boundary: the 2nu-tap rows then read nu double2 pairs (half the
+    // shared-memory wavefronts of 2nu scalar loads at a 16-byte lane stride).
+    // (slack: +1 in both slots)
+    auto pair_al = [&](double* base, int x0) {  // shifted slot start for a window from x0
+        const int par = (int)((reinterpret_cast<uintptr_t>(base) >> 3) & 1);
+        return ((par + 1 - NU - x0) & 1) ? base + 1 : base;
+    };
+    double* const S0 = X;  // slot bases (unshifted)
+    double* const S1 = Y;
     {
         const double* src = p.src + v * p.src_vs;
         const int lo = xlo[p.top], w = xhi[p.top] - lo, n = 1 << p.top;
-        if (vmp) {  // window start shifted to the source's 16-byte phase (host slack: +1 in slot 0)
-            if ((reinterpret_cast<uintptr_t>(X) ^ reinterpret_cast<uintptr_t>(src + lo)) & 8) ++X;
-            warp_copy_span(X, src + lo, w, lane);
-        } else {
+        X = pair_al(S0, lo);
+        if (vmp) warp_copy_span(X, src + lo, w, lane);  // 16-byte copies when the phases agree
+        else
             for (int t = lane; t < w; t += 32) cp_async8(X + t, src + ((lo + t) & (n - 1)));
-        }
     }
     cp_async_wait_all();
     __syncwarp();
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
     double* yb = p.y + p.ly.vbase(p.yv0 + v);  // large path: contiguous 1D output
+    bool xin0 = true;  // X lives in slot 0
     for (int s = p.top; s > p.bot; --s) {
         const int n = 1 << s, half = n >> 1;
         const int lo = rlo[s], hi = rhi[s];
         const int plo = c << (s - 1 - lnc), phi = (c + 1) << (s - 1 - lnc);
         const double* xv = X - xlo[s];
+        Y = pair_al(xin0 ? S1 : S0, lo);  // the next step reads rows [lo, hi) as its window
         double* yv = Y - lo;
         const bool last = s == p.bot + 1;
         for (int mm = lo + lane; mm < hi; mm += 32) {
             double c0, d0;
-            dwt_pair_log<NU>(F, tp, xv, n, mm, vmp, c0, d0);
+            if (!vmp || (mm >= NU && mm < half - NU)) {  // interior: nu aligned pairs
+                const double2* xp = reinterpret_cast<const double2*>(xv + 2 * mm - NU + 1);
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < NU; ++k) {
+                    const double2 pr = xp[k];  // u = 2k - nu + 1 (.x) and u + 1 (.y)
+                    a0 = fma(tp.h[2 * k], pr.x, a0);
+                    b0 = fma(tp.g[2 * k], pr.x, b0);
+                    a1 = fma(tp.h[2 * k + 1], pr.y, a1);
+                    b1 = fma(tp.g[2 * k + 1], pr.y, b1);
+                }
+                c0 = a0 + a1;
+                d0 = b0 + b1;
+            } else {
+                dwt_pair_log<NU>(F, tp, xv, n, mm, vmp, c0, d0);
+            }
             if (!last) yv[mm] = c0;
             if (mm >= plo && mm < phi) {
                 yb[half + mm] = d0;
@@ -1458,9 +1483,8 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
             }
         }
         __syncwarp();
-        double* t0 = X;
         X = Y;
-        Y = t0;
+        xin0 = !xin0;
     }
     if (p.tail) dwt_coarse_tail<NU>(p, F, sm + FS, v, tid, blockDim.x);
 }
