@@ -524,39 +524,6 @@ __device__ __forceinline__ void dwt_pair(const FiltSmem<NU>& F, const double* x,
     d = b0 + b1;
 }
 
-// Two adjacent interior analysis rows mm, mm + 1 (VMP interior or in-range
-// periodic indices) from one window of 2nu + 2 fine samples x[2mm-nu+1 ..].
-template <int NU>
-__device__ __forceinline__ void dwt_quad_inner(const Taps<NU>& tp, const double* x, int mm, double& c0,
-                                               double& d0, double& c1, double& d1) {
-    constexpr int WN = 2 * NU + 2;
-    double xw[WN];
-#pragma unroll
-    for (int w = 0; w < WN; ++w) xw[w] = x[2 * mm - NU + 1 + w];
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-#pragma unroll
-        for (int u = -NU + 1; u <= NU; ++u) {
-            const double xv = xw[2 * p + u + NU - 1];
-            if (u & 1) {
-                a1 = fma(tp.h[u + NU - 1], xv, a1);
-                b1 = fma(tp.g[u + NU - 1], xv, b1);
-            } else {
-                a0 = fma(tp.h[u + NU - 1], xv, a0);
-                b0 = fma(tp.g[u + NU - 1], xv, b0);
-            }
-        }
-        if (p == 0) {
-            c0 = a0 + a1;
-            d0 = b0 + b1;
-        } else {
-            c1 = a0 + a1;
-            d1 = b0 + b1;
-        }
-    }
-}
-
 // Programmatic dependent launch (PDL): every kernel triggers its dependents
 // at entry and waits for its predecessor's results before touching memory;
 // both are no-ops when the launch did not use the PDL attribute.

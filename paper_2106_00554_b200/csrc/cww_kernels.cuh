@@ -408,6 +408,7 @@ inline long long small_smem_bytes(int V, int j, int q, bool adj, bool vf) {
     }
     d += (long long)V << j;          // X
     d += (long long)V << (j > 0 ? j - 1 : 0);  // C (final-level coarse input / DWT ping)
+    if (adj) d += 3;                 // 16-byte phase slack of X and C, and T after C (k_small_adj)
     d += (long long)V * small_tile_stride(A * G::RS, V);  // tiles (also wavelet ping-pong / output staging)
     return d * 8;
 }
@@ -655,9 +656,15 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
     const double* KAP = KE;
     const double* EM = KE + (2 * NU - 1) * S;
     double* EPW = W + V * S * 2 * NP;         // [V][nslot][S][2NP]
-    double* X = EPW + V * nslot * S * 2 * NP;
-    double* C = X + V * M;
-    double* T = C + (V * M >> 1);
+    // X and C (the analysis ping-pong) start at the 8-byte phase that puts each
+    // analysis row's first tap 2mm - nu + 1 on a 16-byte boundary (double2 tap
+    // pairs); one slack double each (small_smem_bytes)
+    auto pair_al = [](double* q) {
+        return q + ((((reinterpret_cast<uintptr_t>(q) >> 3) & 1) + 1 - NU) & 1);
+    };
+    double* X = pair_al(EPW + V * nslot * S * 2 * NP);
+    double* C = pair_al(X + V * M);
+    double* T = C + (V * M >> 1) + 1;
     const int tst = small_tile_stride(A * RS, V);
     const int hM = M >> 1;
     const int Gs = NT / V, gid = tid / Gs, gt = tid % Gs;
@@ -795,23 +802,27 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
             const bool last = lev == p.r0 + 1;
             double* dst = last ? ov : ((t & 1) ? xv : cv);  // coarse rows ping-pong C <-> X
             const double* s2 = src;
-            if (NU > 1 && vmp_ && half >= 2 * NU + 2) {  // (VMP needs nu >= 2: no code for Haar)
-                // interior rows [NU, half - NU) two per thread (shared window), then
-                // the odd leftover and the 2 NU edge rows on the last threads
+            if (NU > 1 && vmp_ && half >= 2 * NU + 2 && (s2 == xv || s2 == cv)) {  // (no code for Haar)
+                // interior rows [NU, half - NU): nu aligned double2 tap pairs per row
+                // (s2 + 2mm - nu + 1 is 16-byte aligned: pair_al above); then the
+                // 2 NU edge rows on the last threads
                 const Taps<NU> tp(F);
-                const int nq = (half - 2 * NU) >> 1;
-                for (int qi = gt; qi < nq; qi += Gs) {
-                    const int mm = NU + 2 * qi;
-                    double c0, d0, c1, d1;
-                    dwt_quad_inner<NU>(tp, s2, mm, c0, d0, c1, d1);
-                    ov[half + mm] = d0;
-                    ov[half + mm + 1] = d1;
-                    dst[mm] = c0;
-                    dst[mm + 1] = c1;
+                for (int mm = NU + gt; mm < half - NU; mm += Gs) {
+                    const double2* xp = reinterpret_cast<const double2*>(s2 + 2 * mm - NU + 1);
+                    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                    for (int k = 0; k < NU; ++k) {
+                        const double2 pr = xp[k];
+                        a0 = fma(tp.h[2 * k], pr.x, a0);
+                        b0 = fma(tp.g[2 * k], pr.x, b0);
+                        a1 = fma(tp.h[2 * k + 1], pr.y, a1);
+                        b1 = fma(tp.g[2 * k + 1], pr.y, b1);
+                    }
+                    ov[half + mm] = b0 + b1;
+                    dst[mm] = a0 + a1;
                 }
-                const int odd = (half - 2 * NU) & 1;
-                for (int k2 = Gs - 1 - gt; k2 < 2 * NU + odd; k2 += Gs) {
-                    const int mm = k2 < NU ? k2 : (k2 < 2 * NU ? half - 2 * NU + k2 : half - NU - 1);
+                for (int k2 = Gs - 1 - gt; k2 < 2 * NU; k2 += Gs) {
+                    const int mm = k2 < NU ? k2 : half - 2 * NU + k2;
                     double c, d;
                     dwt_pair<NU>(F, s2, n, mm, true, c, d);
                     ov[half + mm] = d;
