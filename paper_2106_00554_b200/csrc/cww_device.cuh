@@ -443,12 +443,30 @@ __device__ __forceinline__ void idwt_quad_inner(const Taps<NU>& tp, const double
                                                 int n, int m, bool vmp, double* o) {
     constexpr int OFF = (NU + 1) / 2;
     const int half = n >> 1;
-    double cw[NU + 2], dw[NU + 2];
+    constexpr int NW = (NU + 3) / 2;  // double2 pairs covering the nu + 2 window
+    double cw[2 * NW], dw[2 * NW];
+    const double* c0 = cv + (m - OFF);
+    const double* d0 = dv + (m - OFF);
+    if (vmp && ((reinterpret_cast<uintptr_t>(c0) | reinterpret_cast<uintptr_t>(d0)) & 15) == 0) {
+        // 16-byte aligned windows (lanes 2 pairs apart): half the shared-memory
+        // wavefronts of the scalar loads (the extra sample of an odd window stays
+        // inside the level: m + 2 + nu - OFF < half for interior quads)
 #pragma unroll
-    for (int k = 0; k <= NU + 1; ++k) {
-        const int idx = vmp ? m - OFF + k : ((m - OFF + k) & (half - 1));
-        cw[k] = cv[idx];
-        dw[k] = dv[idx];
+        for (int k = 0; k < NW; ++k) {
+            const double2 a = reinterpret_cast<const double2*>(c0)[k];
+            const double2 b = reinterpret_cast<const double2*>(d0)[k];
+            cw[2 * k] = a.x;
+            cw[2 * k + 1] = a.y;
+            dw[2 * k] = b.x;
+            dw[2 * k + 1] = b.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k <= NU + 1; ++k) {
+            const int idx = vmp ? m - OFF + k : ((m - OFF + k) & (half - 1));
+            cw[k] = cv[idx];
+            dw[k] = dv[idx];
+        }
     }
 #pragma unroll
     for (int p = 0; p < 2; ++p) {  // pair m + p: window shifted by p

@@ -408,7 +408,7 @@ inline long long small_smem_bytes(int V, int j, int q, bool adj, bool vf) {
     }
     d += (long long)V << j;          // X
     d += (long long)V << (j > 0 ? j - 1 : 0);  // C (final-level coarse input / DWT ping)
-    if (adj) d += 3;                 // 16-byte phase slack of X and C, and T after C (k_small_adj)
+    d += 3;                          // 16-byte phase slack of X, C and the tiles
     d += (long long)V * small_tile_stride(A * G::RS, V);  // tiles (also wavelet ping-pong / output staging)
     return d * 8;
 }
@@ -438,9 +438,12 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
     double* KE = filt + FiltSmem<NU>::SIZE;  // kap | em
     double* EV = KE + small_ke_size(NU, S);
     double* ES = EV + V * 2 * NU;
-    double* X = ES + V * S * 2 * NP;
-    double* C = X + V * M;
-    double* T = C + (V * M >> 1);
+    // 16-byte aligned X, C and tile bases: the synthesis quads then read their
+    // windows as double2 pairs (idwt_quad_inner); slack in small_smem_bytes
+    auto al2 = [](double* q) { return q + ((reinterpret_cast<uintptr_t>(q) >> 3) & 1); };
+    double* X = al2(ES + V * S * 2 * NP);
+    double* C = al2(X + V * M);
+    double* T = al2(C + (V * M >> 1));
     const int tst = small_tile_stride(A * RS, V);
     const int hM = M >> 1;
     const double* KAP = KE;
