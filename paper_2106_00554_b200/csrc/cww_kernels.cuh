@@ -1379,15 +1379,34 @@ __device__ __forceinline__ void dwt_coarse_tail(const PyrArgs& p, const FiltSmem
     const bool vmp = p.vmp != 0;
     double* yb = p.y + p.ly.vbase(p.yv0 + v);
     const int n0 = 1 << p.bot;
+    // both ping-pong halves at the phase that puts tap 2k - nu + 1 on a 16-byte
+    // boundary: interior rows read nu double2 pairs (host slack: 2 doubles)
+    buf += (((reinterpret_cast<uintptr_t>(buf) >> 3) & 1) + 1 - NU) & 1;
     double* cur = buf;
     double* nxt = buf + n0;
     for (int i = tid; i < n0; i += nt) cur[i] = __ldcg(p.cws + v * p.cws_vs + i);
     __syncthreads();
+    const Taps<NU> tp(F);
     for (int lev = p.bot; lev > p.r0; --lev) {
         const int m = 1 << lev, half = m >> 1;
         for (int k = tid; k < half; k += nt) {
             double cc, dd;
-            dwt_pair<NU>(F, cur, m, k, vmp, cc, dd);
+            if (NU > 1 && vmp && k >= NU && k < half - NU) {
+                const double2* xp = reinterpret_cast<const double2*>(cur + 2 * k - NU + 1);
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < NU; ++q) {
+                    const double2 pr = xp[q];
+                    a0 = fma(tp.h[2 * q], pr.x, a0);
+                    b0 = fma(tp.g[2 * q], pr.x, b0);
+                    a1 = fma(tp.h[2 * q + 1], pr.y, a1);
+                    b1 = fma(tp.g[2 * q + 1], pr.y, b1);
+                }
+                cc = a0 + a1;
+                dd = b0 + b1;
+            } else {
+                dwt_pair<NU>(F, cur, m, k, vmp, cc, dd);
+            }
             yb[half + k] = dd;
             nxt[k] = cc;
         }

@@ -111,7 +111,7 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
     const dim3 grid((unsigned)(nchunk / nw), (unsigned)a.nvec);
     if (analysis) {
         long long nb = (long long)nw * (64ll + a.wmax + a.wmax2);
-        if (a.tail && nb < (2ll << a.bot)) nb = 2ll << a.bot;
+        if (a.tail && nb < (2ll << a.bot) + 2) nb = (2ll << a.bot) + 2;  // + 16-byte phase slack
         const long long smem = (FS + nb) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_dwt_wpyr<CWW_NU>;
