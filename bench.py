@@ -349,7 +349,7 @@ def main():
             op.forward(x_dev, fo_dev)
             op.adjoint(y_dev, ao_dev)
 
-    s_fwd, s_adj = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_fwd, s_adj = torch.cuda.Stream(dev, priority=pf), torch.cuda.Stream(dev, priority=pa)
 
     def step_e2e():
         if not (rowpart or is5):
