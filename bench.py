@@ -8,27 +8,35 @@ metric : forward+adjoint matvecs/s (a matvec = one U W^-1 or one W U* applicatio
 step   : config 1-4: one forward of the whole batch + one adjoint of the whole
          batch (2*batch matvecs; independent, so on two streams); config 5: 50
          iterations of the normal operator U*U on the image (100 matvecs).
-         Default config: 2 (BASELINE configs[1]).  The step is captured once into
-         a CUDA graph per rank and replayed (same launches, no per-launch host
-         overhead; eager fallback if capture or a bitwise replay check fails;
-         config 5 on P > 1 GPUs, whose step holds NCCL all-to-alls, stays eager).
+         Default config: 3 (M = 2^21, N = 2^23, batch 32: the north_star's
+         2^23-length target and the largest 1D configuration).  The step is
+         captured once into a CUDA graph per rank and replayed (eager fallback if
+         capture or a bitwise replay check fails).
+inputs : seeded synthetic data of SURVEY.md 8d (test_rng): vector b of config c
+         has seed 1000c + b (forward input) and 1000c + 500 + b (adjoint input,
+         N(0,1)); the same generator and seeds feed --impl reference.
 value  : whole-job throughput, inputs resident in HBM, device-timed with CUDA
          events per step, L2 flushed (256 MiB write) between steps, max over ranks.
 e2e    : the same metric through the public API with the step's inputs copied
          from pinned host memory and the results copied back, inside the timed
          region.
-roofline: dominant kernel (largest device time), algorithmic bytes
-          / its CUDA-event time, vs MEASURED_PEAKS.json.
+roofline: dominant kernel (largest device time); its algorithmic bytes are its
+         share of the path's SURVEY 8(d) bytes (8(M+N) per 1D matvec, 8(M^2+N^2)
+         per 2D matvec): only the path's own inputs and outputs it reads or
+         writes, intermediates excluded.  Peak from MEASURED_PEAKS.json.
 cpu_baseline: the reference library itself (oracle/_ref, built from
          /root/reference) on the host cores, rank 0 at N = 1, bounded sample.
-Multi-GPU: one process per GPU (torchrun); independent batches per rank,
-         no data-path collective ("scaling": "weak").
+Multi-GPU: one process per GPU (torchrun).  Configs 2-4: the fixed global batch
+         is sharded across ranks (dist.shard_batch, no data-path collective,
+         "scaling": "strong" -- the total work is fixed).  Config 1: independent
+         replicas ("weak").  Config 5: rows partitioned, NCCL all-to-all
+         transposes ("strong").
 """
 from __future__ import annotations
 
 import argparse
+import glob
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -39,7 +47,7 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-# (family, nu, boundary, j, q, dim, r0, batch, input kind, density, workload name)
+# (family, nu, boundary, j, q, dim, r0, global batch, input kind, density, workload name)
 CONFIGS = {
     1: (0, 1, 0, 10, 1, 1, 1, 1, 0, 1.0, "cfg1: 1D Haar r0=1 M=2^10 q=1, single vector"),
     2: (0, 4, 1, 16, 2, 1, 4, 64, 1, 1.0, "cfg2: 1D db4 boundary-VMP r0=4 M=2^16 q=2 (N=2^18), batch 64, level-decaying coeffs"),
@@ -47,6 +55,7 @@ CONFIGS = {
     4: (0, 4, 1, 10, 1, 2, 4, 16, 1, 0.05, "cfg4: 2D db4 boundary-VMP r0=4 M=1024^2 q=1 (N=2048^2), batch 16, 5% nonzeros"),
     5: (0, 2, 1, 12, 1, 2, 3, 1, 0, 0.02, "cfg5: 2D db2 boundary-VMP r0=3 M=4096^2 q=1 (N=8192^2), 50 U*U iterations, 2% nonzeros"),
 }
+DEFAULT_CONFIG = 3
 CFG5_ITERS = 50
 
 
@@ -56,6 +65,62 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def shard(config_id: int, world: int, rank: int):
+    """(first global item, items on this rank) -- configs 2-4 shard the fixed
+    global batch (dist.shard_batch); config 1 runs one replica per rank and
+    config 5 has one (row-partitioned) image."""
+    cfg = CONFIGS[config_id]
+    batch = cfg[7]
+    if config_id in (2, 3, 4) and world > 1:
+        base, rem = divmod(batch, world)
+        return rank * base + min(rank, rem), base + (1 if rank < rem else 0)
+    return 0, batch
+
+
+def scaling_kind(config_id: int, world: int) -> str:
+    return "weak" if config_id == 1 else "strong"
+
+
+def config_dict(config_id: int, world: int) -> dict:
+    """The `config` object of the JSON line; identical for both arms."""
+    fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = CONFIGS[config_id]
+    if config_id == 5:
+        step = (f"{CFG5_ITERS} x U*U on the image (cww_normal: banded normal form W G W^-1 per axis, "
+                "G = U*U exactly banded since H^T H = M I)")
+        par = f"rows/{world} + all-to-all transposes" if world > 1 else "1 GPU"
+    else:
+        step = "forward + adjoint of the batch"
+        par = (f"{world} independent replicas" if config_id == 1 and world > 1
+               else (f"batch sharded {batch}/{world} per GPU (dp{world}, no collective)" if world > 1 else "1 GPU"))
+    per = shard(config_id, world, 0)[1]
+    return {"workload": name, "global_batch": batch, "batch_per_gpu": per, "step": step,
+            "l2": "flushed (256 MiB write) between timed steps", "parallelism": par,
+            "inputs": "seeded test_rng (seed 1000c+b; adjoint input 1000c+500+b)"}
+
+
+def make_inputs(synth, config_id: int, start: int, count: int):
+    """Forward inputs (wavelet coefficients) and adjoint inputs (N(0,1) Walsh
+    samples) of global items start..start+count-1; `synth` is the product's or
+    the oracle's test_rng generator (bit-identical, tests/test_oracle.py)."""
+    import numpy as np
+    fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = CONFIGS[config_id]
+    xs = np.stack([synth(kind, 1000 * config_id + b, j, r0, dens, dim) for b in range(start, start + count)])
+    if config_id == 5:
+        return xs, None
+    ys = np.stack([synth(0, 1000 * config_id + 500 + b, j + q, r0, 1.0, dim) for b in range(start, start + count)])
+    return xs, ys
 
 
 class Clocks:
@@ -115,140 +180,161 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(cfg, kernel: str, batch: int) -> float:
-    """Minimal DRAM bytes of one step's launches of `kernel`."""
+def path_bytes(cfg) -> int:
+    """SURVEY 8(d) algorithmic bytes of one matvec: 8(M+N) (1D), 8(M^2+N^2) (2D)."""
+    j, q, dim = cfg[3], cfg[4], cfg[5]
+    M, N = 1 << j, 1 << (j + q)
+    return 8 * ((M + N) if dim == 1 else (M * M + N * N))
+
+
+def algorithmic_bytes(cfg, kernel: str, nvec: int) -> float:
+    """The SURVEY 8(d) bytes that one step's launches of `kernel` account for:
+    the path's inputs it reads and the path's outputs it writes (each once);
+    intermediates (xi, the Hadamard intermediate G, the 2D row-pass T) are
+    excluded.  nvec = vectors (1D) / images (2D) of the step per direction."""
     fam, nu, bnd, j, q, dim, r0 = cfg[:7]
     M, N = 1 << j, 1 << (j + q)
     if kernel in ("normal_rows", "transpose"):
-        # banded normal form (config 5): every launch reads and writes each
-        # M-row once; per U*U: 2 row passes + 1 transpose over the M x M image
+        # banded normal form (config 5): no Walsh-domain output exists; every
+        # launch reads and writes the M x M image once (actual bytes, labelled)
         per_iter = 2 if kernel == "normal_rows" else 1
         iters = CFG5_ITERS if cfg is CONFIGS[5] else 1
-        return 16.0 * batch * (M * M if dim == 2 else M) * per_iter * iters
+        return 16.0 * nvec * M * M * per_iter * iters
     if dim == 2:
-        mats = CFG5_ITERS if cfg is CONFIGS[5] else 1
-        # small_fwd: row pass (M^2 -> MN) + column pass (MN -> N^2); small_adj mirrored
-        return 8.0 * batch * mats * (M * M + 2 * M * N + N * N)
-    CW = 32 + 2 * (nu - 1)
-    A = M // 32
-    lc = min(j - 1, 10)  # coarse levels <= 10 run in k_wav_coarse / the analysis tail (CWW_PYR_SYN_BOT)
+        # small_fwd: row pass reads X (M^2), column pass writes Y (N^2); small_adj mirrored
+        return 8.0 * nvec * (M * M + N * N) if kernel in ("small_fwd", "small_adj") else 0.0
+    lc = min(j - 1, 10)  # coarse synthesis levels <= 10 run in k_wav_coarse
+    idwt = r0 < j
     per = {
         "small_fwd": M + N, "small_adj": M + N,
-        "large_fwd1": M + A * CW, "large_fwd1_syn": M + A * CW, "large_fwd2": A * CW + N,
-        "large_adj2": N + A * CW, "large_adj1": A * CW + M,
-        # all launches of a step together: every coefficient read once, every sample written once
-        "idwt_pyr": 2 * M, "dwt_pyr": 2 * M,
-        "wav_coarse": 2 * (1 << lc),
+        "wav_coarse": (1 << lc) if idwt else 0,
+        "idwt_pyr": M - (1 << lc),               # the detail coefficients above level lc
+        "large_fwd1": 0 if idwt else M, "large_fwd": N if idwt else M + N,
+        "large_fwd2": N,
+        "large_adj2": N, "large_adj": M if not idwt else N,
+        "large_adj1": 0 if idwt else M,
+        "dwt_pyr": M,                            # every coefficient written once
     }
-    return 8.0 * batch * per.get(kernel, 0)
+    return 8.0 * nvec * per.get(kernel, 0)
+
+
+def latest_traffic(config_id: int):
+    """ncu DRAM bytes per launch of this config's kernels from the newest
+    committed profiles/rNN_traffic.json that has the config."""
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+            ent = d.get(str(config_id))
+        except (OSError, ValueError):
+            continue
+        if ent:
+            return (ent if isinstance(ent, list) else [ent]), os.path.basename(path)
+    return [], None
+
+
+def _ref_op(cfg):
+    """The compiled reference (oracle/_ref) or, if it was not built, the C port."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    from oracle_py import Oracle, Reference
+    fam, nu, bnd, j, q, dim, r0 = cfg[:7]
+    try:
+        return Reference().op(fam, nu, bnd, j, q, dim, r0), "reference", Oracle()
+    except Exception:  # noqa: BLE001 -- reference not built: the C restatement
+        return None, "port", Oracle()
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference's own CPU implementation, all host threads."""
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    """--impl reference: the reference's own CPU implementation (oracle/_ref:
+    the unmodified proj/src/{walsh,wavelet,kernel,fastop}.cpp) on every host
+    thread, on the GPU arm's inputs, config and metric.  The product package
+    is never imported here."""
     import numpy as np
     fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = cfg
     threads = os.cpu_count() or 1
-    kind_s = "reference"
-    try:
-        from oracle_py import Reference
-        R = Reference()
-        op = R.op(fam, nu, bnd, j, q, dim, r0)
-    except Exception as e:  # noqa: BLE001 -- reference not built: the C restatement
-        from oracle_py import Oracle
-        kind_s = "port"
-        op = None
-        err = str(e)
-    # bounded sample per step: config 1-4 up to `threads` vectors/images, config 5: 1 iteration
-    if cfg is CONFIGS[5]:
-        sample, iters, matv = 1, 1, 2
-    else:
-        sample = min(batch, max(1, threads)) if dim == 1 else 1
-        iters, matv = 1, 2 * sample
-    from paper_2106_00554_b200 import synth  # input generator only (host, no GPU)
+    op, kind_s, orc = _ref_op(cfg)
+    world = args.gpus
+    xs, ys = make_inputs(orc.synth, args.config, 0, batch)
     M, N = 1 << j, 1 << (j + q)
     nin, nout = (M, N) if dim == 1 else (M * M, N * N)
-    xs = np.stack([synth(kind, 1000 * args.config + b, j, r0, dens, dim) for b in range(sample)])
-    rng = np.random.default_rng(args.config)
-    ys = rng.standard_normal((sample, nout))
-    outf = np.empty((sample, nout))
-    outa = np.empty((sample, nin))
+    outf = np.empty((batch, nout))
+    outa = np.empty((batch, nin))
+    if op is None:
+        oop = orc.op(fam, nu, bnd, j, q, dim, r0)
 
     def one_step():
-        if op is None:
-            raise RuntimeError("reference library unavailable: " + err)
-        if cfg is CONFIGS[5]:
-            t = op.bench(2, xs, outa, 1, threads, iters)
-        else:
-            t = op.bench(0, xs, outf, sample, threads)
-            t += op.bench(1, ys, outa, sample, threads)
-        return t
+        """The whole batch (configs 1-4); config 5: one U*U iteration of the 50."""
+        if op is None:  # scalar port, one thread
+            t0 = time.perf_counter()
+            if args.config == 5:
+                oop.adjoint(oop.forward(xs[0]))
+            else:
+                for b in range(batch):
+                    outf[b] = oop.forward(xs[b])
+                    outa[b] = oop.adjoint(ys[b])
+            return time.perf_counter() - t0
+        if args.config == 5:
+            return op.bench(2, xs, outa, 1, threads, 1)
+        return op.bench(0, xs, outf, batch, threads) + op.bench(1, ys, outa, batch, threads)
 
     for _ in range(args.warmup):
         one_step()
     ts = [one_step() for _ in range(args.steps)]
     total = sum(ts)
+    matv = 2 if args.config == 5 else 2 * batch
     value = matv * args.steps / total
+    sample = ("1 U*U iteration (2 matvecs) of the 50 per step; FastOp::set_threads"
+              if args.config == 5 else f"the full batch: {batch} x (forward + adjoint) per step, one std::thread per vector"
+              if dim == 1 else f"the full batch: {batch} x (forward + adjoint) per step, FastOp::set_threads")
     line = {
         "impl": "reference", "metric": "forward+adjoint matvecs/s", "value": value, "unit": "matvec/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": scaling_kind(args.config, world),
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded test_rng inputs, SURVEY.md 8d)",
-        "config": {"workload": name, "batch": batch, "sample_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": threads, "kind": kind_s,
-                         "sample": f"{sample} vector(s) forward + adjoint per step" if cfg is not CONFIGS[5]
-                         else "1 U*U iteration per step (of the 50-iteration config)"},
+        "config": config_dict(args.config, world),
+        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": threads if op is not None else 1,
+                         "kind": kind_s, "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
-def cpu_baseline(cfg, config_id):
-    """Reference CPU path on a bounded sample (rank 0, N = 1)."""
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
+def cpu_baseline(cfg, config_id, xs, ys):
+    """Reference CPU path on a bounded sample of this rank's inputs (rank 0, N = 1)."""
     import numpy as np
-    fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = cfg
+    fam, nu, bnd, j, q, dim, r0 = cfg[:7]
     threads = os.cpu_count() or 1
-    try:
-        from oracle_py import Reference
-        op = Reference().op(fam, nu, bnd, j, q, dim, r0)
-        kind_s = "reference"
-    except Exception:  # noqa: BLE001
-        from oracle_py import Oracle
-        op = None
-        kind_s = "port"
-    from paper_2106_00554_b200 import synth
+    op, kind_s, orc = _ref_op(cfg)
     M, N = 1 << j, 1 << (j + q)
     nin, nout = (M, N) if dim == 1 else (M * M, N * N)
-    if cfg is CONFIGS[5]:
-        sample = 1
-    else:
-        sample = min(batch, threads) if dim == 1 else 1
-    xs = np.stack([synth(kind, 1000 * config_id + b, j, r0, dens, dim) for b in range(sample)])
-    ys = np.random.default_rng(0).standard_normal((sample, nout))
+    sample = 1 if (config_id == 5 or dim == 2) else min(len(xs), threads)
+    xs = np.ascontiguousarray(xs[:sample])
+    ys = None if ys is None else np.ascontiguousarray(ys[:sample])
     outf, outa = np.empty((sample, nout)), np.empty((sample, nin))
     if op is None:
-        from oracle_py import Oracle
-        o = Oracle().op(fam, nu, bnd, j, q, dim, r0)
+        o = orc.op(fam, nu, bnd, j, q, dim, r0)
         t0 = time.perf_counter()
         for b in range(sample):
             o.forward(xs[b])
-            o.adjoint(ys[b])
+            if ys is not None:
+                o.adjoint(ys[b])
         t = time.perf_counter() - t0
-        return {"value": 2 * sample / t, "unit": "matvec/s", "cores": 1, "kind": "port",
-                "sample": f"{sample} vector(s) forward + adjoint"}
+        return {"value": (2 if ys is not None else 1) * sample / t, "unit": "matvec/s", "cores": 1,
+                "kind": "port", "cpu_model": cpu_model(), "sample": f"{sample} vector(s) forward + adjoint"}
     total, mv, reps = 0.0, 0, 0
     while total < 8.0 and reps < 50:
-        if cfg is CONFIGS[5]:
+        if config_id == 5:
             total += op.bench(2, xs, outa, 1, threads, 1)
             mv += 2
         else:
             total += op.bench(0, xs, outf, sample, threads) + op.bench(1, ys, outa, sample, threads)
             mv += 2 * sample
         reps += 1
-    return {"value": mv / total, "unit": "matvec/s", "cores": threads, "kind": kind_s,
+    return {"value": mv / total, "unit": "matvec/s", "cores": threads, "kind": kind_s, "cpu_model": cpu_model(),
             "sample": (f"{reps} x ({sample} vector(s) forward + adjoint), one std::thread per vector"
-                       if cfg is not CONFIGS[5] else f"{reps} U*U iteration(s), FastOp::set_threads({threads})"),
+                       if config_id != 5 and dim == 1 else
+                       f"{reps} x (1 image forward + adjoint), FastOp::set_threads({threads})" if config_id != 5
+                       else f"{reps} U*U iteration(s), FastOp::set_threads({threads})"),
             "seconds": total}
 
 
@@ -257,17 +343,18 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
-    fam, nu, bnd, j, q, dim, r0, batch, kind, dens, name = cfg
+    fam, nu, bnd, j, q, dim, r0, gbatch, kind, dens, name = cfg
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    args.gpus = max(args.gpus, world) if world > 1 else args.gpus
 
     if args.impl == "reference":
         if rank == 0:
@@ -297,13 +384,12 @@ def main():
     else:
         op = cw.ComposedOp(cw.FastOp(spec, j, q, dim), None, True, r0)
     nin, nout = op.cols(), op.rows()
-    # per-rank inputs (weak scaling: each rank owns a full batch)
-    xs = np.stack([cw.synth(kind, 1000 * args.config + rank * batch + b, j, r0, dens, dim)
-                   for b in range(batch)])
-    g = torch.Generator(device="cpu").manual_seed(1000 * args.config + 500 + rank)
-    ys = torch.randn((batch, nout), generator=g, dtype=torch.float64)
+    start, batch = shard(args.config, world, rank)
+    xs, ys = make_inputs(cw.synth, args.config, start, batch)
+    if ys is None:
+        ys = np.zeros((batch, nout))
     x_pin = torch.from_numpy(xs).pin_memory()
-    y_pin = ys.pin_memory()
+    y_pin = torch.from_numpy(ys).pin_memory()
     x_dev, y_dev = x_pin.to(dev), y_pin.to(dev)
     fo_dev = torch.empty((batch, nout), dtype=torch.float64, device=dev)
     ao_dev = torch.empty((batch, nin), dtype=torch.float64, device=dev)
@@ -316,26 +402,21 @@ def main():
         M_ = 1 << j
         mr = M_ // world
         x_rows0 = x_dev.view(M_, M_)[rank * mr:(rank + 1) * mr].contiguous()
+        x_rows = torch.empty_like(x_rows0)
 
     # forward and adjoint of the step are independent: two streams, so one chain's
-    # latency-bound launches overlap the other's (inside the replayed CUDA graph:
-    # cfg2 0.210 vs 0.240 ms sequential; eager launches measured no gain)
-    conc = os.environ.get("CWW_BENCH_CONCURRENT", "1") == "1"
-    # stream priorities (env CWW_BENCH_PRIO = f,a; lower = higher priority): the
-    # adjoint chain is the longer one, so it goes first and the forward fills the
-    # gaps (cfg2 0.1985 vs 0.2024 ms; the forward first: 0.225 ms)
-    pf, pa = (int(t) for t in os.environ.get("CWW_BENCH_PRIO", "0,-1").split(","))
-    s_dev_f, s_dev_a = torch.cuda.Stream(dev, priority=pf), torch.cuda.Stream(dev, priority=pa)
+    # latency-bound launches overlap the other's; the adjoint chain (the longer one)
+    # at the higher priority
+    s_dev_f, s_dev_a = torch.cuda.Stream(dev, priority=0), torch.cuda.Stream(dev, priority=-1)
 
-    def step_device(concurrent=conc):
+    def step_device(concurrent=True):
         if rowpart:
-            d2.normal(x_rows0, CFG5_ITERS)
+            x_rows.copy_(x_rows0)
+            d2.normal(x_rows, CFG5_ITERS)
         elif is5:
             ao_dev.copy_(x_dev)
             op.normal(ao_dev, iters=CFG5_ITERS, work=fo_dev)
         elif concurrent:
-            # forward and adjoint of the batch are independent: two streams, so one
-            # chain's latency-bound phases and launch tails overlap the other's
             cur = torch.cuda.current_stream(dev)  # (the capture stream inside a graph capture)
             s_dev_f.wait_stream(cur)
             s_dev_a.wait_stream(cur)
@@ -349,15 +430,14 @@ def main():
             op.forward(x_dev, fo_dev)
             op.adjoint(y_dev, ao_dev)
 
-    s_fwd, s_adj = torch.cuda.Stream(dev, priority=pf), torch.cuda.Stream(dev, priority=pa)
+    s_fwd, s_adj = torch.cuda.Stream(dev, priority=0), torch.cuda.Stream(dev, priority=-1)
 
     def step_e2e():
         if not (rowpart or is5):
             # the public host API on pinned buffers (cww_*_host_async): chunk-pipelined H2D /
             # compute / D2H; forward and adjoint are independent, so they run on two streams
-            # and the two PCIe directions overlap.  Tiny inputs (config 1) go zero-copy: the
-            # kernels read and write the pinned buffers over PCIe, no copy launches.
-            cur = torch.cuda.current_stream(dev)  # (the capture stream inside a graph capture)
+            # and the two PCIe directions overlap.  Tiny inputs (config 1) go zero-copy.
+            cur = torch.cuda.current_stream(dev)
             s_fwd.wait_stream(cur)
             s_adj.wait_stream(cur)
             with torch.cuda.stream(s_fwd):
@@ -369,17 +449,12 @@ def main():
             return
         x_dev.copy_(x_pin, non_blocking=True)
         if rowpart:
-            xr = d2.normal(x_dev.view(1 << j, 1 << j)[rank * mr:(rank + 1) * mr], CFG5_ITERS)
+            x_rows.copy_(x_dev.view(1 << j, 1 << j)[rank * mr:(rank + 1) * mr])
+            xr = d2.normal(x_rows, CFG5_ITERS)
             ao_pin.view(1 << j, 1 << j)[rank * mr:(rank + 1) * mr].copy_(xr, non_blocking=True)
-        elif is5:
+        else:
             ao_dev.copy_(x_dev)
             op.normal(ao_dev, iters=CFG5_ITERS, work=fo_dev)
-            ao_pin.copy_(ao_dev, non_blocking=True)
-        else:
-            y_dev.copy_(y_pin, non_blocking=True)
-            op.forward(x_dev, fo_dev)
-            op.adjoint(y_dev, ao_dev)
-            fo_pin.copy_(fo_dev, non_blocking=True)
             ao_pin.copy_(ao_dev, non_blocking=True)
 
     def barrier():
@@ -407,12 +482,9 @@ def main():
         return ms
 
     def graphed(fn, outs):
-        """The step captured once into a CUDA graph and replayed (the launch-bound
-        configs lose their per-launch host overhead); falls back to eager calls
-        when capture fails or a replay does not reproduce the eager outputs bit
-        for bit.  Returns (callable, kernel launches per step or None)."""
-        if os.environ.get("CWW_BENCH_GRAPH", "1") != "1":
-            return fn, None
+        """The step captured once into a CUDA graph and replayed; eager calls when
+        capture fails or a replay does not reproduce the eager outputs bit for bit.
+        Returns (callable, kernel launches per step or None)."""
         try:
             fn()
             torch.cuda.synchronize(dev)
@@ -436,7 +508,9 @@ def main():
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize(dev)
-    dev_outs = [ao_dev] if (is5 or rowpart) else [fo_dev, ao_dev]
+    dev_outs = [ao_dev] if is5 else [fo_dev, ao_dev]
+    if rowpart:
+        dev_outs = [x_rows]
     step_dev_g, per_launch = graphed(step_device, dev_outs) if not rowpart else (step_device, None)
     for _ in range(args.warmup):
         step_dev_g()
@@ -459,62 +533,55 @@ def main():
 
     for _ in range(2):
         step_e2e()
-    e2e_outs = [ao_pin] if (is5 or rowpart) else [fo_pin, ao_pin]
+    e2e_outs = [ao_pin] if is5 else [fo_pin, ao_pin]
     step_e2e_g, _ = graphed(step_e2e, e2e_outs) if not rowpart else (step_e2e, None)
     for _ in range(2):
         step_e2e_g()
     ms_e2e = timed(step_e2e_g, args.steps)
 
-    # weak scaling (independent batches per rank) except config 5 on P GPUs,
-    # where the one image is shared (strong scaling)
+    # configs 2-4: the global batch split over the ranks (sum of the shards);
+    # config 1: one replica per rank; config 5: one shared image
     total_mv = mv_per_step * args.steps * (1 if rowpart else world)
+    if args.config in (2, 3, 4) and world > 1:
+        total_mv = 2 * gbatch * args.steps
     value = total_mv / (ms / 1e3)
     e2e = total_mv / (ms_e2e / 1e3)
     h2d = x_pin.numel() * 8 + (0 if is5 else y_pin.numel() * 8)
     d2h = ao_pin.numel() * 8 + (0 if is5 else fo_pin.numel() * 8)
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel: its SURVEY 8(d) bytes / its device time
     peak, peak_kind = peaks()
     roof = None
+    nvec = batch
     if prof:
         kname = max(prof, key=lambda k: prof[k][0])
         kms, kn = prof[kname]
-        steps_bytes = algorithmic_bytes(cfg, kname, batch) * args.steps
+        steps_bytes = algorithmic_bytes(cfg, kname, nvec) * args.steps
         achieved = steps_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
         traffic, tnote = None, None
-        try:  # committed ncu captures of this config's leading kernels (profiles/r01_traffic.json)
-            trs = json.load(open(os.path.join(REPO, "profiles", "r01_traffic.json")))[str(args.config)]
-            for tr in (trs if isinstance(trs, list) else [trs]):
-                if tr["kernel"] == kname:
-                    traffic, tnote = tr["bytes"], tr["launch"] + " (ncu dram__bytes_read+write, profiles/)"
-        except (OSError, KeyError, ValueError):
-            pass
+        entries, src = latest_traffic(args.config)
+        for tr in entries:
+            if tr["kernel"] == kname:
+                traffic, tnote = tr["bytes"], f"{tr['launch']} (ncu dram__bytes_read+write, profiles/{src})"
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": traffic, "traffic_launch": tnote, "kernel_ms_per_launch": kms / kn, "launches": kn,
+                "traffic": traffic, "traffic_launch": tnote,
+                "algorithmic_bytes_per_launch": steps_bytes / kn if kn else None,
+                "kernel_ms_per_launch": kms / kn, "launches": kn,
                 "kernel_share_of_step": round(kms / ms_prof, 4)}
-    M, N = 1 << j, 1 << (j + q)
-    per_mv = 8 * ((M + N) if dim == 1 else (M * M + N * N))
+    per_mv = path_bytes(cfg)
     path_gbs = per_mv * total_mv / world / (ms / 1e3) / 1e9
 
     line = {
         "metric": "forward+adjoint matvecs/s", "value": round(value, 3), "unit": "matvec/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "strong" if rowpart else "weak",
+        "scaling": scaling_kind(args.config, world),
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded test_rng inputs, SURVEY.md 8d)",
-        "config": {"workload": name, "batch_per_gpu": batch,
-                   "step": (f"{CFG5_ITERS} x U*U on the image (cww_normal: banded normal form W G W^-1 per "
-                            "axis, G = U*U exactly banded since H^T H = M I; rows fused IDWT-band-DWT, tiled "
-                            "transposes)" if is5 else
-                            ("forward + adjoint of the batch (independent: two streams)" if conc else
-                             "forward + adjoint of the batch")),
-                   "launch": ("one CUDA graph per step (captured once, replayed; eager fallback)"
-                              if per_launch is not None else "eager launches"),
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": (f"rows/{world} + NCCL all-to-all transposes" if rowpart
-                                   else f"dp{world} (independent batches)")},
+        "config": config_dict(args.config, world),
+        "launch": ("one CUDA graph per step (captured once, replayed)" if per_launch is not None
+                   else "eager launches"),
         "path_gbs_per_gpu": round(path_gbs, 1), "path_frac": round(path_gbs / peak, 4),
         **({"path_frac_kind": "effective (algorithmic bytes 2*8(M^2+N^2) per U*U; the banded normal form "
                               "moves 3*16*M^2 per U*U on one GPU)",
@@ -525,14 +592,12 @@ def main():
         "gpu_launches": launches,
         "e2e": {"value": round(e2e, 3), "unit": "matvec/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e / args.steps, 4),
-                # host link throughput of the e2e step (PCIe Gen5 x16 on this box: ~55 GB/s per
-                # direction, ~99 GB/s both directions at once, tools/pcie_bw.py)
                 "link_gbs": round((h2d + d2h) / (ms_e2e / args.steps / 1e3) / 1e9, 1)},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(cfg, args.config)
+            line["cpu_baseline"] = cpu_baseline(cfg, args.config, xs, None if is5 else ys)
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

@@ -259,6 +259,13 @@ class _Handle:
         self.h = h
         self.L = L
         self.device = device
+        if device is None:  # the op lives on the device that was current at creation
+            try:
+                import torch
+                self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
+            except ImportError:  # pragma: no cover
+                pass
+        self._inflight = []  # (event, inp, out) of asynchronous pinned-host calls
         ni, no = C.c_size_t(), C.c_size_t()
         _check(L.cww_op_sizes(h, C.byref(ni), C.byref(no)))
         self.nin, self.nout = ni.value, no.value
@@ -282,8 +289,17 @@ class _Handle:
                     raise CwwError(("adjoint" if adjoint else "forward") + ": dimension mismatch", 2)
                 batch = inp.numel() // nin
                 fn = self.L.cww_adjoint_host_async if adjoint else self.L.cww_forward_host_async
+                dev = torch.device("cuda", self.device) if self.device is not None else torch.device("cuda")
+                stream = torch.cuda.current_stream(dev)
                 _check(fn(self.h, inp.data_ptr(), inp.numel(), out.data_ptr(), out.numel(), batch,
-                          torch.cuda.current_stream().cuda_stream))
+                          stream.cuda_stream))
+                # torch's pinned-memory allocator does not see this use: keep both
+                # buffers alive until the stream has finished with them
+                if not torch.cuda.is_current_stream_capturing():
+                    self._inflight = [r for r in self._inflight if not r[0].query()]
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    self._inflight.append((ev, inp, out))
                 return out
             if not inp.is_cuda:
                 inp = inp.detach().numpy()

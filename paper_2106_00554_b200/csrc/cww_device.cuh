@@ -34,9 +34,6 @@ struct Tables {
     int o_ef;   // [2][ A(nu*nu) | B(nu*(2nu-1)) | Aw | Bw ]  left, right
     int o_syn;  // [2 sides][3nu-1][2 bands][2nu]  dense synthesis edge blocks
     int o_ana;  // [2 sides][2 bands][nu][3nu-1]   dense analysis edge rows
-    int o_csyn; // [nc][nc] dense coarse synthesis (levels r0+1..log2 nc), [k][i]
-    int o_cana; // [nc][nc] dense coarse analysis (levels log2 nc..r0+1), [i][k]
-    int nc;     // 64, or 0 when unused
     int n;      // total doubles
 };
 
@@ -542,11 +539,6 @@ __device__ __forceinline__ void dwt_pair(const FiltSmem<NU>& F, const double* x,
     d = b0 + b1;
 }
 
-// Programmatic dependent launch (PDL): every kernel triggers its dependents
-// at entry and waits for its predecessor's results before touching memory;
-// both are no-ops when the launch did not use the PDL attribute.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 // Asynchronous 16-byte global -> shared copy (both addresses 16-byte aligned).
 __device__ __forceinline__ void cp_async16(double* sdst, const double* gsrc) {

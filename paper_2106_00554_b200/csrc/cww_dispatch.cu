@@ -17,9 +17,7 @@ namespace cww {
     cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);                    \
     cudaError_t launch_pyr_nu##N(bool, const PyrArgs&, cudaStream_t);               \
     cudaError_t launch_normal_rows_nu##N(const NormArgs&, cudaStream_t);               \
-    cudaError_t launch_normal_rows_reg_nu##N(const NormArgs&, cudaStream_t);          \
-    cudaError_t launch_fwd1_syn_nu##N(const LargeArgs&, const PyrArgs&, cudaStream_t); \
-    long long fwd1_syn_smem_nu##N(int, const PyrArgs&);
+    cudaError_t launch_normal_rows_reg_nu##N(const NormArgs&, cudaStream_t);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6)
 #undef DECL
 
@@ -98,11 +96,7 @@ cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long
 
 bool normal_reg_ok(int nu, int j, int r0, int use_idwt) {
     (void)nu;
-    static const bool reg = [] {
-        const char* e = std::getenv("CWW_NORMAL_REG");
-        return !(e && e[0] == '0');
-    }();
-    return reg && use_idwt && j >= 9 && j <= 12 && r0 < kRegLog;
+    return use_idwt && j >= 9 && j <= 12 && r0 < kRegLog;
 }
 
 cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st) {
@@ -117,46 +111,40 @@ cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st) {
     return cudaErrorInvalidValue;
 }
 
-// 32 x 32 tiles through shared memory (odd row stride: conflict-free both ways)
-__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, long long n) {
+// Batched out-of-place transpose of rows x cols fp64 matrices: 32 x 32 tiles
+// through shared memory (odd row stride: conflict-free both ways).
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, long long rows,
+                            long long cols) {
     __shared__ double tile[32][33];
-    const long long base = (long long)blockIdx.z * n * n;
-    const long long bx = (long long)blockIdx.x * 32, by = (long long)blockIdx.y * 32;
+    const long long base = (long long)blockIdx.z * rows * cols;
+    const long long bx = (long long)blockIdx.x * 32, by = (long long)blockIdx.y * 32;  // column / row tile
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
 #pragma unroll
     for (int r = 0; r < 32; r += 8) {
         const long long row = by + ty + r, col = bx + tx;
-        if (row < n && col < n) tile[ty + r][tx] = in[base + row * n + col];
+        if (row < rows && col < cols) tile[ty + r][tx] = in[base + row * cols + col];
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 32; r += 8) {
-        const long long row = bx + ty + r, col = by + tx;
-        if (row < n && col < n) out[base + row * n + col] = tile[tx][ty + r];
+        const long long orow = bx + ty + r, ocol = by + tx;  // out is cols x rows
+        if (orow < cols && ocol < rows) out[base + orow * rows + ocol] = tile[tx][ty + r];
     }
 }
 
-cudaError_t launch_transpose(const double* in, double* out, long long n, long long batch, cudaStream_t st) {
-    const unsigned g = (unsigned)((n + 31) / 32);
+cudaError_t launch_transpose_rect(const double* in, double* out, long long rows, long long cols, long long batch,
+                                  cudaStream_t st) {
+    const unsigned gx = (unsigned)((cols + 31) / 32), gy = (unsigned)((rows + 31) / 32);
     for (long long b0 = 0; b0 < batch; b0 += 65535) {
         const long long nb = batch - b0 < 65535 ? batch - b0 : 65535;
-        k_transpose<<<dim3(g, g, (unsigned)nb), dim3(32, 8), 0, st>>>(in + b0 * n * n, out + b0 * n * n, n);
+        k_transpose<<<dim3(gx, gy, (unsigned)nb), dim3(32, 8), 0, st>>>(in + b0 * rows * cols, out + b0 * rows * cols,
+                                                                         rows, cols);
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_fwd1_syn(int nu, const LargeArgs& a, const PyrArgs& p, cudaStream_t st) {
-#define C(N) launch_fwd1_syn_nu##N(a, p, st)
-    SWITCH_NU(nu, C)
-#undef C
-    return cudaErrorInvalidValue;
-}
-
-long long fwd1_syn_smem(int nu, int kl, const PyrArgs& p) {
-#define C(N) fwd1_syn_smem_nu##N(kl, p)
-    SWITCH_NU(nu, C)
-#undef C
-    return -1;
+cudaError_t launch_transpose(const double* in, double* out, long long n, long long batch, cudaStream_t st) {
+    return launch_transpose_rect(in, out, n, n, batch, st);
 }
 
 long long large_nslot(int nu, int q, int j, int kl, int ng) {

@@ -619,9 +619,6 @@ struct cww_op {
         double* d = nullptr;
     };
     std::shared_ptr<Gram> gram = std::make_shared<Gram>();
-    // side stream of the two-stream batch pipeline (run_large_split), created on first use
-    std::shared_ptr<std::once_flag> side_once = std::make_shared<std::once_flag>();
-    cudaStream_t side = nullptr;
 };
 
 namespace {
@@ -707,47 +704,6 @@ cww_status build_tables(cww_op& op) {
             }
         tab.insert(tab.end(), ana.begin(), ana.end());
     }
-    // Dense composite of the coarse levels r0+1..Lc (2^Lc = nc = 64): the
-    // exact product of those level maps, built by applying the level
-    // arithmetic above to unit vectors.  Synthesis stored [k][i] (output i
-    // fastest), analysis [i][k] (output k fastest).  Unused (nc = 0) when
-    // there is no coarse level to collapse or no level above it.
-    t.nc = 0;
-    t.o_csyn = t.o_cana = int(tab.size());
-    {
-        // Disabled: streaming the 32 KB matrix per vector through L1 costs more
-        // than the coarse levels it replaces (the kernels are L1-bound); kept
-        // for experiments (set CWW_DENSE_COARSE=1).
-        const int Lc = 6;
-        const char* dc = std::getenv("CWW_DENSE_COARSE");
-        if (dc && dc[0] == '1' && op.r0 + 1 < Lc && int(op.j) > Lc) {
-            const int nc = 1 << Lc;
-            std::vector<double> syn(size_t(nc * nc)), ana(size_t(nc * nc));
-            for (int k = 0; k < nc; ++k) {
-                std::vector<double> x(size_t(nc), 0.0);
-                x[size_t(k)] = 1.0;
-                std::vector<double> y = x;
-                for (int lev = op.r0 + 1; lev <= Lc; ++lev) {
-                    std::vector<double> part(y.begin(), y.begin() + (1 << lev));
-                    part = op.vmp ? level_inverse_vmp_host(op.f, part) : level_inverse_periodic_host(op.f, part);
-                    std::copy(part.begin(), part.end(), y.begin());
-                }
-                for (int i = 0; i < nc; ++i) syn[size_t(k * nc + i)] = y[size_t(i)];
-                std::vector<double> z = x;
-                for (int lev = Lc; lev > op.r0; --lev) {
-                    std::vector<double> part(z.begin(), z.begin() + (1 << lev));
-                    part = level_forward_host(op.f, part, op.vmp != 0);
-                    std::copy(part.begin(), part.end(), z.begin());
-                }
-                for (int o = 0; o < nc; ++o) ana[size_t(k * nc + o)] = z[size_t(o)];  // input k, output o
-            }
-            t.nc = nc;
-            t.o_csyn = int(tab.size());
-            tab.insert(tab.end(), syn.begin(), syn.end());
-            t.o_cana = int(tab.size());
-            tab.insert(tab.end(), ana.begin(), ana.end());
-        }
-    }
     t.n = int(tab.size());
     CUDA_TRY(cudaMalloc(&op.d_tab, tab.size() * sizeof(double)));
     CUDA_TRY(cudaMemcpy(op.d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -797,8 +753,8 @@ cww_status validate(const cww_op_desc* d) {
     if (d->j + d->q > 30) return fail(CWW_ERR_UNSUPPORTED, "j + q must be <= 30");
     if (d->j < 1) return fail(CWW_ERR_UNSUPPORTED, "j must be >= 1 (M = 1 is not supported)");
     if (d->q > 10) return fail(CWW_ERR_UNSUPPORTED, "q must be <= 10");
-    if (d->dim == 2 && int(d->j) > cww::kSmallMaxLog)
-        return fail(CWW_ERR_UNSUPPORTED, "2D operator supports j <= %d", cww::kSmallMaxLog);
+    if (d->dim == 2 && d->j + d->q > 17)
+        return fail(CWW_ERR_UNSUPPORTED, "2D: j + q must be <= 17 (N^2 doubles of one image must fit a device)");
     int r0 = d->min_level < 0 ? J0 : d->min_level;
     if (r0 > int(d->j)) return fail(CWW_ERR_SPEC, "dwt: j below the coarsest admissible level");
     if (d->boundary == 1 && r0 < J0)
@@ -863,9 +819,13 @@ cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out
         return fail(CWW_ERR_UNSUPPORTED, "shared-memory footprint too large for nu=%d j=%u q=%u", op->nu, op->j, op->q);
     auto a = small_args(op, in, lin, out, lout, nvec, V);
     if (!wav) a.use_idwt = 0;  // 2D: the wavelet transform of this axis runs as a separate panel pass
-    // block-contiguous inputs allow a plain 16-byte copy (forward kernel)
+    // block-contiguous inputs allow a plain 16-byte copy (forward kernel); the
+    // caller's buffer is only guaranteed 8-byte aligned, so a misaligned base
+    // (e.g. x + 1) takes the element-wise path
     const long long M = op->M;
-    if (lin.contig() && (V == 1 || (lin.vsh >= 62 && lin.vs == M))) a.in_block = 1;
+    const bool al16 = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    if (!al16) {
+    } else if (lin.contig() && (V == 1 || (lin.vsh >= 62 && lin.vs == M))) a.in_block = 1;
     else if (lin.vs == 1 && lin.esh >= 62 && lin.es == V && lin.vsh < 62 && (1ll << lin.vsh) == V &&
              lin.vb == M * V)
         a.in_block = 2;
@@ -874,27 +834,15 @@ cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out
     return CWW_OK;
 }
 
-// Wavelet pyramid plan (tuning knobs overridable from the environment)
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e && *e ? std::atoi(e) : dflt;
 }
-const int kPyrSynBot = env_int("CWW_PYR_SYN_BOT", 10);  // coarse levels <= this: separate kernel
-const int kWpyrLog = env_int("CWW_WPYR_LOG", 9);       // warp pyramid: 2^9 fine samples per warp
-const int kWpyrLevels = env_int("CWW_WPYR_LEVELS", 0);  // synthesis levels per launch (0: 6 if j <= 17, else 4)
-const int kWpyrAnaLevels = env_int("CWW_WPYR_ANA_LEVELS", 3);  // analysis steps per launch
-// analysis levels <= this: one CTA per vector (k_wav_coarse).  Off: measured even
-// (cfg2 0.2584 vs 0.2600 ms at 12, worse at 13; cfg3 2.512 vs 2.514 ms)
-const int kAnaCtaTail = env_int("CWW_ANA_CTA_TAIL", 0);
-const int kWpyrMinLog = env_int("CWW_WPYR_MIN_LOG", 9);      // narrowest analysis warp chunk (9: off)
-const long long kWpyrMinWarps = env_int("CWW_WPYR_MIN_WARPS", 148 * 16);  // warps wanted per launch
-// last synthesis pyramid inside forward pass 1 (xi never written).  Off: on
-// B200 the fused kernel is no faster (cfg2 68 us vs 42 + 27 us; cfg3 slower) --
-// both halves are latency-bound, so the saved xi round trip does not show.
-const bool kFuseFwd1 = env_int("CWW_FUSE_FWD1", 0) != 0;
-// coarse synthesis levels r0+1..kPyrSynBot once per CTA inside the first warp pyramid
-// (instead of the one-CTA-per-vector k_wav_coarse launch)
-const bool kCtaCoarse = env_int("CWW_CTA_COARSE", 0) != 0;  // off: cfg2 idwt 66.9 vs 46.9 + 12.7 us
+
+// Wavelet pyramid plan of the large path
+constexpr int kPyrSynBot = 10;      // coarse levels <= 10: k_wav_coarse (one CTA per vector)
+constexpr int kWpyrLog = 9;         // warp pyramids: 2^9 samples of the top level per warp
+constexpr int kWpyrAnaLevels = 3;   // analysis steps per pyramid launch
 
 cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     cww::PyrArgs y{};
@@ -903,230 +851,75 @@ cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     y.nvec = nvec;
     y.vmp = op->vmp;
     y.r0 = op->r0;
-    y.cbot = -1;  // no CTA coarse stage
     return y;
 }
 
-// 2D: column wavelet transforms as a separate panel pass (see run_2d).  Off:
-// measured no faster on B200 (cfg4 1.997 vs 1.994 ms per step: the panel
-// passes cost 2 x 0.21 ms, about what the N-column passes save); read per
-// call so tests can exercise it.
-bool hoist_col_wav() { return env_int("CWW_HOIST_COLWAV", 0) != 0; }
-
-// Multilevel IDWT (inverse) / DWT of nvec vectors through layouts, V per CTA.
-cww_status run_panel_wav(const cww_op* op, const double* src, Layout ls, double* dst, Layout ld,
-                         long long nvec, bool inverse, cudaStream_t st) {
-    if (nvec == 0) return CWW_OK;
-    cww::WavArgs w{};
-    w.kind = 1;
-    w.V = small_V(op->M, nvec, 16);
-    w.tab = op->d_tab;
-    w.t = op->tabs;
-    w.nvec = nvec;
-    w.lev = int(op->j);
-    w.r0 = op->r0;
-    w.inverse = inverse ? 1 : 0;
-    w.vmp = op->vmp;
-    w.src = src;
-    w.ls = ls;
-    w.dst = dst;
-    w.ld = ld;
-    Prof pr(inverse ? "panel_idwt" : "panel_dwt", st);
-    CUDA_TRY(cww::launch_wav(op->nu, w, st));
+// Multilevel synthesis W^-1 (wavelet.cpp:487-514, Inverse) of nvec vectors of
+// length M > 2^12 read through `lin`: the coarse levels r0+1..10 in one CTA per
+// vector (k_wav_coarse), then chained warp pyramids of <= 6 (j <= 17) or 4
+// levels each.  The level-j samples land contiguously (M apart) in w0 or w1;
+// *xi points at them.
+cww_status synth_chain(const cww_op* op, const double* in, Layout lin, long long nvec, double* w0, double* w1,
+                       const double** xi, cudaStream_t st) {
+    const int j = int(op->j), nu = op->nu;
+    const long long M = op->M;
+    int bot = std::max(op->r0, std::min(kPyrSynBot, j - 1));
+    const double* src = nullptr;  // level-bot coarse vector (nullptr: the op input)
+    long long src_vs = 0;
+    if (bot > op->r0) {
+        cww::WavArgs w{};
+        w.tab = op->d_tab;
+        w.t = op->tabs;
+        w.nvec = nvec;
+        w.r0 = op->r0;
+        w.vmp = op->vmp;
+        w.kind = 0;
+        w.lev = bot;
+        w.inverse = 1;
+        w.src = in;
+        w.ls = lin;
+        w.dst = w1;
+        w.dst_vs = 1ll << bot;
+        Prof pr("wav_coarse", st);
+        CUDA_TRY(cww::launch_wav(nu, w, st));
+        src = w1;
+        src_vs = 1ll << bot;
+    }
+    double* bufs[2] = {w0, w1};
+    while (bot < j) {
+        const int top = std::min(j, bot + (j <= 17 ? 6 : 4));
+        cww::PyrArgs y = pyr_args(op, nvec);
+        y.top = top;
+        y.bot = bot;
+        y.cb = std::min(top, kWpyrLog);
+        y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum, &y.wmax2);
+        y.x = in;
+        y.lx = lin;
+        y.src_is_x = src ? 0 : 1;
+        y.src = src;
+        y.src_vs = src_vs;
+        y.out = bufs[src == w0 ? 1 : 0];  // never overwrite the level being read
+        y.out_vs = M;
+        {
+            Prof pr("idwt_pyr", st);
+            CUDA_TRY(cww::launch_pyr(nu, false, y, st));
+        }
+        src = y.out;
+        src_vs = M;
+        bot = top;
+    }
+    *xi = src;
     return CWW_OK;
 }
 
-// ---- large path (1D, M > 2^13) ----
-struct LargePlan {
-    int kl, ng, ng_adj;  // ng: fwd2 sub-tiles per CTA; ng_adj: adj2 (one row per thread)
-};
-LargePlan large_plan(unsigned j) {
-    int a = int(j) - cww::kLogB;
-    int kl = (a + 1) / 2;
-    if (kl > 8) kl = 8;
-    static const int kl_env = env_int("CWW_LARGE_KL", 0);  // tuning: low K bits of the contiguous pass
-    if (kl_env > 0 && kl_env < a) kl = kl_env;
-    int kh = a - kl;
-    int ng = 1;
-    while (ng * (1 << kh) < 128 && ng * 2 <= (1 << kl)) ng *= 2;
-    int ng_adj = 1;  // adj2 runs one tile row per thread: fill the CTA
-    while (ng_adj * (1 << kh) < 256 && ng_adj * 2 <= (1 << kl)) ng_adj *= 2;
-    return {kl, ng, ng_adj};
-}
-
-cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
-                     long long nvec, bool adj, cudaStream_t st, cudaEvent_t mark = nullptr) {
-    if (nvec == 0) return CWW_OK;
-    auto first = [&] {  // `mark` fires once the first kernel of the chain completes
-        if (mark) {
-            cudaEventRecord(mark, st);
-            mark = nullptr;
-        }
-    };
+// Multilevel analysis W (wavelet.cpp:487-514, Forward) of nvec contiguous
+// level-j vectors in w0 (M apart; clobbered) into coefficients through
+// `lout`: chained warp pyramids of <= 3 steps; the launch that reaches level
+// <= 10 finishes the coarse levels in its last CTA per vector (atomic ticket).
+cww_status analysis_chain(const cww_op* op, double* w0, double* w1, double* out, Layout lout, long long nvec,
+                          cudaStream_t st) {
     const long long M = op->M;
-    const int nu = op->nu, NP = 2 * nu - 1, CW = 32 + 2 * (nu - 1);
-    const long long A = M >> cww::kLogB;
-    const auto pl = large_plan(op->j);
-    const bool idwt = op->d.use_idwt && op->r0 < int(op->j);
-    const long long nslot = cww::large_nslot(nu, int(op->q), int(op->j), pl.kl, pl.ng_adj);
-    DevBuf w0, w1, G, ev, epw;
-    CUDA_TRY(G.alloc(size_t(nvec * A * CW), st));
-    CUDA_TRY(ev.alloc(size_t(nvec * 2 * nu), st));
-    if (idwt) {
-        CUDA_TRY(w0.alloc(size_t(nvec * M), st));
-        CUDA_TRY(w1.alloc(size_t(nvec * M), st));
-    }
-    if (adj) CUDA_TRY(epw.alloc(size_t(nvec * nslot * op->S * 2 * NP + 1), st));
-
-    cww::LargeArgs a{};
-    a.tab = op->d_tab;
-    a.t = op->tabs;
-    a.j = int(op->j);
-    a.q = int(op->q);
-    a.kl = pl.kl;
-    a.ng = pl.ng;
-    a.nvec = nvec;
-    a.v0 = 0;
-    a.in = in;
-    a.lin = lin;
-    a.G = G.p;
-    a.ev = ev.p;
-    a.epw = epw.p;
-    a.nslot = nslot;
-    a.cta_red = cww::large_cta_red(nu, int(op->q)) ? 1 : 0;
-    a.out = out;
-    a.lout = lout;
-
-    a.r0 = op->r0;
-    a.use_idwt = op->d.use_idwt;
-    a.vmp = op->vmp;
-    if (!adj) {
-        const double* xi = nullptr;
-        cww::PyrArgs fused{};
-        bool use_fused = false;
-        if (idwt) {
-            // coarse levels r0+1..bot in one CTA per vector, then the fine
-            // levels in chained warp pyramids of <= kWpyrLevels levels
-            const int j = int(op->j);
-            int bot = std::max(op->r0, std::min(kPyrSynBot, j - 1));
-            const double* src = nullptr;  // level-bot coarse vector (nullptr: the op input)
-            long long src_vs = 0;
-            const bool cta_coarse = bot > op->r0 && kCtaCoarse;  // coarse levels inside the first pyramid
-            if (bot > op->r0 && !cta_coarse) {
-                cww::WavArgs w{};
-                w.tab = op->d_tab;
-                w.t = op->tabs;
-                w.nvec = nvec;
-                w.r0 = op->r0;
-                w.vmp = op->vmp;
-                w.kind = 0;
-                w.lev = bot;
-                w.inverse = 1;
-                w.src = in;
-                w.ls = lin;
-                w.dst = w1.p;
-                w.dst_vs = 1ll << bot;
-                {
-                    Prof pr("wav_coarse", st);
-                    CUDA_TRY(cww::launch_wav(nu, w, st));
-                    first();
-                }
-                src = w1.p;
-                src_vs = 1ll << bot;
-            }
-            double* bufs[2] = {w0.p, w1.p};
-            int ob = 0;
-            while (bot < j) {
-                const int top = std::min(j, bot + (kWpyrLevels > 0 ? kWpyrLevels : (j <= 17 ? 6 : 4)));
-                if (top == j && kFuseFwd1) {  // the last pyramid may run inside forward pass 1
-                    cww::PyrArgs y = pyr_args(op, nvec);
-                    y.top = j;
-                    y.bot = bot;
-                    y.cb = 9;  // 512-sample warp cones
-                    y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum);
-                    const int lev = j - bot, hh = nu - 1;  // halo-extended edge cones: margin
-                    y.wmax += hh + 4;
-                    y.wmax2 = y.wmax;
-                    y.dsum += lev * (hh + 4);
-                    y.x = in;
-                    y.lx = lin;
-                    y.src_is_x = src ? 0 : 1;
-                    y.src = src;
-                    y.src_vs = src_vs;
-                    const long long sm = cww::fwd1_syn_smem(nu, pl.kl, y);
-                    if (sm > 0 && sm <= 227 * 1024) {
-                        fused = y;
-                        use_fused = true;
-                        break;
-                    }
-                }
-                cww::PyrArgs y = pyr_args(op, nvec);
-                y.top = top;
-                y.bot = bot;
-                y.cb = std::min(top, kWpyrLog);
-                y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum, &y.wmax2);
-                y.x = in;
-                y.lx = lin;
-                y.src_is_x = src ? 0 : 1;
-                y.src = src;
-                y.src_vs = src_vs;
-                if (cta_coarse && src == nullptr) {  // first pyramid: levels r0+1..bot per CTA
-                    const int nchunk = 1 << (top - y.cb), nw = nchunk < 8 ? nchunk : 8;
-                    int lnw = 0;
-                    while ((1 << lnw) < nw) ++lnw;
-                    y.cbot = op->r0;
-                    y.cwmax = cww::pyr_wmax_cta(nu, top, bot, op->r0, y.cb + lnw, op->vmp != 0, &y.cdsum);
-                }
-                ob = (src == w0.p) ? 1 : 0;  // never overwrite the level being read
-                y.out = bufs[ob];
-                y.out_vs = M;
-                {
-                    Prof pr("idwt_pyr", st);
-                    CUDA_TRY(cww::launch_pyr(nu, false, y, st));
-                    first();
-                }
-                src = bufs[ob];
-                src_vs = M;
-                bot = top;
-            }
-            xi = src;
-        }
-        a.xi = xi;
-        a.xi_vs = M;
-        a.xi_is_input = idwt ? 0 : 1;
-        if (use_fused) {
-            Prof pr("large_fwd1_syn", st);
-            CUDA_TRY(cww::launch_fwd1_syn(nu, a, fused, st));
-            first();
-        } else {
-            Prof pr("large_fwd1", st);
-            CUDA_TRY(cww::launch_large(nu, 0, a, st));
-            first();
-        }
-        {
-            Prof pr("large_fwd2", st);
-            CUDA_TRY(cww::launch_large(nu, 1, a, st));
-        }
-        return CWW_OK;
-    }
-    a.ng = pl.ng_adj;
-    // adjoint
-    {
-        Prof pr("large_adj2", st);
-        CUDA_TRY(cww::launch_large(nu, 2, a, st));
-        first();
-    }
-    a.xo = idwt ? w0.p : nullptr;
-    a.xo_vs = M;
-    a.xo_is_output = idwt ? 0 : 1;
-    {
-        Prof pr("large_adj1", st);
-        CUDA_TRY(cww::launch_large(nu, 3, a, st));
-    }
-    if (!idwt) return CWW_OK;
-    // analysis: chained warp pyramids of <= kWpyrAnaLevels steps (halo ~
-    // (2nu-2) 2^d per 2^kWpyrLog-row chunk); the launch that reaches level
-    // <= kPyrSynBot finishes the coarse levels in its last CTA per vector
+    const int nu = op->nu;
     unsigned* cnt = nullptr;
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cnt), size_t(nvec) * sizeof(unsigned), st));
     struct CntFree {
@@ -1136,34 +929,10 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     } cnt_free{cnt, st};
     CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(nvec) * sizeof(unsigned), st));
     int T = int(op->j);
-    const double* src = w0.p;
-    double* sink[2] = {w1.p, w0.p};
+    const double* src = w0;
+    double* sink[2] = {w1, w0};
     for (int it = 0;; ++it) {
-        if (T > op->r0 && T <= kAnaCtaTail && it > 0) {
-            // the remaining levels T .. r0+1 (2^T samples) in one CTA per vector,
-            // shared-memory ping-pong (k_wav_coarse, analysis direction)
-            cww::WavArgs w{};
-            w.kind = 0;
-            w.tab = op->d_tab;
-            w.t = op->tabs;
-            w.nvec = nvec;
-            w.lev = T;
-            w.r0 = op->r0;
-            w.inverse = 0;
-            w.vmp = op->vmp;
-            w.src = src;
-            w.src_vs = M;
-            w.dst = out;
-            w.ld = lout;
-            w.dv0 = 0;
-            Prof pr("dwt_pyr", st);
-            CUDA_TRY(cww::launch_wav(nu, w, st));
-            break;
-        }
-        int cb = std::min(T, kWpyrLog);
-        // small grids (the last launches of short vectors): narrower warp chunks so
-        // at least ~2 CTAs of 8 warps per SM get work (halo overhead grows instead)
-        while (cb > kWpyrMinLog && nvec * (1ll << (T - cb)) < kWpyrMinWarps) --cb;
+        const int cb = std::min(T, kWpyrLog);
         const int bot = std::max({op->r0, T - kWpyrAnaLevels, T - cb});
         const bool tail = bot > op->r0 && bot <= std::max(kPyrSynBot, op->r0);
         cww::PyrArgs y = pyr_args(op, nvec);
@@ -1191,56 +960,173 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
     return CWW_OK;
 }
 
-// Two-stream batch pipeline for the large path: the batch is halved, the
-// second half runs on a side stream and starts once the first half's first
-// kernel has finished, so each half's latency-bound launches (the coarse
-// wavelet levels, the last-wave tails) overlap the other half's bandwidth-
-// bound passes.  Joined back into the caller's stream before returning.
-// Off: measured slower on B200 (cfg2 0.269 vs 0.262 ms, cfg3 2.68 vs 2.55 ms):
-// the big passes keep every SM's shared memory full, so the halves do not
-// co-reside, they only add launches.
-int split_halves() { return env_int("CWW_SPLIT", 0); }
+// ---- large path (1D, M > 2^12) ----
+struct LargePlan {
+    int kl, ng, ng_adj;  // kl: low K bits of the contiguous passes; ng: fwd2 sub-tiles per CTA; ng_adj: adj2
+};
+LargePlan large_plan(unsigned j) {
+    int a = int(j) - cww::kLogB;
+    int kl = (a + 1) / 2;
+    if (kl > 8) kl = 8;
+    int kh = a - kl;
+    int ng = 1;
+    while (ng * (1 << kh) < 128 && ng * 2 <= (1 << kl)) ng *= 2;
+    int ng_adj = 1;  // adj2 runs one tile row per thread: fill the CTA
+    while (ng_adj * (1 << kh) < 256 && ng_adj * 2 <= (1 << kl)) ng_adj *= 2;
+    return {kl, ng, ng_adj};
+}
 
-cww_status run_large_split(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
-                           long long nvec, bool adj, cudaStream_t st) {
-    if (!split_halves() || nvec < 2) return run_large(op, in, lin, out, lout, nvec, adj, st);
-    cww_op* mop = const_cast<cww_op*>(op);
-    std::call_once(*mop->side_once, [&] { cudaStreamCreateWithFlags(&mop->side, cudaStreamNonBlocking); });
-    if (!op->side) return run_large(op, in, lin, out, lout, nvec, adj, st);
-    const long long h = nvec / 2;
-    cudaEvent_t e1 = nullptr, e2 = nullptr;
-    CUDA_TRY(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
-    struct EvFree {
-        cudaEvent_t a, b;
-        ~EvFree() {
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
+// Vectors per slice of the large path: the whole chain (pyramids, pass 1,
+// pass 2) runs slice by slice so that the intermediates (xi, the Hadamard
+// intermediate G, the pyramid levels) of one slice stay L2-resident and only
+// the path's own inputs and outputs stream through HBM.
+long long large_slice(const cww_op* op, long long nvec) {
+    static const long long env = env_int("CWW_LARGE_SLICE", 0);
+    if (env > 0) return std::min(env, nvec);
+    const long long M = op->M, A = M >> cww::kLogB, CW = 32 + 2 * (op->nu - 1);
+    const long long per = 8 * (2 * M + A * CW);  // w0 + w1 + G per vector
+    const long long budget = 40ll << 20;
+    return std::max(1ll, std::min(nvec, budget / per));
+}
+
+struct LargeBufs {
+    DevBuf w0, w1, G, ev, epw;
+};
+
+cww_status run_large_slice(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
+                           long long nvec, bool adj, LargeBufs& B, cudaStream_t st) {
+    const int nu = op->nu;
+    const long long M = op->M;
+    const auto pl = large_plan(op->j);
+    const bool idwt = op->d.use_idwt && op->r0 < int(op->j);
+    cww::LargeArgs a{};
+    a.tab = op->d_tab;
+    a.t = op->tabs;
+    a.j = int(op->j);
+    a.q = int(op->q);
+    a.kl = pl.kl;
+    a.ng = pl.ng;
+    a.nvec = nvec;
+    a.v0 = 0;
+    a.in = in;
+    a.lin = lin;
+    a.G = B.G.p;
+    a.ev = B.ev.p;
+    a.epw = B.epw.p;
+    a.nslot = cww::large_nslot(nu, int(op->q), int(op->j), pl.kl, pl.ng_adj);
+    a.cta_red = cww::large_cta_red(nu, int(op->q)) ? 1 : 0;
+    a.out = out;
+    a.lout = lout;
+    a.r0 = op->r0;
+    a.use_idwt = op->d.use_idwt;
+    a.vmp = op->vmp;
+    if (!adj) {
+        const double* xi = nullptr;
+        if (idwt) {
+            cww_status s = synth_chain(op, in, lin, nvec, B.w0.p, B.w1.p, &xi, st);
+            if (s != CWW_OK) return s;
         }
-    } evf{e1, e2};
-    cww_status s = run_large(op, in, lin, out, lout, h, adj, st, e1);
-    if (s != CWW_OK) return s;
-    CUDA_TRY(cudaStreamWaitEvent(op->side, e1, 0));
-    s = run_large(op, in + lin.vbase(h), lin, out + lout.vbase(h), lout, nvec - h, adj, op->side);
-    // join even on failure so nothing of this call outlives it on the side stream
-    CUDA_TRY(cudaEventRecord(e2, op->side));
-    CUDA_TRY(cudaStreamWaitEvent(st, e2, 0));
-    return s;
+        a.xi = xi;
+        a.xi_vs = M;
+        a.xi_is_input = idwt ? 0 : 1;
+        {
+            Prof pr("large_fwd1", st);
+            CUDA_TRY(cww::launch_large(nu, 0, a, st));
+        }
+        Prof pr("large_fwd2", st);
+        CUDA_TRY(cww::launch_large(nu, 1, a, st));
+        return CWW_OK;
+    }
+    a.ng = pl.ng_adj;
+    {
+        Prof pr("large_adj2", st);
+        CUDA_TRY(cww::launch_large(nu, 2, a, st));
+    }
+    a.xo = idwt ? B.w0.p : nullptr;
+    a.xo_vs = M;
+    a.xo_is_output = idwt ? 0 : 1;
+    {
+        Prof pr("large_adj1", st);
+        CUDA_TRY(cww::launch_large(nu, 3, a, st));
+    }
+    if (!idwt) return CWW_OK;
+    return analysis_chain(op, B.w0.p, B.w1.p, out, lout, nvec, st);
+}
+
+// Forward (IDWT, pass 1, pass 2) or adjoint (pass 2, pass 1, DWT) of nvec
+// contiguous vectors, slice by slice (large_slice) through one set of
+// slice-sized intermediates.
+cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out, Layout lout, long long nvec,
+                     bool adj, cudaStream_t st) {
+    if (nvec == 0) return CWW_OK;
+    const long long M = op->M;
+    const int nu = op->nu, NP = 2 * nu - 1, CW = 32 + 2 * (nu - 1);
+    const long long A = M >> cww::kLogB;
+    const auto pl = large_plan(op->j);
+    const bool idwt = op->d.use_idwt && op->r0 < int(op->j);
+    const long long sl = large_slice(op, nvec);
+    const long long nslot = cww::large_nslot(nu, int(op->q), int(op->j), pl.kl, pl.ng_adj);
+    LargeBufs B;
+    CUDA_TRY(B.G.alloc(size_t(sl * A * CW), st));
+    CUDA_TRY(B.ev.alloc(size_t(sl * 2 * nu), st));
+    if (idwt) {
+        CUDA_TRY(B.w0.alloc(size_t(sl * M), st));
+        CUDA_TRY(B.w1.alloc(size_t(sl * M), st));
+    }
+    if (adj) CUDA_TRY(B.epw.alloc(size_t(sl * nslot * op->S * 2 * NP + 1), st));
+    for (long long v0 = 0; v0 < nvec; v0 += sl) {
+        const long long nv = std::min(sl, nvec - v0);
+        cww_status s = run_large_slice(op, in + lin.vbase(v0), lin, out + lout.vbase(v0), lout, nv, adj, B, st);
+        if (s != CWW_OK) return s;
+    }
+    return CWW_OK;
 }
 
 cww_status run_1d(const cww_op* op, const double* in, double* out, long long nvec, bool adj,
                   cudaStream_t st) {
     Layout lin = lay_contig(adj ? op->N : op->M), lout = lay_contig(adj ? op->M : op->N);
     if (op->j <= unsigned(cww::kSmallMaxLog)) return run_small(op, in, lin, out, lout, nvec, adj, st);
-    return run_large_split(op, in, lin, out, lout, nvec, adj, st);
+    return run_large(op, in, lin, out, lout, nvec, adj, st);
 }
 
 // 2D: rows then columns (forward), columns then rows (adjoint), with the
 // M x N intermediate stored in column panels of VC columns: [N/VC][M][VC].
+// Above 2^12 per axis (large path): every pass runs on contiguous rows, with
+// batched out-of-place transposes between the passes.
 cww_status run_2d(const cww_op* op, const double* in, double* out, long long batch, bool adj,
                   cudaStream_t st) {
     const long long M = op->M, N = op->N;
     const int j = int(op->j), jq = int(op->j + op->q);
+    cww_status s;
+    if (j > cww::kSmallMaxLog) {
+        // forward:  T = rows(X) (M x N), T^T (N x M), Z = rows(T^T) = Y^T (N x N), Y = Z^T
+        // adjoint:  Y^T (N x N), V^T = rows(Y^T) (N x M), V (M x N), X = rows(V) (M x M)
+        DevBuf t1, t2;
+        CUDA_TRY(t1.alloc(size_t(batch * std::max(M * N, N * N)), st));
+        CUDA_TRY(t2.alloc(size_t(batch * std::max(M * N, N * N)), st));
+        if (!adj) {
+            if ((s = run_large(op, in, lay_contig(M), t1.p, lay_contig(N), batch * M, false, st)) != CWW_OK) return s;
+            {
+                Prof pr("transpose", st);
+                CUDA_TRY(cww::launch_transpose_rect(t1.p, t2.p, M, N, batch, st));
+            }
+            if ((s = run_large(op, t2.p, lay_contig(M), t1.p, lay_contig(N), batch * N, false, st)) != CWW_OK)
+                return s;
+            Prof pr("transpose", st);
+            CUDA_TRY(cww::launch_transpose_rect(t1.p, out, N, N, batch, st));
+            return CWW_OK;
+        }
+        {
+            Prof pr("transpose", st);
+            CUDA_TRY(cww::launch_transpose_rect(in, t1.p, N, N, batch, st));
+        }
+        if ((s = run_large(op, t1.p, lay_contig(N), t2.p, lay_contig(M), batch * N, true, st)) != CWW_OK) return s;
+        {
+            Prof pr("transpose", st);
+            CUDA_TRY(cww::launch_transpose_rect(t2.p, t1.p, N, M, batch, st));
+        }
+        return run_large(op, t1.p, lay_contig(N), out, lay_contig(M), batch * M, true, st);
+    }
     int VC = small_V(M, N, 16);
     int lvc = 0;
     while ((1 << lvc) < VC) ++lvc;
@@ -1248,29 +1134,9 @@ cww_status run_2d(const cww_op* op, const double* in, double* out, long long bat
     CUDA_TRY(T.alloc(size_t(batch * M * N), st));
     // row vectors: v = b*M + m ; column vectors: v = b*N + n
     Layout x_rows{0, M, 0, 1, 62, 62};                     // x[v*M + i]
-    Layout x_cols{M * M, 1, 0, M, j, 62};                  // x: (v>>j)*M^2 + (v&(M-1)) + i*M
     Layout t_rows{M * N, VC, M * VC, 1, j, lvc};           // T: (v>>j)*MN + (v&(M-1))*VC + (i>>lvc)*M*VC + (i&(VC-1))
     Layout t_cols{M * VC, 1, 0, VC, lvc, 62};              // T: (v>>lvc)*M*VC + (v&(VC-1)) + i*VC
     Layout y_cols{N * N, 1, 0, N, jq, 62};                 // y: (v>>jq)*N^2 + (v&(N-1)) + i*N
-    cww_status s;
-    // Column wavelet transforms hoisted onto the M columns of the coefficient
-    // image: G = U W^-1 along columns and W^-1 acts on a different axis than
-    // the row pass, so  G X G^T = U ((W^-1 X) W^-T U^T)  -- the N-column pass
-    // runs U alone (M instead of N column wavelet transforms; exact algebra,
-    // only the rounding order changes).  Adjoint: W (U^T Y U W^T) by symmetry.
-    const bool hoist = hoist_col_wav() && op->d.use_idwt && op->r0 < j && j >= 8;
-    if (hoist) {
-        DevBuf Xw;
-        CUDA_TRY(Xw.alloc(size_t(batch * M * M), st));
-        if (!adj) {
-            if ((s = run_panel_wav(op, in, x_cols, Xw.p, x_cols, batch * M, true, st)) != CWW_OK) return s;
-            if ((s = run_small(op, Xw.p, x_rows, T.p, t_rows, batch * M, false, st)) != CWW_OK) return s;
-            return run_small(op, T.p, t_cols, out, y_cols, batch * N, false, st, false);
-        }
-        if ((s = run_small(op, in, y_cols, T.p, t_cols, batch * N, true, st, false)) != CWW_OK) return s;
-        if ((s = run_small(op, T.p, t_rows, Xw.p, x_rows, batch * M, true, st)) != CWW_OK) return s;
-        return run_panel_wav(op, Xw.p, x_cols, out, x_cols, batch * M, false, st);
-    }
     if (!adj) {
         if ((s = run_small(op, in, x_rows, T.p, t_rows, batch * M, false, st)) != CWW_OK) return s;
         return run_small(op, T.p, t_cols, out, y_cols, batch * N, false, st);
@@ -1414,7 +1280,6 @@ cww_status cww_op_destroy(cww_op* op) {
     if (op->d_tab) cudaFree(op->d_tab);
     if (op->d_mask) cudaFree(op->d_mask);
     if (op->gram->d) cudaFree(op->gram->d);
-    if (op->side) cudaStreamDestroy(op->side);
     delete op;
     return CWW_OK;
 }
@@ -1456,15 +1321,6 @@ cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* 
     if (batch == 0) return CWW_OK;
     if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     return run(op, y, x, (long long)batch, true, S_(stream));
-}
-
-// CWW_NORMAL_EXPLICIT=1: normal operator / solver through forward + adjoint
-bool normal_explicit() {
-    static const bool v = [] {
-        const char* e = std::getenv("CWW_NORMAL_EXPLICIT");
-        return e && e[0] == '1';
-    }();
-    return v;
 }
 
 // ---- banded normal form (U* U along one axis) -----------------------------
@@ -1579,29 +1435,6 @@ cww_status normal_banded(const cww_op* op, double* x, double* w, long long batch
         }
         return CWW_OK;
     }
-    static const bool strided = [] {
-        const char* e = std::getenv("CWW_NORMAL_STRIDED");
-        return e && e[0] == '1';
-    }();
-    if (strided && cww::normal_reg_ok(op->nu, int(op->j), op->r0, op->d.use_idwt)) {
-        // register kernel: rows in place, then columns in place (strided, no transposes).
-        // Opt-in: measured at config 5 the strided column pass costs 2.1x a row pass,
-        // more than the transpose it saves (27.3 vs 19.4 ms per 50 iterations).
-        for (int it = 0; it < iters; ++it) {
-            cww::NormArgs a = norm_args(op, x, batch * M);
-            {
-                Prof pr("normal_rows", st);
-                CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
-            }
-            a.vpi = M;
-            a.ivs = M * M;
-            a.in_vs = a.out_vs = 1;
-            a.es = M;
-            Prof pr("normal_cols", st);
-            CUDA_TRY(cww::launch_normal_rows(op->nu, a, st));
-        }
-        return CWW_OK;
-    }
     double* cur = x;
     double* oth = w;
     for (int it = 0; it < iters; ++it) {
@@ -1643,7 +1476,7 @@ cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work, s
         w = wb.p;
     }
     CUDA_TRY(cudaSetDevice(op->device));
-    if (!op->masked && !normal_explicit() && op->M <= 4096) {
+    if (!op->masked && op->M <= 4096) {
         std::call_once(op->gram->once, [op] { build_gram(op); });
         if (op->gram->ok) return normal_banded(op, x, w, (long long)batch, iters, st);
     }
@@ -1873,7 +1706,7 @@ cww_status cww_gs_solve(const cww_op* op, const double* y, size_t y_len, double*
     if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     if (max_iters < 0 || !(residual_tol >= 0.0)) return fail(CWW_ERR_INVALID_ARG, "gs_solve: bad parameters");
     CUDA_TRY(cudaSetDevice(op->device));
-    if (!op->masked && op->M <= 4096 && !normal_explicit()) {
+    if (!op->masked && op->M <= 4096) {
         std::call_once(op->gram->once, [op] { build_gram(op); });
         if (op->gram->ok)
             return gs_solve_normal(op, y, x, (long long)batch, residual_tol, max_iters, use_x0 != 0, iters,
@@ -1950,7 +1783,7 @@ static cww_status host_call_async(const cww_op* op, const double* in, size_t in_
     if (!in || !out) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     if (!is_pinned(in) || !is_pinned(out)) return host_call(op, in, in_len, out, out_len, batch, adj);
     CUDA_TRY(cudaSetDevice(op->device));
-    static const size_t zc_max = size_t(env_int("CWW_ZERO_COPY_KB", 256)) << 10;
+    constexpr size_t zc_max = size_t(256) << 10;
     if ((in_len + out_len) * sizeof(double) <= zc_max && op->M <= (1ll << cww::kSmallMaxLog)) {
         // tiny transforms (small path: each input read once, each output written
         // once): the kernels read / write the pinned buffers over PCIe directly
@@ -1980,7 +1813,7 @@ static cww_status host_call_async(const cww_op* op, const double* in, size_t in_
         ss.device = op->device;
     }
     const size_t ni = in_len / batch, no = out_len / batch;
-    static const size_t target = size_t(env_int("CWW_HOST_CHUNK_MB", 64)) << 20;  // input+output per chunk (tuned: 8-256 MB)
+    constexpr size_t target = size_t(64) << 20;  // input+output per chunk (tuned: 8-256 MB)
     size_t cb = std::max<size_t>(1, target / ((ni + no) * sizeof(double)));
     cb = std::min(cb, batch);
     const size_t nch = (batch + cb - 1) / cb;
@@ -2032,71 +1865,105 @@ cww_status cww_adjoint_host(const cww_op* op, const double* y, size_t y_len, dou
     return host_call(op, y, y_len, x, x_len, batch, true);
 }
 
+// In-place multilevel DWT / IDWT of `batch` vectors (1D) or images (2D,
+// rows then columns: dwt_apply_2d) on the op's spec, j and r0
+// (wavelet.cpp:487-536).  M <= 2^12: one CTA per vector (k_wav_coarse,
+// through the data's layout).  Larger M: the large path's warp pyramids
+// (synth_chain / analysis_chain) on contiguous rows; 2D columns via batched
+// transposes.
 cww_status cww_dwt(const cww_op* op, double* data, size_t len, size_t batch, int dir, void* stream) {
     if (!op) return fail(CWW_ERR_INVALID_ARG, "null op");
+    if (!data && batch) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (dir != CWW_DWT_FORWARD && dir != CWW_DWT_INVERSE) return fail(CWW_ERR_INVALID_ARG, "dwt: bad direction");
     size_t ni;
     cww_op_sizes(op, &ni, nullptr);
     if (len != ni * batch) return fail(CWW_ERR_DIMENSION, "dwt: bad input length");
     if (batch == 0 || op->r0 >= int(op->j)) return CWW_OK;
+    CUDA_TRY(cudaSetDevice(op->device));
     cudaStream_t st = S_(stream);
     const long long M = op->M;
     const int nu = op->nu;
     const bool inverse = dir == CWW_DWT_INVERSE;
-    long long nvec = (long long)batch * (op->dim == 2 ? M : 1);
-    auto pass = [&](Layout l, long long nv) -> cww_status {
-        if (M <= (1ll << cww::kSmallMaxLog)) {  // k_wav_coarse: 3 * 2^j doubles of smem
-            cww::WavArgs w{};
-            w.kind = 0;
-            w.tab = op->d_tab;
-            w.t = op->tabs;
-            w.nvec = nv;
-            w.lev = int(op->j);
-            w.r0 = op->r0;
-            w.inverse = inverse;
-            w.vmp = op->vmp;
-            // in place: both sides through the layout (src read fully before writes)
-            DevBuf tmp;
-            CUDA_TRY(tmp.alloc(size_t(nv * M), st));
-            w.src = data;
-            w.ls = l;
-            w.sv0 = 0;
-            w.src_vs = M;
+    const long long nvec = (long long)batch * (op->dim == 2 ? M : 1);
+    if (M > (1ll << cww::kSmallMaxLog)) {
+        // contiguous rows through the pyramids; 2D: rows, transpose, rows, transpose back
+        DevBuf w0, w1, tr;
+        CUDA_TRY(w0.alloc(size_t(nvec * M), st));
+        CUDA_TRY(w1.alloc(size_t(nvec * M), st));
+        if (op->dim == 2) CUDA_TRY(tr.alloc(size_t(nvec * M), st));
+        auto rows = [&](double* buf) -> cww_status {  // in place on nvec contiguous rows of buf
             if (inverse) {
-                w.dst = tmp.p;
-                w.dst_vs = M;
-                Prof pr("wav_coarse", st, 2);
-                CUDA_TRY(cww::launch_wav(nu, w, st));
-                // copy back through the layout with a forward "coarse" of zero levels
-                cww::WavArgs c = w;
-                c.inverse = 0;
-                c.r0 = int(op->j);
-                c.src = tmp.p;
-                c.src_vs = M;
-                c.dst = data;
-                c.ld = l;
-                c.dv0 = 0;
-                CUDA_TRY(cww::launch_wav(nu, c, st));
-            } else {
-                // gather into contiguous scratch, transform, scatter back
-                cww::WavArgs g = w;
-                g.inverse = 1;
-                g.r0 = int(op->j);
-                g.dst = tmp.p;
-                g.dst_vs = M;
-                Prof pr("wav_coarse", st, 2);
-                CUDA_TRY(cww::launch_wav(nu, g, st));
-                cww::WavArgs f = w;
-                f.inverse = 0;
-                f.src = tmp.p;
-                f.src_vs = M;
-                f.dst = data;
-                f.ld = l;
-                f.dv0 = 0;
-                CUDA_TRY(cww::launch_wav(nu, f, st));
+                const double* xi = nullptr;
+                cww_status s = synth_chain(op, buf, lay_contig(M), nvec, w0.p, w1.p, &xi, st);
+                if (s != CWW_OK) return s;
+                CUDA_TRY(cudaMemcpyAsync(buf, xi, size_t(nvec * M) * 8, cudaMemcpyDeviceToDevice, st));
+                return CWW_OK;
             }
-            return CWW_OK;
+            CUDA_TRY(cudaMemcpyAsync(w0.p, buf, size_t(nvec * M) * 8, cudaMemcpyDeviceToDevice, st));
+            return analysis_chain(op, w0.p, w1.p, buf, lay_contig(M), nvec, st);
+        };
+        cww_status s = rows(data);
+        if (s != CWW_OK || op->dim == 1) return s;
+        {
+            Prof pr("transpose", st);
+            CUDA_TRY(cww::launch_transpose(data, tr.p, M, (long long)batch, st));
         }
-        return fail(CWW_ERR_UNSUPPORTED, "standalone DWT supports j <= %d", cww::kSmallMaxLog);
+        if ((s = rows(tr.p)) != CWW_OK) return s;
+        Prof pr("transpose", st);
+        CUDA_TRY(cww::launch_transpose(tr.p, data, M, (long long)batch, st));
+        return CWW_OK;
+    }
+    auto pass = [&](Layout l, long long nv) -> cww_status {  // k_wav_coarse: 3 * 2^j doubles of smem
+        cww::WavArgs w{};
+        w.kind = 0;
+        w.tab = op->d_tab;
+        w.t = op->tabs;
+        w.nvec = nv;
+        w.lev = int(op->j);
+        w.r0 = op->r0;
+        w.inverse = inverse;
+        w.vmp = op->vmp;
+        // in place: both sides through the layout (src read fully before writes)
+        DevBuf tmp;
+        CUDA_TRY(tmp.alloc(size_t(nv * M), st));
+        w.src = data;
+        w.ls = l;
+        w.sv0 = 0;
+        w.src_vs = M;
+        if (inverse) {
+            w.dst = tmp.p;
+            w.dst_vs = M;
+            Prof pr("wav_coarse", st, 2);
+            CUDA_TRY(cww::launch_wav(nu, w, st));
+            // copy back through the layout with a forward "coarse" of zero levels
+            cww::WavArgs c = w;
+            c.inverse = 0;
+            c.r0 = int(op->j);
+            c.src = tmp.p;
+            c.src_vs = M;
+            c.dst = data;
+            c.ld = l;
+            c.dv0 = 0;
+            CUDA_TRY(cww::launch_wav(nu, c, st));
+        } else {
+            // gather into contiguous scratch, transform, scatter back
+            cww::WavArgs g = w;
+            g.inverse = 1;
+            g.r0 = int(op->j);
+            g.dst = tmp.p;
+            g.dst_vs = M;
+            Prof pr("wav_coarse", st, 2);
+            CUDA_TRY(cww::launch_wav(nu, g, st));
+            cww::WavArgs f = w;
+            f.inverse = 0;
+            f.src = tmp.p;
+            f.src_vs = M;
+            f.dst = data;
+            f.ld = l;
+            f.dv0 = 0;
+            CUDA_TRY(cww::launch_wav(nu, f, st));
+        }
+        return CWW_OK;
     };
     if (op->dim == 1) return pass(lay_contig(M), nvec);
     // 2D: rows (v = b*M + r: x[v*M + i]) then columns (v = b*M + c: x[(v>>j)*M^2 + (v&(M-1)) + i*M])

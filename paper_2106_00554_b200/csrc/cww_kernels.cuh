@@ -30,7 +30,6 @@
 namespace cww {
 
 constexpr int kSmallNT = 256;  // threads per small-path CTA (2 CTAs per SM)
-constexpr int kNc = 64;        // dense coarse wavelet block (levels r0+1..6)
 constexpr int kWarpLev = 8;  // wavelet levels of <= 256 samples run warp-private
 #ifndef CWW_CONTIG_MAXR
 #define CWW_CONTIG_MAXR 4  // large contiguous passes: widest in-register Hadamard pass (bits)
@@ -135,7 +134,7 @@ __device__ __forceinline__ void row_adj_accum_pf(double* trow, const double* kp,
         const int kd = e - 2 * H;  // last use of y[kd] was this column
         if (kd >= 0 && kd < B && pe) {
             const unsigned xb = brev_c(kd, LOGB);
-            y[kd] = __ldg(((__popc(xb) & 1) ? po : pe) + (long long)gray_inv_c(xb) * step);
+            y[kd] = __ldcs(((__popc(xb) & 1) ? po : pe) + (long long)gray_inv_c(xb) * step);  // streamed once
         }
     }
 }
@@ -334,28 +333,9 @@ __device__ __forceinline__ void group_sync(int gid, int G, int ngroups) {
 template <int NU, int NT>
 __device__ __forceinline__ const double* idwt_group(const FiltSmem<NU>& F, const double* xv, double* p0,
                                                     double* p1, double* cbuf, int j, int r0, bool vmp,
-                                                    int gt, int G, int gid, int ngroups,
-                                                    const double* csyn, int nc) {
+                                                    int gt, int G, int gid, int ngroups) {
     const double* src = xv;
     int lev = r0 + 1;
-    if (nc > 0) {  // collapsed coarse levels r0+1..log2(nc): one dense pass
-        const int Lc = 31 - __clz(nc);
-        double* dst = (Lc == j - 1) ? cbuf : p0;
-        for (int i = gt; i < kNc; i += G) {  // nc == kNc (64) whenever enabled
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll 16
-            for (int k = 0; k < kNc; k += 4) {
-                a0 += __ldg(csyn + k * kNc + i) * xv[k];
-                a1 += __ldg(csyn + (k + 1) * kNc + i) * xv[k + 1];
-                a2 += __ldg(csyn + (k + 2) * kNc + i) * xv[k + 2];
-                a3 += __ldg(csyn + (k + 3) * kNc + i) * xv[k + 3];
-            }
-            dst[i] = (a0 + a1) + (a2 + a3);
-        }
-        group_sync<NT>(gid, G, ngroups);
-        src = dst;
-        lev = Lc + 1;
-    }
     for (; lev < j; ++lev) {
         const int n = 1 << lev;
         double* dst = (lev == j - 1) ? cbuf : (src == p0 ? p1 : p0);
@@ -424,8 +404,6 @@ __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 template <int NU, int LOGB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
     const bool vmp_ = NU > 1 && p.vmp != 0;  // VMP needs nu >= 2: no VMP code in the Haar kernels
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     using G = Geo<NU, LOGB>;
     constexpr int B = G::B, H = G::H, CW = G::CW, RS = G::RS, NP = G::NP;
     extern __shared__ double sm[];
@@ -516,7 +494,7 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
         // levels run in ONE phase without barriers (wavelet.cpp:387-400 per step)
         constexpr bool haar = NU == 1;
         if (idwt && !haar) cfin = idwt_group<NU, NT>(F, xv, tv, tv + hM, C + v * hM, j, p.r0, vmp_, gt, Gs, gid,
-                                                          nv, p.tab + p.t.o_csyn, p.t.nc);
+                                                          nv);
         PHASE(2);
         auto put = [&](int i, double val) {
             if (NU > 1 && (i < NU || i >= M - NU)) {
@@ -639,8 +617,6 @@ __global__ void __launch_bounds__(NT, 2) k_small_fwd(SmallArgs p) {
 template <int NU, int LOGB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
     const bool vmp_ = NU > 1 && p.vmp != 0;  // VMP needs nu >= 2: no VMP code in the Haar kernels
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     using G = Geo<NU, LOGB>;
     constexpr int B = G::B, H = G::H, CW = G::CW, RS = G::RS, NP = G::NP;
     extern __shared__ double sm[];
@@ -798,9 +774,7 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
         double* xv = X + v * M;
         double* cv = C + v * hM;
         const double* src = xv;
-        const int nc = p.t.nc;
-        const int lstop = nc > 0 ? 31 - __clz(nc) : p.r0;  // levels above lstop one by one
-        for (int lev = j; lev > lstop; --lev) {
+        for (int lev = j; lev > p.r0; --lev) {
             const int t = j - lev, n = 1 << lev, half = n >> 1;
             const bool last = lev == p.r0 + 1;
             double* dst = last ? ov : ((t & 1) ? xv : cv);  // coarse rows ping-pong C <-> X
@@ -842,20 +816,6 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
             group_sync<NT>(gid, Gs, nv);
             src = dst;
         }
-        if (nc > 0) {  // collapsed coarse levels log2(nc)..r0+1: one dense pass
-            const double* cana = p.tab + p.t.o_cana;
-            for (int o = gt; o < kNc; o += Gs) {
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll 16
-                for (int i = 0; i < kNc; i += 4) {
-                    a0 += __ldg(cana + i * kNc + o) * src[i];
-                    a1 += __ldg(cana + (i + 1) * kNc + o) * src[i + 1];
-                    a2 += __ldg(cana + (i + 2) * kNc + o) * src[i + 2];
-                    a3 += __ldg(cana + (i + 3) * kNc + o) * src[i + 3];
-                }
-                ov[o] = (a0 + a1) + (a2 + a3);
-            }
-        }
     }
     __syncthreads();
     PHASE(4);
@@ -882,151 +842,6 @@ __global__ void __launch_bounds__(NT, 2) k_small_adj(SmallArgs p) {
 }
 
 // ---------------------------------------------------------------------------
-// panel wavelet pass (2D driver): the full multilevel IDWT / DWT of V vectors
-// per CTA through arbitrary layouts -- used for the column transforms of the
-// 2D operator, hoisted out of the N-column U pass onto the M columns of the
-// coefficient image (W^-1 along columns commutes with the row pass).
-// smem per vector: X [M] (input; analysis ping), Wb [M] (synthesis ping-pong
-// halves; output staging), C [M/2] (last coarse level / analysis pong).
-// ---------------------------------------------------------------------------
-__host__ __device__ inline long long panel_wav_smem_bytes(int fs, int V, int j) {
-    return ((long long)fs + (long long)V * ((5ll << j) / 2)) * 8;
-}
-
-template <int NU, int NT>
-__global__ void __launch_bounds__(NT, 2) k_panel_wav(WavArgs p) {
-    pdl_trigger();
-    pdl_wait();
-    extern __shared__ double sm[];
-    const int tid = threadIdx.x;
-    const int j = p.lev, M = 1 << j, hM = M >> 1;
-    const int V = p.V, lV = ilog2(V);
-    const long long v0 = (long long)blockIdx.x * V;
-    const int nv = (int)((p.nvec - v0) < V ? (p.nvec - v0) : V);
-    double* filt = sm;
-    double* X = filt + FiltSmem<NU>::SIZE;
-    double* Wb = X + V * M;
-    double* C = Wb + V * M;
-    const int Gs = NT / V, gid = tid / Gs, gt = tid % Gs;
-    stage_filters<NU>(filt, p.tab, p.t, tid, NT);
-    {
-        const bool vf = p.ls.vfast();  // lanes vary the vector first (column panels)
-        constexpr int U = 8;           // loads in flight per thread
-        if (vf && p.ls.esh >= 62 && p.ls.vsh >= lV && nv == V) {
-            // the CTA's V vectors are adjacent columns of one image: pointer stepping
-            const int v = tid & (V - 1), i0 = tid >> lV, di = NT >> lV;
-            const long long es = p.ls.es;
-            const double* b = p.src + p.ls.vbase(v0) + v + (long long)i0 * es;
-            double* xd = X + v * M + i0;
-            for (int i = 0; i < M; i += U * di) {
-                double r[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) r[u] = (i + u * di + i0 < M) ? __ldg(b + (long long)(i + u * di) * es) : 0.0;
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (i + u * di + i0 < M) xd[i + u * di] = r[u];
-            }
-        } else
-        for (int f0 = tid; f0 < V * M; f0 += U * NT) {
-            double r[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int f = f0 + u * NT;
-                const int v = vf ? f & (V - 1) : f >> j;
-                const int i = vf ? f >> lV : f & (M - 1);
-                r[u] = (f < V * M && v < nv) ? __ldg(p.src + p.ls.at(v0 + v, i)) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int f = f0 + u * NT;
-                const int v = vf ? f & (V - 1) : f >> j;
-                const int i = vf ? f >> lV : f & (M - 1);
-                if (f < V * M) X[v * M + i] = r[u];
-            }
-        }
-    }
-    __syncthreads();
-    const FiltSmem<NU> F{filt};
-    double* const ov = Wb;  // output staging (both directions)
-    if (gid < nv) {
-        const int v = gid;
-        double* xv = X + v * M;
-        double* wv = Wb + v * M;
-        double* cv = C + v * hM;
-        if (p.inverse) {  // synthesis levels r0+1 .. j (wavelet.cpp:505-513)
-            const double* cfin = idwt_group<NU, NT>(F, xv, wv, wv + hM, cv, j, p.r0, p.vmp, gt, Gs, gid, nv,
-                                                    p.tab + p.t.o_csyn, p.t.nc);
-            double* o = ov + v * M;  // the final level reads cfin (C or X) and X: Wb is free
-            constexpr int EL = FiltSmem<NU>::EL;
-            const int mlo = p.vmp ? (EL + 1) >> 1 : 0;
-            const int mhi = p.vmp ? (M - EL) >> 1 : hM;
-            const Taps<NU> tp(F);
-            for (int m = mlo + gt; m < mhi; m += Gs) {
-                double o0, o1;
-                idwt_pair_inner<NU>(tp, cfin, xv + hM, M, m, p.vmp, o0, o1);
-                o[2 * m] = o0;
-                o[2 * m + 1] = o1;
-            }
-            if (p.vmp) {
-                const int nl = 2 * mlo, nr = M - 2 * mhi;
-                for (int k2 = Gs - 1 - gt; k2 < nl + nr; k2 += Gs) {
-                    const int i = k2 < nl ? k2 : 2 * mhi + (k2 - nl);
-                    o[i] = idwt_one<NU>(F, cfin, xv + hM, M, i, true);
-                }
-            }
-        } else {  // analysis levels j .. r0+1 (wavelet.cpp:497-504)
-            double* o = ov + v * M;  // [c_r0 | d_r0 | ... | d_(j-1)]
-            const double* src = xv;
-            const int nc = p.t.nc;
-            const int lstop = nc > 0 ? 31 - __clz(nc) : p.r0;
-            for (int lev = j; lev > lstop; --lev) {
-                const int t = j - lev, n = 1 << lev, half = n >> 1;
-                const bool last = lev == p.r0 + 1;
-                double* dst = last ? o : ((t & 1) ? xv : cv);
-                for (int mm = gt; mm < half; mm += Gs) {
-                    double c, d;
-                    dwt_pair<NU>(F, src, n, mm, p.vmp, c, d);
-                    o[half + mm] = d;
-                    dst[mm] = c;
-                }
-                group_sync<NT>(gid, Gs, nv);
-                src = dst;
-            }
-            if (nc > 0) {
-                const double* cana = p.tab + p.t.o_cana;
-                for (int oo = gt; oo < kNc; oo += Gs) {
-                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll 16
-                    for (int i = 0; i < kNc; i += 4) {
-                        a0 += __ldg(cana + i * kNc + oo) * src[i];
-                        a1 += __ldg(cana + (i + 1) * kNc + oo) * src[i + 1];
-                        a2 += __ldg(cana + (i + 2) * kNc + oo) * src[i + 2];
-                        a3 += __ldg(cana + (i + 3) * kNc + oo) * src[i + 3];
-                    }
-                    o[oo] = (a0 + a1) + (a2 + a3);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    const bool vf = p.ld.vfast();
-    if (vf && p.ld.esh >= 62 && p.ld.vsh >= lV && nv == V) {
-        const int v = tid & (V - 1), i0 = tid >> lV, di = NT >> lV;
-        const long long es = p.ld.es;
-        double* b = p.dst + p.ld.vbase(v0) + v + (long long)i0 * es;
-        const double* od = ov + v * M + i0;
-#pragma unroll 4
-        for (int i = 0; i + i0 < M; i += di) b[(long long)i * es] = od[i];
-        return;
-    }
-    for (int f = tid; f < V * M; f += NT) {
-        const int v = vf ? f & (V - 1) : f >> j;
-        const int i = vf ? f >> lV : f & (M - 1);
-        if (v < nv) p.dst[p.ld.at(v0 + v, i)] = ov[v * M + i];
-    }
-}
-
-// ---------------------------------------------------------------------------
 // wavelet levels in global memory (large path)
 // ---------------------------------------------------------------------------
 
@@ -1039,8 +854,6 @@ __global__ void __launch_bounds__(256) k_wav_coarse(const double* tab, Tables t,
                                                     double* dst, Layout ld, long long dv0,
                                                     long long dst_vs, int r0, int Lc, int inverse,
                                                     int vmp) {
-    pdl_trigger();
-    pdl_wait();
     extern __shared__ double sm[];
     double* filt = sm;
     const int n = 1 << Lc;
@@ -1235,8 +1048,7 @@ __device__ __forceinline__ void warp_syn_windows(const PyrArgs& p, double* wb, i
 // level p.top and hand the top samples to put(i, value).
 template <int NU, class Put>
 __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU>& F, const Taps<NU>& tp,
-                                             double* wb, int v, int lane, bool vmp, Put&& put,
-                                             const double* cb_smem = nullptr, int cb_lo = 0) {
+                                             double* wb, int v, int lane, bool vmp, Put&& put) {
     const int* wlo = reinterpret_cast<const int*>(wb);
     const int* whi = wlo + 32;
     const int* doff = wlo + 64;
@@ -1250,11 +1062,7 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
     const double* cs = p.src_is_x ? xb : p.src + v * p.src_vs;
     {
         const int lo = wlo[p.bot], w = whi[p.bot] - lo, hb = 1 << p.bot;
-        if (cb_smem) {  // the CTA stage's level-bot window (logical indices from cb_lo)
-            for (int t = lane; t < w; t += 32) P[t] = cb_smem[lo + t - cb_lo];
-        } else {
-            for (int t = lane; t < w; t += 32) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
-        }
+        for (int t = lane; t < w; t += 32) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
     }
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {  // details of level lev (half = 2^(lev-1))
         const int lo = wlo[lev - 1], w = whi[lev - 1] - lo, hf = 1 << (lev - 1);
@@ -1289,8 +1097,6 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
 // compute and store phases freely.
 template <int NU>
 __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     extern __shared__ double sm[];
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
@@ -1298,67 +1104,11 @@ __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
     double* wb = sm + FS + wid * (48 + p.wmax + p.wmax2 + p.dsum);
     const int c = blockIdx.x * nw + wid, v = blockIdx.y;
     const bool vmp = p.vmp != 0;
-    const bool cta_stage = p.cbot >= 0 && p.cbot < p.bot;
-    // CTA stage scratch after the warps' areas: ints (48) | P | Q (cwmax) | D (cdsum)
-    double* cw = sm + FS + nw * (48 + p.wmax + p.wmax2 + p.dsum);
-    int* clo = reinterpret_cast<int*>(cw);
-    int* chi = clo + 32;
-    int* cdoff = clo + 64;
-    double* CP = cw + 48;
-    double* CQ = CP + p.cwmax;
-    double* CD = CQ + p.cwmax;
     for (int i = tid; i < FS; i += nt) filt[i] = p.tab[p.t.o_h + i];
     if (lane == 0) warp_syn_windows<NU>(p, wb, c << p.cb, (c + 1) << p.cb, vmp);
-    if (cta_stage && tid == (nw > 1 ? 32 : 0)) {  // the CTA's cone: top range of its warps, down to cbot
-        Win f{(blockIdx.x * nw) << p.cb, (blockIdx.x * nw + nw) << p.cb};
-        for (int lev = p.top; lev > p.bot; --lev) f = syn_need(NU, 1 << lev, f, vmp);
-        for (int lev = p.bot; lev >= p.cbot; --lev) {
-            clo[lev] = f.lo;
-            chi[lev] = f.hi;
-            if (lev > p.cbot) {
-                f = syn_need(NU, 1 << lev, f, vmp);
-                if (f.hi - f.lo > p.cwmax) __trap();
-            }
-        }
-        int off = 0;
-        for (int lev = p.cbot + 1; lev <= p.bot; ++lev) {
-            cdoff[lev] = off;
-            off += chi[lev - 1] - clo[lev - 1];
-        }
-        if (off > p.cdsum) __trap();
-    }
     __syncthreads();  // filters (CTA-wide) and the windows
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
-    const double* xb = p.x + p.lx.vbase(p.xv0 + v);
-    if (cta_stage) {  // coarse levels cbot+1..bot once per CTA (shared by its warps' cones)
-        {
-            const int lo = clo[p.cbot], w = chi[p.cbot] - lo, hb = 1 << p.cbot;
-            for (int t = tid; t < w; t += nt) cp_async8(CP + t, xb + (vmp ? lo + t : ((lo + t) & (hb - 1))));
-        }
-        for (int lev = p.cbot + 1; lev <= p.bot; ++lev) {
-            const int lo = clo[lev - 1], w = chi[lev - 1] - lo, hf = 1 << (lev - 1);
-            for (int t = tid; t < w; t += nt)
-                cp_async8(CD + cdoff[lev] + t, xb + hf + (vmp ? lo + t : ((lo + t) & (hf - 1))));
-        }
-        cp_async_wait_all();
-        __syncthreads();
-        double* P = CP;
-        double* Q = CQ;
-        for (int lev = p.cbot + 1; lev <= p.bot; ++lev) {
-            const int n = 1 << lev, lo = clo[lev], hi = chi[lev];
-            double* q = Q - lo;
-            idwt_window<NU>(F, tp, P, CD + cdoff[lev], clo[lev - 1], n, lo, hi, vmp, tid, nt,
-                            [&](int i, double val) { q[i] = val; });
-            __syncthreads();
-            double* t0 = P;
-            P = Q;
-            Q = t0;
-        }
-        double* ob = p.out + v * p.out_vs;
-        warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) { ob[i] = val; }, P, clo[p.bot]);
-        return;
-    }
     double* ob = p.out + v * p.out_vs;
     warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) { ob[i] = val; });
 }
@@ -1425,8 +1175,6 @@ __device__ __forceinline__ void dwt_coarse_tail(const PyrArgs& p, const FiltSmem
 // the output when bot == r0).  __syncwarp only.
 template <int NU>
 __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     extern __shared__ double sm[];
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
@@ -1596,8 +1344,6 @@ __device__ __forceinline__ void band_vec(const double* __restrict__ gE, const do
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_normal_rows(NormArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     PHASE(0);
     // smem: filters | band edge rows | A, B, C [V][M] each.  A holds the
     // staged input (coarse + every level's details); the synthesis ping-pongs
@@ -1877,8 +1623,6 @@ __global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
     double* L0 = Pb + PM;          // plain buffers of the coarse (<= 2^RLOG) levels
     double* L1 = L0 + NL;
     double* XL = L1 + NL;          // plain copy of the input's first 2^RLOG values
-    pdl_trigger();
-    pdl_wait();
     const int tid = threadIdx.x;
     const bool vmp = p.vmp != 0;
     for (int i = tid; i < FS; i += RNT) filt[i] = p.tab[p.t.o_h + i];
@@ -1978,333 +1722,6 @@ __global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
 }
 
 // ---------------------------------------------------------------------------
-// compact-halo register rows (k_normal_rows_x): k_normal_rows_reg without the
-// shared-memory copies of the register levels.  Every level publishes only
-//   * its segment boundaries -- the first / last HH values of each thread's
-//     segment (Ex: [thread][2 HH + 1], odd stride: conflict free), from which
-//     the neighbours take their window halos, and
-//   * its edge zones -- the first / last EW values of the level (Z: [2][EW]),
-//     from which the threads that OWN the VMP edge samples / rows / band edge
-//     rows compute them (no helper threads, no re-reads after the barrier).
-// Exchange and zone buffers are double-buffered across the one barrier per
-// level.  ~56 KB of shared memory instead of ~110 KB: 3 CTAs per SM.
-// ---------------------------------------------------------------------------
-template <int NU>
-struct NxGeo {
-    static constexpr int OFF = (NU + 1) / 2;       // synthesis window: left reach (coarse)
-    static constexpr int SR = NU + 1 - OFF;        // synthesis window: right reach
-    static constexpr int Bw = 2 * NU - 2;          // band half width
-    static constexpr int WL = NU - 1;              // analysis window reach (fine), both sides
-    static constexpr int m1 = OFF > SR ? OFF : SR;
-    static constexpr int m2 = Bw > WL ? Bw : WL;
-    static constexpr int HH = (m1 > m2 ? m1 : m2) > 0 ? (m1 > m2 ? m1 : m2) : 1;  // halo depth
-    static constexpr int XS = 2 * HH + 1;          // exchange stride per thread
-    static constexpr int EW = 64;                  // edge-zone width (>= 3nu-1, 2nu, E + Bw)
-};
-
-// value g (0 <= g < K * RNT) of a level published with K values per thread
-template <int HH>
-__device__ __forceinline__ double nx_get(const double* ex, int XS, int g, int lk, int K) {
-    const int u = g >> lk, o = g & (K - 1);
-    if (K <= HH || o < HH) return ex[u * XS + o];
-    return ex[u * XS + HH + o - (K - HH)];
-}
-
-// publish this thread's segment v[K] (first / last HH, edge zones of a level of n values)
-template <int HH, int K>
-__device__ __forceinline__ void nx_put(double* ex, int XS, double* z, int EW, int n, const double (&v)[K]) {
-    const int tid = threadIdx.x, g0 = tid * K;
-#pragma unroll
-    for (int o = 0; o < (K < HH ? K : HH); ++o) ex[tid * XS + o] = v[o];
-    if (K > HH) {
-#pragma unroll
-        for (int o = 0; o < HH; ++o) ex[tid * XS + HH + o] = v[K - HH + o];
-    }
-    if (g0 < EW) {
-#pragma unroll
-        for (int o = 0; o < K; ++o)
-            if (g0 + o < EW) z[g0 + o] = v[o];
-    }
-    if (g0 + K > n - EW) {
-#pragma unroll
-        for (int o = 0; o < K; ++o)
-            if (g0 + o >= n - EW) z[EW + g0 + o - (n - EW)] = v[o];
-    }
-}
-
-template <int NU, int J, int RNT>
-__global__ void __launch_bounds__(RNT, 3) k_normal_rows_x(NormArgs p) {
-    constexpr int RLOG = 8;  // levels <= 2^RLOG: plain shared memory (one value per thread at RLOG)
-    static_assert(RNT == (1 << RLOG), "one level-RLOG value per thread");
-    constexpr int M = 1 << J, KT = M / (2 * RNT), FT = 2 * KT;
-    constexpr int FS = FiltSmem<NU>::SIZE, W = 4 * NU - 3, PM = M + M / 32, NL = 1 << RLOG;
-    using X_ = NxGeo<NU>;
-    constexpr int HH = X_::HH, XS = X_::XS, EW = X_::EW, OFF = X_::OFF, Bw = X_::Bw, WL = X_::WL;
-    constexpr int EL = FiltSmem<NU>::EL, CI = FiltSmem<NU>::CI;
-    extern __shared__ double sm[];
-    double* filt = sm;
-    double* gE = sm + FS;
-    double* X = gE + 2 * p.E * W;  // staged input row, padded (coarse + every level's details)
-    double* Ex0 = X + PM;          // boundary exchange, double-buffered
-    double* Ex1 = Ex0 + RNT * XS;
-    double* Z0 = Ex1 + RNT * XS;   // edge zones [2][EW], double-buffered
-    double* Z1 = Z0 + 2 * EW;
-    double* L0 = Z1 + 2 * EW;      // plain buffers of the coarse (<= 2^RLOG) levels
-    double* L1 = L0 + NL;
-    double* XL = L1 + NL;          // plain copy of the input's first 2^RLOG values
-    pdl_trigger();
-    pdl_wait();
-    const int tid = threadIdx.x;
-    const bool vmp = p.vmp != 0;
-    for (int i = tid; i < FS; i += RNT) filt[i] = p.tab[p.t.o_h + i];
-    for (int i = tid; i < 2 * p.E * W; i += RNT) gE[i] = p.band[i];
-    double gI[W];
-#pragma unroll
-    for (int d = 0; d < W; ++d) gI[d] = __ldg(p.band + 2 * p.E * W + d);
-    const long long v = blockIdx.x;
-    const long long es = p.es > 0 ? p.es : 1;
-    const long long vb = p.es > 0 ? (v / p.vpi) * p.ivs + (v % p.vpi) * p.in_vs : v * p.in_vs;
-    const double* xg = p.in + vb;
-    double* out = p.out + (p.es > 0 ? vb : v * p.out_vs);
-#pragma unroll
-    for (int r = 0; r < M / RNT; ++r) cp_async8(X + pidx(tid + r * RNT), xg + (tid + r * RNT) * es);
-    cp_async8(XL + tid, xg + tid * es);
-    cp_async_wait_all();
-    __syncthreads();
-    const FiltSmem<NU> F{filt};
-    const Taps<NU> tp(F);
-    // coarse synthesis levels r0+1 .. RLOG (plain shared memory)
-    const int nc = 1 << p.r0;
-    {
-        const double* src = XL;
-        double* dst = L0;
-        for (int lev = p.r0 + 1; lev <= RLOG; ++lev) {
-            const int n = 1 << lev;
-            idwt_level_vec<NU>(F, src, XL + (n >> 1), dst, n, vmp, tid, RNT);
-            __syncthreads();
-            src = dst;
-            dst = (dst == L0) ? L1 : L0;
-        }
-        // the level-RLOG values, one per thread, published as a register level
-        const double c1[1] = {src[tid]};
-        nx_put<HH, 1>(Ex0, XS, Z0, EW, NL, c1);
-    }
-    __syncthreads();
-    double* exc = Ex0;  // published coarse level (read side)
-    double* zc = Z0;
-    double* exn = Ex1;  // next level (write side)
-    double* zn = Z1;
-    // ---- register synthesis levels RLOG+1 .. J: K coarse values -> 2K fine ----
-    double fine[FT];
-    {
-        double cbuf[KT];  // coarse values of the current level (K of them used)
-        cbuf[0] = exc[tid * XS];  // level RLOG: the thread's own value
-        // unrolled over K = 1, 2, 4, .., KT
-#define NX_SYN_LEVEL(K)                                                                                   \
-        {                                                                                                 \
-            constexpr int kK = (K);                                                                       \
-            constexpr int lk = (kK == 1 ? 0 : kK == 2 ? 1 : kK == 4 ? 2 : kK == 8 ? 3 : kK == 16 ? 4 : 5); \
-            const int half = kK * RNT, n = 2 * half, m0 = tid * kK;                                       \
-            const double* ds = X + pidx(half);                                                            \
-            constexpr int WN = kK + NU + 1;                                                               \
-            double cw[WN], dw[WN];                                                                        \
-            _Pragma("unroll") for (int w = 0; w < WN; ++w) {                                              \
-                int idx = m0 - OFF + w;                                                                   \
-                const bool ok = !vmp || (idx >= 0 && idx < half);                                         \
-                idx &= half - 1;                                                                          \
-                if (w >= OFF && w < OFF + kK) cw[w] = cbuf[w - OFF];                                      \
-                else cw[w] = ok ? nx_get<HH>(exc, XS, idx, lk, kK) : 0.0;                                 \
-                dw[w] = ok ? ds[pidx(idx)] : 0.0;                                                         \
-            }                                                                                             \
-            double f[2 * kK];                                                                             \
-            _Pragma("unroll") for (int q = 0; q < kK; ++q) {                                              \
-                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;                                            \
-                _Pragma("unroll") for (int u = -NU + 1; u <= NU; ++u) {                                   \
-                    if ((u & 1) == 0) {                                                                   \
-                        const int ix = OFF - u / 2 + q;                                                   \
-                        a0 = fma(tp.h[u + NU - 1], cw[ix], a0);                                           \
-                        b0 = fma(tp.g[u + NU - 1], dw[ix], b0);                                           \
-                    } else {                                                                              \
-                        const int ix = OFF - (u - 1) / 2 + q;                                             \
-                        a1 = fma(tp.h[u + NU - 1], cw[ix], a1);                                           \
-                        b1 = fma(tp.g[u + NU - 1], dw[ix], b1);                                           \
-                    }                                                                                     \
-                }                                                                                         \
-                f[2 * q] = a0 + b0;                                                                       \
-                f[2 * q + 1] = a1 + b1;                                                                   \
-            }                                                                                             \
-            if (vmp && (2 * m0 < EL || 2 * m0 + 2 * kK > n - EL)) {  /* owned VMP edge samples */        \
-                _Pragma("unroll") for (int q = 0; q < 2 * kK; ++q) {                                      \
-                    const int i = 2 * m0 + q;                                                             \
-                    if (i < EL || i >= n - EL) {                                                          \
-                        const int side = i < EL ? 0 : 1, ii = side ? n - 1 - i : i;                       \
-                        const double* sc = F.syn(side, ii, 0);                                            \
-                        const double* sd = F.syn(side, ii, 1);                                            \
-                        double e0 = 0.0, e1 = 0.0;                                                        \
-                        _Pragma("unroll") for (int k = 0; k < CI; ++k) {                                  \
-                            const int idx = side ? half - 1 - k : k;                                      \
-                            const double cv = side ? zc[EW + EW - 1 - k] : zc[k];                         \
-                            e0 = fma(sc[k * EL], cv, e0);                                                 \
-                            e1 = fma(sd[k * EL], ds[pidx(idx)], e1);                                      \
-                        }                                                                                 \
-                        f[q] = e0 + e1;                                                                   \
-                    }                                                                                     \
-                }                                                                                         \
-            }                                                                                             \
-            if constexpr (kK < KT) {                                                                      \
-                nx_put<HH, 2 * kK>(exn, XS, zn, EW, n, f);                                                \
-                _Pragma("unroll") for (int q = 0; q < 2 * kK; ++q) cbuf[q] = f[q];                        \
-            } else {                                                                                      \
-                nx_put<HH, 2 * kK>(exn, XS, zn, EW, n, f);                                                \
-                _Pragma("unroll") for (int q = 0; q < 2 * kK; ++q) fine[q] = f[q];                        \
-            }                                                                                             \
-            __syncthreads();                                                                              \
-            { double* t_ = exc; exc = exn; exn = t_; t_ = zc; zc = zn; zn = t_; }                         \
-        }
-        if constexpr (KT >= 1) NX_SYN_LEVEL(1)
-        if constexpr (KT >= 2) NX_SYN_LEVEL(2)
-        if constexpr (KT >= 4) NX_SYN_LEVEL(4)
-        if constexpr (KT >= 8) NX_SYN_LEVEL(8)
-        if constexpr (KT >= 16) NX_SYN_LEVEL(16)
-#undef NX_SYN_LEVEL
-    }
-    // ---- band product in registers (halos and edge rows from the published top level) ----
-    double y[FT];
-    {
-        const int i0 = tid * FT;
-        constexpr int WN = FT + 2 * Bw;
-        constexpr int lk = (FT == 2 ? 1 : FT == 4 ? 2 : FT == 8 ? 3 : FT == 16 ? 4 : 5);
-        double xw[WN];
-#pragma unroll
-        for (int w = 0; w < WN; ++w) {
-            const int idx = i0 - Bw + w;
-            if (w >= Bw && w < Bw + FT) xw[w] = fine[w - Bw];
-            else xw[w] = (!vmp || (idx >= 0 && idx < M)) ? nx_get<HH>(exc, XS, idx & (M - 1), lk, FT) : 0.0;
-        }
-#pragma unroll
-        for (int r = 0; r < FT; ++r) {
-            double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-            for (int d = 0; d < W; ++d) {
-                if (d & 1) a1 = fma(gI[d], xw[r + d], a1);
-                else a0 = fma(gI[d], xw[r + d], a0);
-            }
-            y[r] = a0 + a1;
-        }
-        const int E = p.E;
-        if (i0 < E || i0 + FT > M - E) {  // owned band edge rows: tabulated, inputs from the edge zones
-#pragma unroll
-            for (int r = 0; r < FT; ++r) {
-                const int i = i0 + r;
-                if (i < E || i >= M - E) {
-                    const double* g = gE + (i < E ? i : i - (M - 2 * E)) * W;
-                    double acc = 0.0;
-#pragma unroll
-                    for (int d = 0; d < W; ++d) {
-                        int k = i + d - Bw;
-                        if (!vmp) k &= M - 1;
-                        if (k >= 0 && k < M) acc = fma(g[d], k < EW ? zc[k] : zc[EW + k - (M - EW)], acc);
-                    }
-                    y[r] = acc;
-                }
-            }
-        }
-        nx_put<HH, FT>(exn, XS, zn, EW, M, y);
-        __syncthreads();
-        { double* t_ = exc; exc = exn; exn = t_; t_ = zc; zc = zn; zn = t_; }
-    }
-    // ---- register analysis levels J .. RLOG+1: 2K fine values -> K coarse + K details ----
-    {
-        double xb[FT];
-#pragma unroll
-        for (int q = 0; q < FT; ++q) xb[q] = y[q];
-#define NX_ANA_LEVEL(K)                                                                                   \
-        {                                                                                                 \
-            constexpr int kK = (K);                                                                       \
-            constexpr int l2 = (kK == 1 ? 1 : kK == 2 ? 2 : kK == 4 ? 3 : kK == 8 ? 4 : kK == 16 ? 5 : 6); \
-            const int half = kK * RNT, n = 2 * half, k0 = tid * kK;                                       \
-            constexpr int WN = 2 * kK + 2 * NU - 2;                                                       \
-            double xw[WN];                                                                                \
-            _Pragma("unroll") for (int w = 0; w < WN; ++w) {                                              \
-                int idx = 2 * k0 - WL + w;                                                                \
-                const bool ok = !vmp || (idx >= 0 && idx < n);                                            \
-                idx &= n - 1;                                                                             \
-                if (w >= WL && w < WL + 2 * kK) xw[w] = xb[w - WL];                                       \
-                else xw[w] = ok ? nx_get<HH>(exc, XS, idx, l2, 2 * kK) : 0.0;                             \
-            }                                                                                             \
-            double c[kK], d[kK];                                                                          \
-            _Pragma("unroll") for (int r = 0; r < kK; ++r) {                                              \
-                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;                                            \
-                _Pragma("unroll") for (int u = -NU + 1; u <= NU; ++u) {                                   \
-                    const double xv = xw[2 * r + u + WL];                                                 \
-                    if (u & 1) {                                                                          \
-                        a1 = fma(tp.h[u + NU - 1], xv, a1);                                               \
-                        b1 = fma(tp.g[u + NU - 1], xv, b1);                                               \
-                    } else {                                                                              \
-                        a0 = fma(tp.h[u + NU - 1], xv, a0);                                               \
-                        b0 = fma(tp.g[u + NU - 1], xv, b0);                                               \
-                    }                                                                                     \
-                }                                                                                         \
-                c[r] = a0 + a1;                                                                           \
-                d[r] = b0 + b1;                                                                           \
-            }                                                                                             \
-            if (vmp && (k0 < NU || k0 + kK > half - NU)) {  /* owned VMP edge rows (wavelet.cpp:403-445) */ \
-                _Pragma("unroll") for (int r = 0; r < kK; ++r) {                                          \
-                    const int k = k0 + r;                                                                 \
-                    if (k < NU || k >= half - NU) {                                                       \
-                        const int side = k < NU ? 0 : 1, m = side ? half - 1 - k : k;                     \
-                        const double* ra = F.ana(side, 0, m);                                             \
-                        const double* rb = F.ana(side, 1, m);                                             \
-                        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;                                    \
-                        _Pragma("unroll") for (int q = 0; q < EL; ++q) {                                  \
-                            const double xv = side ? zc[EW + EW - 1 - q] : zc[q];                         \
-                            if (q & 1) {                                                                  \
-                                a1 = fma(ra[q], xv, a1);                                                  \
-                                b1 = fma(rb[q], xv, b1);                                                  \
-                            } else {                                                                      \
-                                a0 = fma(ra[q], xv, a0);                                                  \
-                                b0 = fma(rb[q], xv, b0);                                                  \
-                            }                                                                             \
-                        }                                                                                 \
-                        c[r] = a0 + a1;                                                                   \
-                        d[r] = b0 + b1;                                                                   \
-                    }                                                                                     \
-                }                                                                                         \
-            }                                                                                             \
-            double* od = out + (half + k0) * es;                                                          \
-            _Pragma("unroll") for (int r = 0; r < kK; ++r) od[r * es] = d[r];                             \
-            if constexpr (kK > 1) {                                                                       \
-                nx_put<HH, kK>(exn, XS, zn, EW, half, c);                                                 \
-                _Pragma("unroll") for (int r = 0; r < kK; ++r) xb[r] = c[r];                              \
-                __syncthreads();                                                                          \
-                { double* t_ = exc; exc = exn; exn = t_; t_ = zc; zc = zn; zn = t_; }                     \
-            } else {                                                                                      \
-                L0[tid] = c[0];                                                                           \
-                __syncthreads();                                                                          \
-            }                                                                                             \
-        }
-        if constexpr (KT >= 16) NX_ANA_LEVEL(16)
-        if constexpr (KT >= 8) NX_ANA_LEVEL(8)
-        if constexpr (KT >= 4) NX_ANA_LEVEL(4)
-        if constexpr (KT >= 2) NX_ANA_LEVEL(2)
-        NX_ANA_LEVEL(1)
-#undef NX_ANA_LEVEL
-    }
-    // coarse analysis levels RLOG .. r0+1 (plain shared memory)
-    double* cur = L0;
-    double* nxt = L1;
-    for (int lev = RLOG; lev > p.r0; --lev) {
-        const int n = 1 << lev, half = n >> 1;
-        dwt_level_vec<NU>(F, tp, cur, nxt, out + half * es, n, vmp, tid, RNT, es);
-        __syncthreads();
-        double* t0 = cur;
-        cur = nxt;
-        nxt = t0;
-    }
-    for (int i = tid; i < nc; i += RNT) out[i * es] = cur[i];
-}
-
-// ---------------------------------------------------------------------------
 // large path: two-pass Hadamard over K with an L2-resident intermediate
 // ---------------------------------------------------------------------------
 // G per vector: [2^kh chunks][R1 physical rows][CW]; chunk c = K_hi (forward
@@ -2312,8 +1729,6 @@ __global__ void __launch_bounds__(RNT, 3) k_normal_rows_x(NormArgs p) {
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     // the contiguous pass's tile rows are unpadded (RS = CW): its lane patterns walk
     // columns only, and the tile is then byte-for-byte the chunk's G block
@@ -2374,71 +1789,8 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p)
     }
 }
 
-// Forward pass 1 fused with the top synthesis levels: the CTA's nw warps
-// synthesise the chunk's R1*B samples of xi (plus the H-sample halos of the
-// neighbouring chunks, computed redundantly by the first / last warp) straight
-// into the extended tile -- xi never goes through HBM -- then H over the low
-// kl bits of K and the G store as in k_large_fwd1.
-template <int NU>
-__global__ void __launch_bounds__(512, 1) k_large_fwd1_syn(LargeArgs a, PyrArgs p) {
-    using Gm = Geo<NU, kLogB>;
-    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = Gm::RS;
-    constexpr int FS = FiltSmem<NU>::SIZE;
-    extern __shared__ double sm[];
-    pdl_trigger();
-    pdl_wait();
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x, nw = nt >> 5;
-    const int j = a.j, M = 1 << j, A = 1 << (j - kLogB);
-    const int kl = a.kl, R1 = 1 << kl;
-    const int chunk = blockIdx.x, v = blockIdx.y;
-    const bool vmp = p.vmp != 0;
-    double* filt = sm;
-    double* T = sm + FS;
-    double* wb = T + R1 * RS + wid * (48 + p.wmax + p.wmax2 + p.dsum);
-    const int base = chunk * R1 * B, span = (R1 * B) / nw;
-    for (int i = tid; i < FS; i += nt) filt[i] = p.tab[p.t.o_h + i];
-    if (lane == 0) {
-        int lo = base + wid * span, hi = lo + span;
-        if (wid == 0) lo = max(0, lo - H);
-        if (wid == nw - 1) hi = min(M, hi + H);
-        warp_syn_windows<NU>(p, wb, lo, hi, vmp);
-    }
-    if (H > 0 && tid < H) {  // halo positions outside the vector are zero
-        if (chunk == 0) T[tid] = 0.0;                                                 // row 0, e < H
-        if (base + R1 * B >= M) T[(int)brev_bits((unsigned)(R1 - 1), kl) * RS + B + H + tid] = 0.0;
-    }
-    __syncthreads();
-    const FiltSmem<NU> F{filt};
-    const Taps<NU> tp(F);
-    warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) {
-        if (NU > 1 && (i < NU || i >= M - NU)) {  // raw edge values; the tile holds 0 there
-            a.ev[(long long)v * 2 * NU + (i < NU ? i : NU + i - (M - NU))] = val;
-            val = 0.0;
-        }
-        const int r = i - base + H;  // position in the chunk's extended range [0, R1 B + 2H)
-        const int rl = r >> kLogB, e = r & (B - 1);
-        if (rl < R1) T[(int)brev_bits((unsigned)rl, kl) * RS + e] = val;
-        if (e < 2 * H && rl >= 1) T[(int)brev_bits((unsigned)(rl - 1), kl) * RS + e + B] = val;
-    });
-    __syncthreads();
-    tile_hadamard<CW, RS, 4>(T, 1, kl, 0, kl, 0, tid, nt);
-    double* g = a.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
-    int e = tid % CW, ph = tid / CW;
-    for (int f = tid; f < R1 * CW; f += nt) {
-        g[f] = T[ph * RS + e];
-        e += nt % CW;
-        ph += nt / CW;
-        if (e >= CW) {
-            e -= CW;
-            ++ph;
-        }
-    }
-}
-
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
@@ -2502,15 +1854,13 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
         for (int nl = 0; nl < B; ++nl) {
             const unsigned x = brev_c5(nl);
             const int gx = (int)gray_inv_c(x);
-            ((__popc(x) & 1) ? po : pe)[(long long)gx * stp] = z[nl];
+            __stcs(((__popc(x) & 1) ? po : pe) + (long long)gx * stp, z[nl]);  // evict-first: streamed out
         }
     }
 }
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
     extern __shared__ double sm[];
@@ -2543,7 +1893,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 #pragma unroll
             for (int nl = 0; nl < B; ++nl) {
                 const unsigned x = brev_c(nl, kLogB);
-                y[nl] = __ldg(((__popc(x) & 1) ? po : pe) + (long long)gray_inv_c(x) * step);
+                y[nl] = __ldcs(((__popc(x) & 1) ? po : pe) + (long long)gray_inv_c(x) * step);  // streamed once
             }
         } else {
 #pragma unroll
@@ -2600,8 +1950,6 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p) {
-    pdl_trigger();  // let the next launch in the stream get resident during our tail
-    pdl_wait();     // the previous launch's results are visible from here on
     using Gm = Geo<NU, kLogB>;
     // unpadded tile rows (RS = CW): the chunk's G block loads as one 16-byte copy
     constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = CW, NP = Gm::NP;

@@ -12,20 +12,7 @@
 
 namespace cww {
 
-// Kernel launch, optionally with programmatic stream serialization (PDL,
-// CWW_PDL=1): the next kernel of a chain is scheduled while this one's last
-// wave drains; kernels order their memory accesses with griddepcontrol.wait
-// (cww_device.cuh).  Off by default: measured on B200 it did not pay (config
-// 2: 0.280 vs 0.274 ms, config 3: 2.96 vs 2.69 ms per step) -- the waiting
-// dependents hold SM slots the primary's tail could use.
-inline bool pdl_enabled() {
-    static const bool v = [] {
-        const char* e = std::getenv("CWW_PDL");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
+// Kernel launch through cudaLaunchKernelEx (typed arguments).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
     cudaLaunchConfig_t cfg{};
@@ -33,13 +20,6 @@ cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    if (pdl_enabled()) {
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-    }
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
@@ -88,8 +68,8 @@ struct LargeArgs {
 };
 
 struct WavArgs {
-    int kind;  // 0: coarse levels (one CTA per vector, shared memory); 1: panel (V vectors per CTA, all levels)
-    int V;     // kind 1: vectors per CTA
+    int kind;  // 0: coarse levels (one CTA per vector, shared memory)
+    int V;
     const double* tab;
     Tables t;
     long long nvec;
@@ -125,10 +105,6 @@ struct PyrArgs {
     int wmax;  // window buffer length (doubles), from pyr_wmax_*: the larger ping-pong slot
     int wmax2; // the other ping-pong slot (levels alternate: about half of wmax)
     int dsum;  // synthesis: total detail-window length over all levels
-    // synthesis only: levels cbot+1..bot run once per CTA (its cone over the CTA's
-    // top range) before the warp cones start at level bot; cbot < 0 disables.
-    // cwmax / cdsum: the CTA stage's window and detail-window sizes.
-    int cbot, cwmax, cdsum;
     const double* x;
     Layout lx;
     long long xv0;
@@ -146,9 +122,6 @@ struct PyrArgs {
 };
 
 cudaError_t launch_pyr(int nu, bool analysis, const PyrArgs& a, cudaStream_t st);
-// forward pass 1 fused with the last synthesis pyramid (top = j); smem query (-1: n/a)
-cudaError_t launch_fwd1_syn(int nu, const LargeArgs& a, const PyrArgs& p, cudaStream_t st);
-long long fwd1_syn_smem(int nu, int kl, const PyrArgs& p);
 
 // Normal form of the full-mask operator along one axis (SURVEY.md 8d "K10
 // normal-op form"): U* U = sum_s (D_s + E_s)^T H^T H (D_s + E_s) and H^T H =
@@ -175,6 +148,9 @@ cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st);
 bool normal_reg_ok(int nu, int j, int r0, int use_idwt);
 // Batched out-of-place transpose of n x n fp64 matrices (matrix stride n*n).
 cudaError_t launch_transpose(const double* in, double* out, long long n, long long batch, cudaStream_t st);
+// Batched out-of-place transpose of rows x cols matrices (out: cols x rows).
+cudaError_t launch_transpose_rect(const double* in, double* out, long long rows, long long cols, long long batch,
+                                  cudaStream_t st);
 
 // Largest window (over all CTAs and levels) of a synthesis pyramid producing
 // chunks of 2^cb samples of level top from level bot.
@@ -200,26 +176,6 @@ inline int pyr_wmax_syn(int nu, int top, int bot, int cb, bool vmp, int* dsum, i
         return wm[0];
     }
     return wm[0] > wm[1] ? wm[0] : wm[1];
-}
-
-// CTA coarse stage of a synthesis pyramid: windows of levels cbot..bot for the
-// cone of top-level chunks of 2^ccb samples (ccb = cb + log2(warps per CTA)).
-inline int pyr_wmax_cta(int nu, int top, int bot, int cbot, int ccb, bool vmp, int* dsum) {
-    int wm = 1, ds = 1;
-    for (long long c = 0; c < (1ll << (top - ccb)); ++c) {
-        Win f{int(c << ccb), int((c + 1) << ccb)};
-        for (int lev = top; lev > bot; --lev) f = syn_need(nu, 1 << lev, f, vmp);
-        if (f.hi - f.lo > wm) wm = f.hi - f.lo;
-        int sum = 0;
-        for (int lev = bot; lev > cbot; --lev) {
-            f = syn_need(nu, 1 << lev, f, vmp);
-            if (f.hi - f.lo > wm) wm = f.hi - f.lo;
-            sum += f.hi - f.lo;
-        }
-        if (sum > ds) ds = sum;
-    }
-    *dsum = ds;
-    return wm;
 }
 
 // Same for an analysis pyramid (steps top..bot+1, chunks of 2^cb at level top);

@@ -4,7 +4,6 @@
 #pragma once
 #include "cww_kernels.cuh"
 
-#include <cstdlib>
 
 #ifndef CWW_NU
 #error "define CWW_NU before including cww_nu_impl.cuh"
@@ -118,8 +117,7 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     } else {
-        long long smem = (FS + (long long)nw * (48ll + a.wmax + a.wmax2 + a.dsum)) * 8;
-        if (a.cbot >= 0 && a.cbot < a.bot) smem += (48 + 2ll * a.cwmax + a.cdsum) * 8;  // CTA coarse stage
+        const long long smem = (FS + (long long)nw * (48ll + a.wmax + a.wmax2 + a.dsum)) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_idwt_wpyr<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -131,20 +129,10 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
 cudaError_t CWW_FN(launch_normal_rows_nu)(const NormArgs& a, cudaStream_t st) {
     const long long smem = (FiltSmem<CWW_NU>::SIZE + 2ll * a.E * (4 * CWW_NU - 3) + 3ll * a.V * (1ll << a.j)) * 8;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    static const int nt = [] {
-        const char* e = std::getenv("CWW_NORMAL_NT");
-        return e && std::atoi(e) == 512 ? 512 : 256;
-    }();
     const unsigned grid = (unsigned)((a.nvec + a.V - 1) / a.V);
-    if (nt == 256) {
-        auto k = k_normal_rows<CWW_NU, 256>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (cudaError_t e = launch_k(k, grid, 256, smem, st, a); e != cudaSuccess) return e;
-    } else {
-        auto k = k_normal_rows<CWW_NU, 512>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (cudaError_t e = launch_k(k, grid, 512, smem, st, a); e != cudaSuccess) return e;
-    }
+    auto k = k_normal_rows<CWW_NU, 256>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaError_t e = launch_k(k, grid, 256, smem, st, a); e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -162,46 +150,8 @@ cudaError_t normal_reg_t(const NormArgs& a, cudaStream_t st) {
 }
 }  // namespace
 
-namespace {
-template <int J>
-cudaError_t normal_x_t(const NormArgs& a, cudaStream_t st) {
-    using X_ = NxGeo<CWW_NU>;
-    const long long smem = (FiltSmem<CWW_NU>::SIZE + 2ll * a.E * (4 * CWW_NU - 3) + ((1 << J) + (1 << J) / 32) +
-                            2ll * 256 * X_::XS + 4ll * X_::EW + 3ll * 256) * 8;
-    auto k = k_normal_rows_x<CWW_NU, J, 256>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaError_t e = launch_k(k, dim3((unsigned)a.nvec), dim3(256), (size_t)smem, st, a); e != cudaSuccess)
-        return e;
-    return cudaGetLastError();
-}
-}  // namespace
-
 // register-resident variant: use_idwt, 2^9 <= M <= 2^12, r0 < kRegLog
 cudaError_t CWW_FN(launch_normal_rows_reg_nu)(const NormArgs& a, cudaStream_t st) {
-    static const bool nx = [] {  // compact-halo variant (k_normal_rows_x, opt-in: measured even)
-        const char* e = std::getenv("CWW_NORMAL_X");
-        return e && e[0] == '1';
-    }();
-    if (nx && a.E + NxGeo<CWW_NU>::Bw <= NxGeo<CWW_NU>::EW && a.j >= 9 && a.j <= 12) {
-        switch (a.j) {
-            case 9: return normal_x_t<9>(a, st);
-            case 10: return normal_x_t<10>(a, st);
-            case 11: return normal_x_t<11>(a, st);
-            default: return normal_x_t<12>(a, st);
-        }
-    }
-    static const int rnt = [] {
-        const char* e = std::getenv("CWW_NORMAL_RNT");
-        return e && std::atoi(e) == 512 ? 512 : 256;
-    }();
-    if (rnt == 512 && a.j >= 10 && a.r0 < 9) {
-        switch (a.j) {
-            case 10: return normal_reg_t<10, 512>(a, st);
-            case 11: return normal_reg_t<11, 512>(a, st);
-            case 12: return normal_reg_t<12, 512>(a, st);
-            default: break;
-        }
-    }
     switch (a.j) {
         case 9: return normal_reg_t<9, 256>(a, st);
         case 10: return normal_reg_t<10, 256>(a, st);
@@ -211,40 +161,9 @@ cudaError_t CWW_FN(launch_normal_rows_reg_nu)(const NormArgs& a, cudaStream_t st
     }
 }
 
-// forward pass 1 fused with the top synthesis levels (warp cones of 512 samples)
-cudaError_t CWW_FN(launch_fwd1_syn_nu)(const LargeArgs& a, const PyrArgs& p, cudaStream_t st) {
-    using Gm = Geo<CWW_NU, kLogB>;
-    const int R1 = 1 << a.kl, kh = (a.j - kLogB) - a.kl;
-    const int nw = R1 * Gm::B / 512;
-    if (nw < 1 || nw > 16) return cudaErrorInvalidConfiguration;
-    const long long smem =
-        (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48ll + p.wmax + p.wmax2 + p.dsum)) * 8;
-    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    auto k = k_large_fwd1_syn<CWW_NU>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaError_t e = launch_k(k, dim3(1u << kh, (unsigned)a.nvec), dim3(32 * nw), (size_t)smem, st, a, p);
-        e != cudaSuccess)
-        return e;
-    return cudaGetLastError();
-}
-
-long long CWW_FN(fwd1_syn_smem_nu)(int kl, const PyrArgs& p) {
-    using Gm = Geo<CWW_NU, kLogB>;
-    const int R1 = 1 << kl, nw = R1 * Gm::B / 512;
-    if (nw < 1 || nw > 16) return -1;
-    return (FiltSmem<CWW_NU>::SIZE + (long long)R1 * Gm::RS + (long long)nw * (48ll + p.wmax + p.wmax2 + p.dsum)) * 8;
-}
-
 cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
     const int nt = 256;
-    if (w.kind == 1) {
-        const long long smem = panel_wav_smem_bytes(FiltSmem<CWW_NU>::SIZE, w.V, w.lev);
-        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-        auto k = k_panel_wav<CWW_NU, 256>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const unsigned grid = (unsigned)((w.nvec + w.V - 1) / w.V);
-        if (cudaError_t e = launch_k(k, dim3(grid), dim3(256), (size_t)smem, st, w); e != cudaSuccess) return e;
-    } else if (w.kind == 0) {
+    if (w.kind == 0) {
         long long smem = (FiltSmem<CWW_NU>::SIZE + 3 * (1ll << w.lev)) * 8;
         auto k = k_wav_coarse<CWW_NU>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

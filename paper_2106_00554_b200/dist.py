@@ -126,10 +126,11 @@ def gather_cols(local: torch.Tensor, group=None) -> torch.Tensor:
 
 
 def cuda_normal_1d(op) -> Callable[[torch.Tensor], torch.Tensor]:
-    """The production local normal pass: rows <- N1 rows in place (1D op)."""
+    """The production local normal pass: returns N1 applied to every row (1D
+    op); the caller's tensor is not modified (cww_normal works in place on a
+    copy)."""
     def f(v: torch.Tensor) -> torch.Tensor:
-        v = v.contiguous()
-        return op.normal(v, iters=1)
+        return op.normal(v.clone(memory_format=torch.contiguous_format), iters=1)
     return f
 
 

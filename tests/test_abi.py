@@ -41,7 +41,7 @@ def _desc(**kw):
 @pytest.mark.parametrize("kw,status", [
     (dict(nu=7), 3), (dict(nu=0), 3), (dict(nu=1, boundary=1), 3), (dict(nu=1, family=1, boundary=0), 3),
     (dict(nu=4, j=2), 3), (dict(nu=2, q=0), 3), (dict(dim=3), 3), (dict(nu=4, j=6, min_level=2), 3),
-    (dict(nu=2, j=5, min_level=6), 3), (dict(family=5), 1), (dict(nu=2, j=14, dim=2), 7),
+    (dict(nu=2, j=5, min_level=6), 3), (dict(family=5), 1), (dict(nu=2, j=17, q=1, dim=2), 7),
 ])
 def test_spec_validation(kw, status):
     import paper_2106_00554_b200 as cw

@@ -96,13 +96,6 @@ def test_parity_2d(orc, cuda, case, use_idwt):
         assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL
 
 
-@pytest.mark.parametrize("case", [c for c in TWO_D if c[3] >= 8], ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d" % c)
-def test_parity_2d_panel_wavelets(orc, cuda, case, monkeypatch):
-    # column wavelet transforms hoisted into a separate panel pass (CWW_HOIST_COLWAV=1)
-    monkeypatch.setenv("CWW_HOIST_COLWAV", "1")
-    test_parity_2d(orc, cuda, case, 1)
-
-
 # large-M path (two-pass Hadamard with the L2-resident intermediate)
 LARGE = [(0, 4, 1, 14, 1, 1, 4), (0, 2, 1, 15, 2, 1, 3), (0, 4, 1, 16, 2, 1, 4), (0, 3, 0, 14, 1, 1, -1),
          (1, 6, 1, 15, 1, 1, -1), (0, 1, 0, 14, 1, 1, 1), (0, 5, 1, 17, 1, 1, -1),
@@ -275,28 +268,6 @@ def test_normal_form_matches_forward_adjoint(orc, cuda, case, use_idwt, iters):
     assert rel(host(got)[0], z) <= 1e-12
 
 
-def test_normal_form_compact_halo_kernel(cuda):
-    """The opt-in compact-halo normal-rows kernel (CWW_NORMAL_X=1, read once per
-    process) against repeated adjoint(forward(x)): run in a child process."""
-    import subprocess
-    import sys
-    code = (
-        "import sys; sys.path.insert(0, %r)\n"
-        "import torch, paper_2106_00554_b200 as cw\n"
-        "for fam, nu, bnd, j, q, dim, r0 in [(0, 2, 1, 12, 1, 2, 3), (0, 4, 1, 10, 2, 1, 4), (1, 3, 0, 9, 1, 1, -1),\n"
-        "                                   (0, 6, 1, 11, 1, 1, 5), (0, 2, 0, 12, 1, 1, 2)]:\n"
-        "    op = cw.ComposedOp(cw.FastOp(cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd)), j, q, dim), None, True, r0)\n"
-        "    x = torch.randn((2, op.cols()), dtype=torch.float64, device='cuda')\n"
-        "    want = op.adjoint(op.forward(op.adjoint(op.forward(x))))\n"
-        "    got = op.normal(x.clone(), iters=2)\n"
-        "    e = float(torch.linalg.norm(got - want) / torch.linalg.norm(want))\n"
-        "    assert e <= 1e-12, (fam, nu, bnd, j, e)\n"
-        "print('ok')\n") % REPO
-    env = dict(os.environ, CWW_NORMAL_X="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
-
-
 @pytest.mark.parametrize("j,q,dim", [(10, 1, 1), (16, 2, 1), (6, 1, 2)])
 def test_cuda_graph_capture(cuda, j, q, dim):
     """cww_forward / cww_adjoint are capturable into a CUDA graph (stream-ordered
@@ -378,7 +349,10 @@ def test_fwht(orc, cuda, bits):
 
 @pytest.mark.parametrize("nu,bnd,j,r0,dim", [(2, 1, 7, 3, 1), (4, 1, 9, 4, 1), (3, 0, 8, -1, 1),
                                              (1, 0, 10, 0, 1), (6, 1, 8, -1, 1), (2, 1, 5, 3, 2),
-                                             (4, 1, 6, 4, 2)])
+                                             (4, 1, 6, 4, 2),
+                                             # the large-M route (warp pyramids): any j, as dwt_apply
+                                             (3, 1, 16, 4, 1), (2, 1, 21, 3, 1), (4, 0, 17, -1, 1),
+                                             (1, 0, 14, 0, 1), (5, 1, 13, 11, 1), (2, 1, 13, 3, 2)])
 def test_dwt(orc, cuda, nu, bnd, j, r0, dim):
     cw = _cw()
     spec = cw.WaveletSpec(cw.Family.Daubechies, nu, cw.Boundary(bnd))
