@@ -619,6 +619,9 @@ struct cww_op {
         double* d = nullptr;
     };
     std::shared_ptr<Gram> gram = std::make_shared<Gram>();
+    // side streams of the large path's slice pipeline (created on first use,
+    // non-blocking; every call forks onto them from the caller's stream and
+    // joins back, so they are only ordering, never shared state)
 };
 
 namespace {
@@ -976,17 +979,14 @@ LargePlan large_plan(unsigned j) {
     return {kl, ng, ng_adj};
 }
 
-// Vectors per slice of the large path: the whole chain (pyramids, pass 1,
-// pass 2) runs slice by slice so that the intermediates (xi, the Hadamard
-// intermediate G, the pyramid levels) of one slice stay L2-resident and only
-// the path's own inputs and outputs stream through HBM.
+// Vectors per slice of the large path: whole batches per launch (the
+// passes need the full grid to stream; L2-sized slices, also pipelined over
+// 2-6 side streams, measured 13-38% slower at config 3), split
+// only to bound the intermediates' memory (w0, w1, G) to 4 GiB.
 long long large_slice(const cww_op* op, long long nvec) {
-    static const long long env = env_int("CWW_LARGE_SLICE", 0);
-    if (env > 0) return std::min(env, nvec);
     const long long M = op->M, A = M >> cww::kLogB, CW = 32 + 2 * (op->nu - 1);
-    const long long per = 8 * (2 * M + A * CW);  // w0 + w1 + G per vector
-    const long long budget = 40ll << 20;
-    return std::max(1ll, std::min(nvec, budget / per));
+    const long long per = 8 * (2 * M + A * CW);
+    return std::max(1ll, std::min(nvec, (4ll << 30) / per));
 }
 
 struct LargeBufs {
