@@ -1781,41 +1781,41 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p)
     }
     tile_hadamard_inl<CW, RS, CWW_CONTIG_MAXR>(T, 1, kl, 0, kl, 0, tid, NT);
     double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
-    {  // tile == G block: 16-byte copy
-        static_assert(CW % 2 == 0, "16-byte G stores");
-        const double2* t2 = reinterpret_cast<const double2*>(T);
-        double2* g2 = reinterpret_cast<double2*>(g);
-        for (int f = tid; f < R1 * CW / 2; f += NT) g2[f] = t2[f];
+    // tile == G block: one bulk store (TMA engine) once every thread's last
+    // Hadamard writes are visible to the async proxy
+    static_assert(CW % 2 == 0, "16-byte bulk G stores");
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+        bulk_s2g(g, T, (unsigned)(R1 * CW * 8));
+        bulk_commit();
+        bulk_wait_read();
     }
 }
 
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
-    constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
+    constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RSL, NP = Gm::NP;
     extern __shared__ double sm[];
     const int tid = threadIdx.x;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
     const int kl = p.kl, R1 = 1 << kl, kh = a - kl, R2 = 1 << kh;
     const int NG = p.ng, lng = 31 - __clz(NG);
     const int rho0 = blockIdx.x * NG, v = blockIdx.y;
-    double* ES = sm;                // [S][2NP]
-    double* T = sm + S * 2 * NP;    // NG tiles of R2 physical rows
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm);  // G rows landed
+    double* ES = sm + 2;            // [S][2NP]
+    double* T = ES + S * 2 * NP;    // NG tiles of R2 physical rows (16-byte aligned rows)
     const int tst = R2 * RS;
     const double* g = p.G + (long long)v * A * CW;
-    {
-        int e = tid % CW, rest = tid / CW;  // (f % CW, f / CW), stepped without division
-        for (int f = tid; f < NG * R2 * CW; f += NT) {
-            const int ng = rest & (NG - 1), khi = rest >> lng;  // NG = 2^lng
-            const int ph = (int)brev_bits((unsigned)khi, kh);
-            cp_async8(T + ng * tst + ph * RS + e, g + ((long long)khi * R1 + rho0 + ng) * CW + e);
-            e += NT % CW;
-            rest += NT / CW;
-            if (e >= CW) {
-                e -= CW;
-                ++rest;
-            }
-        }
+    if (tid == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (tid == 0) mbar_arrive_expect(bar, (unsigned)(NG * R2 * CW * 8));
+    // one bulk copy (TMA engine) per G row: row (khi, rho0 + ng) -> physical row bitrev(khi) of sub-tile ng
+    for (int f = tid; f < NG * R2; f += NT) {
+        const int ng = f & (NG - 1), khi = f >> lng;  // NG = 2^lng
+        const int ph = (int)brev_bits((unsigned)khi, kh);
+        bulk_g2s(T + ng * tst + ph * RS, g + ((long long)khi * R1 + rho0 + ng) * CW, (unsigned)(CW * 8), bar);
     }
     if (NU > 1) {
         for (int f = tid; f < S * 2 * NP; f += NT) {
@@ -1826,7 +1826,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
             ES[f] = acc;
         }
     }
-    cp_async_wait_all();
+    mbar_wait(bar, 0);
     __syncthreads();
     tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
     double* ob = p.out + p.lout.vbase(p.v0 + v);
@@ -1862,7 +1862,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;
-    constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RS, NP = Gm::NP;
+    constexpr int B = Gm::B, CW = Gm::CW, RS = Gm::RSL, NP = Gm::NP;
     extern __shared__ double sm[];
     const int tid = threadIdx.x, lane = tid & 31;
     const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, S = 1 << p.q;
@@ -1935,17 +1935,19 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
         }
     }
     tile_hadamard<CW, RS>(T, NG, kh, 0, kh, tst, tid, NT);
-    // physical row ph of sub-tile ng is logical K_hi = bitrev_kh(ph); one warp
-    // per row, lane = column
+    // physical row ph of sub-tile ng is logical K_hi = bitrev_kh(ph): one bulk
+    // store (TMA engine) per G row once the last Hadamard writes are visible
+    // to the async proxy
+    fence_proxy_async();
+    __syncthreads();
     double* g = p.G + (long long)v * A * CW;
-    const int lane2 = tid & 31;
-    for (int rr = tid >> 5; rr < NG * R2; rr += NT / 32) {
-        const int ng = rr & (NG - 1), khi = rr >> lng;  // NG = 2^lng
-        const double* t = T + ng * tst + (int)brev_bits((unsigned)khi, kh) * RS;
-        double* gr = g + ((long long)khi * R1 + rho0 + ng) * CW;
-        gr[lane2] = t[lane2];
-        if (lane2 < CW - 32) gr[32 + lane2] = t[32 + lane2];
+    for (int f = tid; f < NG * R2; f += NT) {
+        const int ng = f & (NG - 1), khi = f >> lng;  // NG = 2^lng
+        bulk_s2g(g + ((long long)khi * R1 + rho0 + ng) * CW, T + ng * tst + (int)brev_bits((unsigned)khi, kh) * RS,
+                 (unsigned)(CW * 8));
     }
+    bulk_commit();
+    bulk_wait_read();
 }
 
 template <int NU, int NT>
@@ -1959,15 +1961,17 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
     const int kl = p.kl, R1 = 1 << kl;
     const int chunk = blockIdx.x, v = blockIdx.y;
     const int FE = S * 2 * NP;
-    double* Wv = sm;                 // [S][2NP]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm);  // G block landed
+    double* Wv = sm + 2;             // [S][2NP]
     double* nb = Wv + FE;            // [2][H]: neighbour-row halo sums
     double* T = nb + 2 * NU;
     double* red = T + R1 * RS;       // reduction scratch: [NT/32][2H] and [NT/FE][FE]
     const double* g = p.G + (long long)v * A * CW;
-    {
-        static_assert(CW % 2 == 0, "16-byte G loads");
-        const double* gc = g + (long long)chunk * R1 * CW;
-        for (int f = tid; f < R1 * CW / 2; f += NT) cp_async16(T + 2 * f, gc + 2 * f);
+    static_assert(CW % 2 == 0, "16-byte bulk G loads");
+    if (tid == 0) {  // the chunk's G block: one bulk copy (TMA engine)
+        mbar_init(bar, 1);
+        mbar_arrive_expect(bar, (unsigned)(R1 * CW * 8));
+        bulk_g2s(T, g + (long long)chunk * R1 * CW, (unsigned)(R1 * CW * 8), bar);
     }
     // halo contributions from the neighbouring chunks' boundary rows (sums over
     // the physical rows rho of their Hadamard rows; popc is bit-reversal invariant):
@@ -2016,8 +2020,8 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
         for (; sl < p.nslot; sl += nr) a0 += e0[sl * FE];
         red2[r * FE + f] = (a0 + a1) + (a2 + a3);
     }
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();    // (also publishes the barrier's initialisation)
+    mbar_wait(bar, 0);
     if (NU > 1 && tid < 2 * H) {
         double acc = 0.0;
 #pragma unroll

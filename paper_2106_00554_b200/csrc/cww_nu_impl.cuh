@@ -70,9 +70,9 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
     const int S = 1 << a.q;
     dim3 g1(1u << kh, (unsigned)a.nvec), g2((unsigned)(R1 / a.ng), (unsigned)a.nvec);
     long long s1 = ((long long)R1 * Gm::CW) * 8;  // contiguous passes: unpadded tile rows
-    long long s2 = ((long long)a.ng * R2 * Gm::RS + S * 2 * Gm::NP) * 8;
+    long long s2 = (2 + (long long)a.ng * R2 * Gm::RSL + S * 2 * Gm::NP) * 8;  // + mbarrier
     const long long FE = (long long)S * 2 * Gm::NP;
-    long long s1a = s1 + (FE + 2 * CWW_NU + (CWW_NT / 32) * 2 * CWW_NU + (FE > CWW_NT ? FE : CWW_NT)) * 8;
+    long long s1a = s1 + (2 + FE + 2 * CWW_NU + (CWW_NT / 32) * 2 * CWW_NU + (FE > CWW_NT ? FE : CWW_NT)) * 8;
     long long s2a = s2 + (a.cta_red ? (CWW_NT / 32) * FE * 8 : 0);
     switch (which) {
         case 0: {
