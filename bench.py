@@ -30,7 +30,7 @@ Multi-GPU: one process per GPU (torchrun).  Configs 2-4: the fixed global batch
          is sharded across ranks (dist.shard_batch, no data-path collective,
          "scaling": "strong" -- the total work is fixed).  Config 1: independent
          replicas ("weak").  Config 5: rows partitioned, NCCL all-to-all
-         transposes ("strong").
+         transposes through the C ABI (cww_dist_*, "strong").
 """
 from __future__ import annotations
 
@@ -377,9 +377,12 @@ def main():
     if nu == 1:
         op = cw.HaarFullRankOp(j, q, r0)
     elif rowpart:
-        from paper_2106_00554_b200.dist import RowPartitioned2D, cuda_apply_1d, cuda_normal_1d
-        op1 = cw.ComposedOp(cw.FastOp(spec, j, q, 1), None, True, r0)
-        d2 = RowPartitioned2D(1 << j, 1 << (j + q), cuda_apply_1d(op1), apply_normal_1d=cuda_normal_1d(op1))
+        # the C ABI's row-partitioned operator: NCCL grouped send/recv transposes
+        import torch.distributed as dist
+        from paper_2106_00554_b200.dist import NativeRowPartitioned2D, nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        d2 = NativeRowPartitioned2D(spec, j, q, r0, rank=rank, nranks=world, nccl_id=obj[0], device=local)
         op = cw.ComposedOp(cw.FastOp(spec, j, q, dim), None, True, r0)
     else:
         op = cw.ComposedOp(cw.FastOp(spec, j, q, dim), None, True, r0)
@@ -412,7 +415,7 @@ def main():
     def step_device(concurrent=True):
         if rowpart:
             x_rows.copy_(x_rows0)
-            d2.normal(x_rows, CFG5_ITERS)
+            d2.normal(x_rows, CFG5_ITERS)  # in place
         elif is5:
             ao_dev.copy_(x_dev)
             op.normal(ao_dev, iters=CFG5_ITERS, work=fo_dev)
@@ -450,8 +453,8 @@ def main():
         x_dev.copy_(x_pin, non_blocking=True)
         if rowpart:
             x_rows.copy_(x_dev.view(1 << j, 1 << j)[rank * mr:(rank + 1) * mr])
-            xr = d2.normal(x_rows, CFG5_ITERS)
-            ao_pin.view(1 << j, 1 << j)[rank * mr:(rank + 1) * mr].copy_(xr, non_blocking=True)
+            d2.normal(x_rows, CFG5_ITERS)
+            ao_pin.view(1 << j, 1 << j)[rank * mr:(rank + 1) * mr].copy_(x_rows, non_blocking=True)
         else:
             ao_dev.copy_(x_dev)
             op.normal(ao_dev, iters=CFG5_ITERS, work=fo_dev)

@@ -51,7 +51,8 @@ typedef enum {
     CWW_ERR_NCCL = 6,
     CWW_ERR_UNSUPPORTED = 7,
     CWW_ERR_INTERNAL = 8,
-    CWW_ERR_NOT_CONVERGED = 9 /* gs_solve: residual above tolerance at max_iters */
+    CWW_ERR_NOT_CONVERGED = 9, /* gs_solve / cs_solve: no convergence at max_iters  */
+    CWW_ERR_INFEASIBLE = 10    /* cs_solve: eta below the least-squares residual    */
 } cww_status;
 
 typedef enum { CWW_DAUBECHIES = 0, CWW_SYMLET = 1 } cww_family;       /* wavelet.hpp:15 */
@@ -135,6 +136,21 @@ cww_status cww_gs_solve(const cww_op* op, const double* y, size_t y_len, double*
                         size_t batch, double residual_tol, int max_iters, int use_x0, int* iters,
                         double* residuals, void* stream);
 
+/* Compressed-sensing reconstruction (the reference spec's cs_solve, QCBP,
+ * SPEC.md:421-429; its src/reconstruct.cpp is empty):
+ *   min ||x||_1  subject to  ||A x - y||^2 <= eta
+ * with A = this op (typically a masked ComposedOp), by the Chambolle-Pock
+ * primal-dual iteration (step sizes from a power-iteration estimate of
+ * ||A||), for `batch` independent systems (device pointers, batch-major),
+ * starting from x = 0.  Stops when every system's relative iterate change
+ * is <= tol and ||A x - y||^2 <= eta + tol ||y||^2 (checked every 20
+ * iterations); otherwise CWW_ERR_INFEASIBLE when eta is below the
+ * least-squares residual, else CWW_ERR_NOT_CONVERGED (x = last iterate).
+ * residuals (batch doubles, host, may be NULL): ||A x - y||^2. */
+cww_status cww_cs_solve(const cww_op* op, const double* y, size_t y_len, double* x, size_t x_len,
+                        size_t batch, double eta, double tol, int max_iters, int* iters,
+                        double* residuals, void* stream);
+
 /* Host-pointer entry points: a literal drop-in for the reference's span API.
  * Stages through pinned buffers and synchronises before returning. */
 cww_status cww_forward_host(const cww_op* op, const double* x, size_t x_len, double* y,
@@ -190,6 +206,47 @@ cww_status cww_op_edge_terms(const cww_op* op, uint64_t* p, int32_t* col, int64_
  * N(0,1)*2^-level; density < 1: sparse.  n = 2^j (dim 1) or 4^j (dim 2). */
 cww_status cww_synth(int kind, uint64_t seed, unsigned j, int r0, double density, int dim,
                      double* out);
+
+/* ---- multi-GPU ------------------------------------------
+ * The reference's only parallelism is the std::thread fan-out over rows and
+ * columns of FastOp::forward_2d / adjoint_2d (fastop.cpp:179-192).
+ *
+ * Batch sharding over the devices of one box (independent vectors / images,
+ * configs 2-4): one op per listed device; the *_host calls split the batch
+ * into contiguous shards (the first batch % ndev one item longer), run each
+ * on its device from its own host thread and return when all are done. */
+typedef struct cww_multi cww_multi;
+cww_status cww_multi_create(const cww_op_desc* desc, int ndev, const int* devices, cww_multi** out);
+cww_status cww_multi_destroy(cww_multi* mu);
+cww_status cww_multi_forward_host(const cww_multi* mu, const double* x, size_t x_len, double* y,
+                                  size_t y_len, size_t batch);
+cww_status cww_multi_adjoint_host(const cww_multi* mu, const double* y, size_t y_len, double* x,
+                                  size_t x_len, size_t batch);
+
+/* Row-partitioned 2D operator (config 5: one 2^j x 2^j image, rows split over
+ * nranks processes, one GPU each).  desc.dim must be 2 (full mask).  Each
+ * rank holds M/nranks consecutive rows (row-major, device memory on
+ * desc.device).  The separable passes run locally on rows; every pass is
+ * followed by a distributed transpose: local rectangular transpose (blocks
+ * bound for rank q become contiguous) -> grouped ncclSend/ncclRecv of
+ * nranks blocks of (M/nranks)^2 doubles -> unpack kernel.  NCCL is loaded at
+ * run time (libnccl.so.2).  Bootstrap: rank 0 calls cww_nccl_unique_id, the
+ * caller broadcasts the 128 bytes, every rank calls cww_dist_create. */
+typedef struct cww_dist cww_dist;
+cww_status cww_nccl_unique_id(unsigned char* id, size_t len);
+cww_status cww_dist_create(const cww_op_desc* desc, int rank, int nranks, const unsigned char* id,
+                           size_t id_len, cww_dist** out);
+cww_status cww_dist_destroy(cww_dist* d);
+/* rows_per_rank = M / nranks, row_len = M */
+cww_status cww_dist_rows(const cww_dist* d, size_t* rows_per_rank, size_t* row_len);
+/* x_rows <- this rank's rows of (U* U)^iters X (cww_normal of the whole image) */
+cww_status cww_dist_normal(cww_dist* d, double* x_rows, size_t len, int iters, void* stream);
+/* The same partition and exchange with nranks virtual ranks inside one
+ * process on one device (device-copy exchange instead of NCCL; every rank's
+ * phase completes before the next phase starts): the partition logic on a
+ * single GPU.  x_rows[r]: rank r's rows. */
+cww_status cww_dist_create_local(const cww_op_desc* desc, int nranks, cww_dist** out);
+cww_status cww_dist_normal_local(cww_dist* d, double* const* x_rows, size_t len, int iters, void* stream);
 
 /* Instrumentation: when enabled, every kernel launch is bracketed by CUDA
  * events on its own stream; cww_profile_dump synchronises them and writes

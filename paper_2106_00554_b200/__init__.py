@@ -101,6 +101,8 @@ def _load():
     L.cww_adjoint_host_async.argtypes = [vp, dp, sz, dp, sz, sz, vp]
     L.cww_gs_solve.argtypes = [vp, dp, sz, dp, sz, sz, C.c_double, C.c_int, C.c_int,
                                C.POINTER(C.c_int), dp, vp]
+    L.cww_cs_solve.argtypes = [vp, dp, sz, dp, sz, sz, C.c_double, C.c_double, C.c_int,
+                               C.POINTER(C.c_int), dp, vp]
     L.cww_dwt.argtypes = [vp, dp, sz, sz, C.c_int, vp]
     L.cww_fwht.argtypes = [dp, C.c_uint, sz, C.c_int, vp]
     L.cww_sequency_perm.argtypes = [C.c_uint, dp, vp]
@@ -555,6 +557,31 @@ def gs_solve(op, y, residual_tol: float = 1e-10, max_iters: int = 1000, x0=None,
                           float(residual_tol), int(max_iters), 0 if x0 is None else 1, C.byref(it),
                           _np_ptr(res), _stream_ptr(y))
     if rc != 0 and (raise_on_fail or rc != 9):
+        _check(rc)
+    return x, it.value, res
+
+
+def cs_solve(op, y, eta: float, tol: float = 1e-8, max_iters: int = 20000, raise_on_fail: bool = True):
+    """Compressed-sensing reconstruction (SPEC.md cs_solve, QCBP): min ||x||_1
+    subject to ||A x - y||^2 <= eta with A = op (typically a masked
+    ComposedOp), by Chambolle-Pock primal-dual iterations on the GPU
+    (cww_cs_solve), batched over the leading dimension of y (a contiguous
+    float64 CUDA tensor).  Returns (x, iterations, ||A x - y||^2 per system).
+    Raises CwwError status 10 when eta is infeasible (below the least-squares
+    residual) and status 9 at max_iters (unless raise_on_fail is False)."""
+    torch = _torch()
+    h = op._h
+    y = _dev_tensor(y, "cs_solve")
+    if y.numel() % h.nout:
+        raise CwwError("cs_solve: dimension mismatch", 2)
+    batch = y.numel() // h.nout
+    shape = (h.nin,) if y.dim() == 1 else tuple(y.shape[:-1]) + (h.nin,)
+    x = torch.empty(shape, dtype=torch.float64, device=y.device)
+    it = C.c_int(0)
+    res = np.zeros(batch)
+    rc = h.L.cww_cs_solve(h.h, y.data_ptr(), y.numel(), x.data_ptr(), x.numel(), batch, float(eta), float(tol),
+                          int(max_iters), C.byref(it), _np_ptr(res), _stream_ptr(y))
+    if rc != 0 and (raise_on_fail or rc not in (9,)):
         _check(rc)
     return x, it.value, res
 

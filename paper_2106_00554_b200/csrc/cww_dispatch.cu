@@ -147,6 +147,34 @@ cudaError_t launch_transpose(const double* in, double* out, long long n, long lo
     return launch_transpose_rect(in, out, n, n, batch, st);
 }
 
+// Unpack of the distributed transpose: rank r's block arrives as recv[r][i][k]
+// (already transposed by the sender); local row i (length P*m) is the
+// concatenation over r.  Grid-stride over the output in row order (m = 2^lm):
+// reads and writes both run along k, 16 bytes per thread.
+__global__ void k_unpack_blocks(const double2* __restrict__ recv, double2* __restrict__ x, int lm, int P,
+                                long long total2) {
+    const long long m2 = (1ll << lm) >> 1;  // double2 per block row
+    const long long row2 = m2 * P;          // double2 per local row
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < total2;
+         f += (long long)gridDim.x * blockDim.x) {
+        const long long i = f / row2, c = f - i * row2;
+        const long long r = c / m2, k = c - r * m2;
+        x[f] = recv[(r * (m2 << lm)) + i * m2 + k];
+    }
+}
+
+cudaError_t launch_unpack_blocks(const double* recv, double* x, long long m, int P, cudaStream_t st) {
+    int lm = 0;
+    while ((1ll << lm) < m) ++lm;
+    if ((1ll << lm) != m || m < 2) return cudaErrorInvalidValue;
+    const long long total2 = m * m * P / 2;
+    long long blocks = (total2 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_unpack_blocks<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(recv),
+                                                     reinterpret_cast<double2*>(x), lm, P, total2);
+    return cudaGetLastError();
+}
+
 long long large_nslot(int nu, int q, int j, int kl, int ng) {
     const int nt = 256;
     const int kh = (j - kLogB) - kl, R1 = 1 << kl, R2 = 1 << kh;

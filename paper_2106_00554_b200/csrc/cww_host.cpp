@@ -1185,6 +1185,16 @@ cww_status run(const cww_op* op, const double* in, double* out, long long batch,
 extern "C" {
 
 const char* cww_last_error(void) { return g_err.c_str(); }
+}  // extern "C"
+
+// shared with the other host translation units (cww_dist.cpp)
+cww_status cww::set_error(cww_status st, const char* msg) {
+    g_err = msg;
+    return st;
+}
+void cww::note_launches(int n) { g_launches += (unsigned long long)n; }
+
+extern "C" {
 const char* cww_version(void) { return "cww_b200 0.1 (sm_100a)"; }
 
 void cww_op_desc_init(cww_op_desc* d) {
@@ -1694,6 +1704,151 @@ static cww_status host_call(const cww_op* op, const double* in, size_t in_len, d
     if (rs == CWW_OK && e != cudaSuccess) rs = fail(CWW_ERR_CUDA, "%s", cudaGetErrorString(e));
     cudaStreamDestroy(st);
     return rs;
+}
+
+// Compressed-sensing reconstruction (SPEC.md cs_solve, Eq. QCBP; SURVEY.md 8f
+// row f2): min ||z||_1 subject to ||A z - y||^2 <= eta, A = this op (masked
+// ComposedOp in the CS use case), by the Chambolle-Pock primal-dual iteration
+// with F = indicator of the ball ||. - y|| <= sqrt(eta), G = ||.||_1, K = A:
+//   xi  <- prox_{sigma F*}(xi + sigma A zbar) = sigma (1 - min(1, sqrt(eta)/||t||)) t,
+//          t = xi / sigma + A zbar - y                       (Moreau)
+//   z'  <- soft(z - tau A* xi, tau);  zbar <- 2 z' - z
+// tau = sigma = 0.99 / L with L^2 = lambda_max(A* A) from a power iteration.
+// Stops (checked every kCheck iterations) when every system has
+// ||z' - z|| <= tol ||z'|| and ||A z - y||^2 <= eta + tol ||y||^2.
+static cww_status cs_solve(const cww_op* op, const double* y, double* z, long long B, double eta, double tol,
+                           int max_iters, int* iters_out, double* resid_out, cudaStream_t st) {
+    size_t ni, no;
+    cww_op_sizes(op, &ni, &no);
+    const long long nx = (long long)ni, nr = (long long)no;
+    DevBuf zbar, s, xi, w, part, sc;
+    CUDA_TRY(zbar.alloc(size_t(B * nx), st));
+    CUDA_TRY(s.alloc(size_t(B * nx), st));
+    CUDA_TRY(xi.alloc(size_t(B * nr), st));
+    CUDA_TRY(w.alloc(size_t(B * nr), st));
+    const long long nb = std::max(cww::dot_nblk(nx, B), cww::dot_nblk(nr, B));
+    CUDA_TRY(part.alloc(size_t(B * nb), st));
+    CUDA_TRY(sc.alloc(size_t(5 * B), st));  // tt | dz2 | z2 | r2 | y2
+    double *tt = sc.p, *dz2 = sc.p + B, *z2 = sc.p + 2 * B, *r2 = sc.p + 3 * B, *y2 = sc.p + 4 * B;
+    cww_status rs;
+    // L^2 = lambda_max(A* A): power iteration from A* y_0 (||A|| <= ~1, no rescaling needed)
+    double L2 = 1.0;
+    {
+        if ((rs = run(op, y, s.p, 1, true, st)) != CWW_OK) return rs;
+        double prev = 0.0;
+        for (int k = 0; k < 30; ++k) {
+            if ((rs = run(op, s.p, w.p, 1, false, st)) != CWW_OK) return rs;
+            if ((rs = run(op, w.p, zbar.p, 1, true, st)) != CWW_OK) return rs;
+            {
+                Prof pr("cp_vec", st, 4);
+                CUDA_TRY(cww::launch_dot(s.p, s.p, nx, 1, part.p, tt, st));
+                CUDA_TRY(cww::launch_dot(zbar.p, zbar.p, nx, 1, part.p, dz2, st));
+            }
+            double h[2];
+            CUDA_TRY(cudaMemcpyAsync(h, tt, sizeof(double), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(h + 1, dz2, sizeof(double), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (!(h[0] > 0.0)) break;  // A* y = 0: any step size works
+            const double lam = std::sqrt(h[1] / h[0]);
+            std::swap(s.p, zbar.p);
+            if (k > 4 && std::fabs(lam - prev) <= 1e-6 * lam) {
+                L2 = lam;
+                break;
+            }
+            prev = lam;
+            L2 = lam;
+        }
+    }
+    const double L = std::sqrt(std::max(L2, 1e-300)) * 1.02;
+    const double tau = 0.99 / L, sigma = 0.99 / L, seta = std::sqrt(eta);
+    CUDA_TRY(cudaMemsetAsync(z, 0, size_t(B * nx) * sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(zbar.p, 0, size_t(B * nx) * sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(xi.p, 0, size_t(B * nr) * sizeof(double), st));
+    {
+        Prof pr("cp_vec", st, 2);
+        CUDA_TRY(cww::launch_dot(y, y, nr, B, part.p, y2, st));
+    }
+    std::vector<double> h(size_t(4 * B));
+    constexpr int kCheck = 20;
+    int it = 0;
+    bool done = false;
+    auto check = [&]() -> cww_status {
+        if ((rs = run(op, z, w.p, B, false, st)) != CWW_OK) return rs;  // A z - y
+        {
+            Prof pr("cp_vec", st, 7);
+            CUDA_TRY(cww::launch_sub(w.p, w.p, y, B * nr, st));
+            CUDA_TRY(cww::launch_dot(w.p, w.p, nr, B, part.p, r2, st));
+            CUDA_TRY(cww::launch_dot(s.p, s.p, nx, B, part.p, dz2, st));
+            CUDA_TRY(cww::launch_dot(z, z, nx, B, part.p, z2, st));
+        }
+        CUDA_TRY(cudaMemcpyAsync(h.data(), dz2, size_t(4 * B) * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        done = true;
+        for (long long b = 0; b < B; ++b) {
+            const double d2 = h[size_t(b)], zz = h[size_t(B + b)], rr = h[size_t(2 * B + b)],
+                         yy = h[size_t(3 * B + b)];
+            if (resid_out) resid_out[b] = rr;
+            if (!(d2 <= tol * tol * zz) || !(rr <= eta + tol * yy)) done = false;
+        }
+        return CWW_OK;
+    };
+    while (it < max_iters) {
+        if ((rs = run(op, zbar.p, w.p, B, false, st)) != CWW_OK) return rs;  // A zbar
+        {
+            Prof pr("cp_vec", st, 4);
+            CUDA_TRY(cww::launch_cp_dual(xi.p, w.p, y, sigma, seta, nr, B, part.p, tt, st));
+        }
+        if ((rs = run(op, xi.p, s.p, B, true, st)) != CWW_OK) return rs;  // A* xi
+        {
+            Prof pr("cp_vec", st);
+            CUDA_TRY(cww::launch_cp_primal(z, zbar.p, s.p, tau, B * nx, st));
+        }
+        ++it;
+        if (it % kCheck == 0 || it == max_iters) {
+            if ((rs = check()) != CWW_OK) return rs;
+            if (done) break;
+        }
+    }
+    if (iters_out) *iters_out = it;
+    if (done) return CWW_OK;
+    if (it == 0 && (rs = check()) != CWW_OK) return rs;
+    if (done) return CWW_OK;
+    // classify the failure: is eta below the least-squares residual (infeasible)?
+    double worst = 0.0;
+    for (long long b = 0; b < B; ++b) worst = std::max(worst, h[size_t(2 * B + b)]);
+    {
+        DevBuf xl;
+        CUDA_TRY(xl.alloc(size_t(B * nx), st));
+        cww_status g = gs_solve(op, y, xl.p, B, 1e-12, int(std::min<long long>(4 * nx + 100, 100000)), false,
+                                nullptr, nullptr, st);
+        if (g == CWW_OK || g == CWW_ERR_NOT_CONVERGED) {
+            if ((rs = run(op, xl.p, w.p, B, false, st)) != CWW_OK) return rs;
+            CUDA_TRY(cww::launch_sub(w.p, w.p, y, B * nr, st));
+            CUDA_TRY(cww::launch_dot(w.p, w.p, nr, B, part.p, r2, st));
+            std::vector<double> ls(static_cast<size_t>(B));
+            CUDA_TRY(cudaMemcpyAsync(ls.data(), r2, size_t(B) * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            for (long long b = 0; b < B; ++b)
+                if (ls[size_t(b)] > eta * (1.0 + 1e-9) + 1e-300)
+                    return fail(CWW_ERR_INFEASIBLE,
+                                "cs_solve: eta = %.3e is below the least-squares residual %.3e of system %lld", eta,
+                                ls[size_t(b)], b);
+        }
+    }
+    return fail(CWW_ERR_NOT_CONVERGED, "cs_solve: no convergence in %d iterations (residual^2 %.3e, eta %.3e)", it,
+                worst, eta);
+}
+
+cww_status cww_cs_solve(const cww_op* op, const double* y, size_t y_len, double* x, size_t x_len, size_t batch,
+                        double eta, double tol, int max_iters, int* iters, double* residuals, void* stream) {
+    cww_status s = check_lens(op, x_len, y_len, batch, false, "cs_solve");
+    if (s != CWW_OK) return s;
+    if (iters) *iters = 0;
+    if (batch == 0) return CWW_OK;
+    if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    if (max_iters < 0 || !(tol >= 0.0) || !(eta >= 0.0)) return fail(CWW_ERR_INVALID_ARG, "cs_solve: bad parameters");
+    CUDA_TRY(cudaSetDevice(op->device));
+    return cs_solve(op, y, x, (long long)batch, eta, tol, max_iters, iters, residuals, S_(stream));
 }
 
 cww_status cww_gs_solve(const cww_op* op, const double* y, size_t y_len, double* x, size_t x_len,

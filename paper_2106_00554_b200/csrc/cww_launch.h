@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "cww_device.cuh"
+#include "../../include/cww_b200.h"
 
 namespace cww {
 
@@ -144,6 +145,12 @@ struct NormArgs {
     long long vpi, ivs, es;
 };
 cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st);
+// record an error message for cww_last_error() (host translation units)
+cww_status set_error(cww_status st, const char* msg);
+// add n kernel launches to cww_kernel_launches() (host translation units)
+void note_launches(int n);
+// distributed transpose: x[i][r*m + k] = recv[r][i][k] (P blocks of m x m, rows of M = P*m)
+cudaError_t launch_unpack_blocks(const double* recv, double* x, long long m, int P, cudaStream_t st);
 // the register-resident kernel serves this shape (strided layouts need it)
 bool normal_reg_ok(int nu, int j, int r0, int use_idwt);
 // Batched out-of-place transpose of n x n fp64 matrices (matrix stride n*n).
@@ -227,6 +234,12 @@ cudaError_t launch_cgls_flags(const double* gam, const double* s0, double tol, i
                               cudaStream_t st);
 cudaError_t launch_sqrt(const double* a, double* out, long long batch, cudaStream_t st);
 cudaError_t launch_sub_from(double* r, const double* y, long long n, cudaStream_t st);
+// Chambolle-Pock vector algebra (cs_solve): dual prox (tt: per-system ||t||^2),
+// primal soft-threshold step, s = a - b
+cudaError_t launch_cp_dual(double* xi, const double* w, const double* y, double sigma, double sqrt_eta,
+                           long long nr, long long batch, double* part, double* tt, cudaStream_t st);
+cudaError_t launch_cp_primal(double* z, double* zbar, double* s, double tau, long long n, cudaStream_t st);
+cudaError_t launch_sub(double* s, const double* a, const double* b, long long n, cudaStream_t st);
 // Sampling-mask epilogues: gather y[b][i] = full[b][idx[i]] (scatter = false) or
 // scatter full[b][idx[i]] = y[b][i] (scatter = true; full pre-zeroed).
 cudaError_t launch_mask(double* full, long long nfull, const uint64_t* idx, long long cnt, double* y,

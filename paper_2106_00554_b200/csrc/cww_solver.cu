@@ -100,7 +100,65 @@ int grid_x(long long n, long long batch) {
     return (int)(g < cap ? g : cap);
 }
 
+// ---- Chambolle-Pock for QCBP (SPEC.md cs_solve) ----
+// dual, step 1: t = xi / sigma + A zbar - y  (in place in xi)
+__global__ void k_cp_dual_t(double* xi, const double* __restrict__ w, const double* __restrict__ y, double inv_sigma,
+                            long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        xi[i] = fma(xi[i], inv_sigma, w[i] - y[i]);
+}
+// dual, step 2: xi = sigma (1 - min(1, sqrt(eta) / ||t||)) t  (= prox of sigma F*,
+// F the indicator of the ball ||. - y|| <= sqrt(eta), by Moreau's identity)
+__global__ void k_cp_dual_scale(double* xi, const double* tt, double sigma, double sqrt_eta, long long nr) {
+    const long long v = blockIdx.y;
+    const double nt = sqrt(tt[v]);
+    const double c = nt > sqrt_eta ? sqrt_eta / nt : 1.0;
+    const double f = sigma * (1.0 - c);
+    double* x = xi + v * nr;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nr; i += (long long)gridDim.x * blockDim.x)
+        x[i] *= f;
+}
+// primal: z' = soft(z - tau s, tau); zbar = 2 z' - z; s <- z' - z (for the stopping test)
+__global__ void k_cp_primal(double* z, double* zbar, double* s, double tau, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double zo = z[i];
+        const double u = zo - tau * s[i];
+        const double zn = u > tau ? u - tau : (u < -tau ? u + tau : 0.0);
+        z[i] = zn;
+        zbar[i] = 2.0 * zn - zo;
+        s[i] = zn - zo;
+    }
+}
+// s = a - b
+__global__ void k_sub(double* s, const double* __restrict__ a, const double* __restrict__ b, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        s[i] = a[i] - b[i];
+}
+
+unsigned flat_grid(long long n) {
+    long long g = (n + 255) / 256;
+    return (unsigned)(g > 148 * 8 ? 148 * 8 : (g < 1 ? 1 : g));
+}
+
 }  // namespace
+
+cudaError_t launch_cp_dual(double* xi, const double* w, const double* y, double sigma, double sqrt_eta,
+                           long long nr, long long batch, double* part, double* tt, cudaStream_t st) {
+    k_cp_dual_t<<<flat_grid(nr * batch), 256, 0, st>>>(xi, w, y, 1.0 / sigma, nr * batch);
+    if (cudaError_t e = launch_dot(xi, xi, nr, batch, part, tt, st); e != cudaSuccess) return e;
+    k_cp_dual_scale<<<dim3(grid_x(nr, batch), (unsigned)batch), 256, 0, st>>>(xi, tt, sigma, sqrt_eta, nr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cp_primal(double* z, double* zbar, double* s, double tau, long long n, cudaStream_t st) {
+    k_cp_primal<<<flat_grid(n), 256, 0, st>>>(z, zbar, s, tau, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sub(double* s, const double* a, const double* b, long long n, cudaStream_t st) {
+    k_sub<<<flat_grid(n), 256, 0, st>>>(s, a, b, n);
+    return cudaGetLastError();
+}
 
 int dot_nblk(long long n, long long batch) {
     long long per = (n + kRedNT * 8 - 1) / (kRedNT * 8);  // >= 8 elements per thread

@@ -139,3 +139,137 @@ def cuda_apply_1d(op) -> Callable[[torch.Tensor, bool], torch.Tensor]:
     def f(v: torch.Tensor, adjoint: bool) -> torch.Tensor:
         return op.adjoint(v) if adjoint else op.forward(v)
     return f
+
+
+# ---------------------------------------------------------------------------
+# Native multi-GPU entry points (C ABI, csrc/cww_dist.cpp; include/cww_b200.h)
+# ---------------------------------------------------------------------------
+def _native():
+    import ctypes as C
+    from . import _load
+    L = _load()
+    if not getattr(L, "_cww_dist_bound", False):
+        vp, sz = C.c_void_p, C.c_size_t
+        L.cww_nccl_unique_id.argtypes = [C.c_char_p, sz]
+        L.cww_dist_create.argtypes = [vp, C.c_int, C.c_int, C.c_char_p, sz, C.POINTER(vp)]
+        L.cww_dist_create_local.argtypes = [vp, C.c_int, C.POINTER(vp)]
+        L.cww_dist_destroy.argtypes = [vp]
+        L.cww_dist_normal.argtypes = [vp, vp, sz, C.c_int, vp]
+        L.cww_dist_normal_local.argtypes = [vp, C.POINTER(vp), sz, C.c_int, vp]
+        L.cww_multi_create.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(vp)]
+        L.cww_multi_destroy.argtypes = [vp]
+        for n in ("cww_multi_forward_host", "cww_multi_adjoint_host"):
+            getattr(L, n).argtypes = [vp, vp, sz, vp, sz, sz]
+        L._cww_dist_bound = True
+    return L
+
+
+def _desc(spec, j: int, q: int, dim: int, min_level: int, use_idwt: bool, device: int):
+    from . import DATA_DIR, _Desc
+    return _Desc(int(spec.family), spec.nu, int(spec.boundary), j, q, dim, min_level, 1 if use_idwt else 0, 0,
+                 device, DATA_DIR.encode(), None, 0, None, 0)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL bootstrap id (rank 0; broadcast it to the other ranks)."""
+    import ctypes as C
+    from . import _check
+    L = _native()
+    buf = C.create_string_buffer(128)
+    _check(L.cww_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+class NativeRowPartitioned2D:
+    """Config 5 on P GPUs through the C ABI (cww_dist_*): this rank's M/P rows
+    of a 2^j x 2^j coefficient image; `normal` applies (U*U)^iters with the
+    banded normal form per axis and NCCL all-to-all transposes (grouped
+    ncclSend / ncclRecv, pack = local transpose, unpack kernel).
+
+    local=True: `nranks` virtual ranks in this process on one GPU with a
+    device-copy exchange (the partition logic on a single GPU)."""
+
+    def __init__(self, spec, j: int, q: int, min_level: int, rank: int = 0, nranks: int = 1,
+                 nccl_id: Optional[bytes] = None, device: int = 0, use_idwt: bool = True, local: bool = False):
+        import ctypes as C
+        from . import _check
+        L = _native()
+        self.L, self.local, self.nranks, self.rank = L, local, nranks, rank
+        self.M = 1 << j
+        self.m = self.M // nranks
+        d = _desc(spec, j, q, 2, min_level, use_idwt, device)
+        h = C.c_void_p()
+        if local:
+            _check(L.cww_dist_create_local(C.byref(d), nranks, C.byref(h)))
+        else:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nccl_id (128 bytes from nccl_unique_id on rank 0) required")
+            _check(L.cww_dist_create(C.byref(d), rank, nranks, nccl_id, 128, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self.L.cww_dist_destroy(h)
+            self.h = None
+
+    def normal(self, x_rows, iters: int = 1):
+        """In place on this rank's rows (an (M/P, M) contiguous float64 CUDA
+        tensor); local mode: a list of every virtual rank's rows."""
+        import ctypes as C
+        from . import _check
+        if self.local:
+            xs = list(x_rows)
+            for x in xs:
+                assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous() and x.numel() == self.m * self.M
+            arr = (C.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+            _check(self.L.cww_dist_normal_local(self.h, arr, self.m * self.M, iters,
+                                                torch.cuda.current_stream(xs[0].device).cuda_stream))
+            return xs
+        x = x_rows
+        assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous() and x.numel() == self.m * self.M
+        _check(self.L.cww_dist_normal(self.h, x.data_ptr(), x.numel(), iters,
+                                      torch.cuda.current_stream(x.device).cuda_stream))
+        return x
+
+
+class MultiDeviceOp:
+    """Batch sharding over the devices of one box in one process (cww_multi_*):
+    host arrays in, host arrays out; the batch is split into contiguous shards
+    (shard_batch), each run on its device from its own host thread."""
+
+    def __init__(self, spec, j: int, q: int, dim: int, min_level: int, devices, use_idwt: bool = True):
+        import ctypes as C
+        from . import _check
+        L = _native()
+        self.L = L
+        d = _desc(spec, j, q, dim, min_level, use_idwt, -1)
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(L.cww_multi_create(C.byref(d), len(devices), devs, C.byref(h)))
+        self.h = h
+        M, N = 1 << j, 1 << (j + q)
+        self.nin, self.nout = (M, N) if dim == 1 else (M * M, N * N)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self.L.cww_multi_destroy(h)
+            self.h = None
+
+    def _call(self, a, adjoint: bool):
+        import numpy as np
+        from . import _check
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        ni, no = (self.nout, self.nin) if adjoint else (self.nin, self.nout)
+        batch = a.size // ni
+        o = np.empty(a.shape[:-1] + (no,), dtype=np.float64)
+        fn = self.L.cww_multi_adjoint_host if adjoint else self.L.cww_multi_forward_host
+        _check(fn(self.h, a.ctypes.data, a.size, o.ctypes.data, o.size, batch))
+        return o
+
+    def forward(self, x):
+        return self._call(x, False)
+
+    def adjoint(self, y):
+        return self._call(y, True)
