@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 
 #include "cww_device.cuh"
 #include "cww_launch.h"
@@ -209,28 +210,74 @@ __global__ void k_fwht_small(double* v, int bits, int sequency) {
     }
 }
 
-// One radix-2 stage h of a large FWHT in global memory.
-__global__ void k_fwht_stage(double* v, int bits, int hb, long long nvec) {
-    const long long n = 1ll << bits, h = 1ll << hb;
-    const long long tot = nvec * (n >> 1);
-    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
-         f += (long long)gridDim.x * blockDim.x) {
-        long long vv = f / (n >> 1), i = f % (n >> 1);
-        long long lo = ((i >> hb) << (hb + 1)) | (i & (h - 1));
-        double* x = v + vv * n;
-        double a = x[lo], b = x[lo + h];
-        x[lo] = a + b;
-        x[lo + h] = a - b;
-    }
+// Large FWHT (bits > 13): passes over groups of index bits, each a tile of
+// 2^nb rows x W columns in shared memory (element (r, c) <-> index
+// hi * 2^(lo+nb) + r * 2^lo + inner0 + c), radix-2 stages in place in the
+// tile, one HBM read + write per pass:
+//   pass 1: bits [0, 13)      contiguous chunks of 8192 (W = 1),
+//   pass k: bits [lo, lo+10)  2^nb x 8 tiles (64-byte row segments).
+// Sequency order (fwht_sequency, walsh.cpp:88-98: out[n] = nat[bitrev(gray(n))])
+// is fused into the last pass, which covers the top bits: column c's 2^nb
+// results land in one aligned block of 2^nb outputs, n = n0(c) ^
+// gray^-1(bitrev_nb(r)), stored in destination order (coalesced).  Passes
+// run in place except that the sequency result alternates v -> scratch -> v.
+constexpr int kFwhtTileLog = 13;  // doubles per tile: 64 KB
+constexpr int kFwhtLW = 3;        // strided passes: 8 columns
+
+__device__ __forceinline__ unsigned gray_inv_u(unsigned x) {
+    x ^= x >> 1;
+    x ^= x >> 2;
+    x ^= x >> 4;
+    x ^= x >> 8;
+    x ^= x >> 16;
+    return x;
 }
 
-__global__ void k_permute_seq(const double* src, double* dst, int bits, long long nvec) {
-    const long long n = 1ll << bits, tot = nvec * n;
-    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < tot;
-         f += (long long)gridDim.x * blockDim.x) {
-        long long vv = f / n, i = f % n;
-        unsigned g = (unsigned)(i ^ (i >> 1));
-        dst[f] = src[vv * n + brev_bits(g, bits)];
+__global__ void __launch_bounds__(256) k_fwht_pass(const double* __restrict__ src, double* dst, int bits, int lo,
+                                                    int nb, int lw, int seq_out) {
+    extern __shared__ double T[];  // [2^nb rows][W + 1 (odd stride when W > 1)]
+    const int W = 1 << lw, RS = W > 1 ? W + 1 : 1, tid = threadIdx.x, nt = blockDim.x;
+    const long long n = 1ll << bits;
+    const int ninner = lo > lw ? 1 << (lo - lw) : 1;   // column blocks per (vector, hi)
+    const long long nhi = 1ll << (bits - lo - nb);
+    long long blk = blockIdx.x;
+    const long long ib = blk % ninner;
+    blk /= ninner;
+    const long long hi = blk % nhi, v = blk / nhi;
+    const long long base = v * n + hi * (1ll << (lo + nb)) + ib * W;
+    const int R = 1 << nb;
+    for (int f = tid; f < R * W; f += nt) {
+        const int r = f >> lw, c = f & (W - 1);
+        T[r * RS + c] = __ldcs(src + base + ((long long)r << lo) + c);
+    }
+    __syncthreads();
+    for (int hb = 0; hb < nb; ++hb) {
+        const int h = 1 << hb;
+        for (int f = tid; f < (R >> 1) * W; f += nt) {
+            const int i = f >> lw, c = f & (W - 1);
+            const int r0 = ((i >> hb) << (hb + 1)) | (i & (h - 1));
+            const double a = T[r0 * RS + c], b = T[(r0 + h) * RS + c];
+            T[r0 * RS + c] = a + b;
+            T[(r0 + h) * RS + c] = a - b;
+        }
+        __syncthreads();
+    }
+    if (!seq_out) {
+        for (int f = tid; f < R * W; f += nt) {
+            const int r = f >> lw, c = f & (W - 1);
+            dst[base + ((long long)r << lo) + c] = T[r * RS + c];
+        }
+        return;
+    }
+    // last pass (lo + nb == bits): natural index k = r 2^lo + inner, inner = ib W + c;
+    // destination n = gray^-1(bitrev_bits(k)) = n0(c) ^ gray^-1(bitrev_nb(r))
+    for (int f = tid; f < R * W; f += nt) {
+        const int c = f >> nb, t = f & (R - 1);
+        const unsigned inner = (unsigned)(ib * W + c);
+        const unsigned n0 = gray_inv_u(brev_bits(inner, bits));
+        const unsigned u = (unsigned)t ^ (n0 & (unsigned)(R - 1));  // = gray^-1(bitrev_nb(r))
+        const int r = (int)brev_bits(u ^ (u >> 1), nb);             // gray(u), reversed
+        dst[v * n + (long long)((n0 & ~(unsigned)(R - 1)) | (unsigned)t)] = T[r * RS + c];
     }
 }
 
@@ -263,10 +310,28 @@ cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, doub
         k_fwht_small<<<(unsigned)batch, 256, smem, st>>>(v, bits, sequency);
         return cudaGetLastError();
     }
-    for (int hb = 0; hb < bits; ++hb) k_fwht_stage<<<148 * 8, 256, 0, st>>>(v, bits, hb, batch);
-    if (sequency) {
-        k_permute_seq<<<148 * 8, 256, 0, st>>>(v, scratch, bits, batch);
-        cudaMemcpyAsync(v, scratch, (size_t)(batch << bits) * 8, cudaMemcpyDeviceToDevice, st);
+    if (sequency && !scratch) return cudaErrorInvalidValue;
+    // passes: [0, 13) contiguous, then <= 10 bits each with 8-column tiles
+    struct Pass { int lo, nb, lw; };
+    std::vector<Pass> ps{{0, kFwhtTileLog, 0}};
+    for (int lo = kFwhtTileLog; lo < bits;) {
+        const int nb = bits - lo < kFwhtTileLog - kFwhtLW ? bits - lo : kFwhtTileLog - kFwhtLW;
+        ps.push_back({lo, nb, kFwhtLW});
+        lo += nb;
+    }
+    cudaFuncSetAttribute(k_fwht_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    const double* src = v;
+    for (size_t i = 0; i < ps.size(); ++i) {
+        const Pass& p = ps[i];
+        const bool last = i + 1 == ps.size();
+        // sequency: the second-to-last pass writes scratch, the last scatters back into v
+        double* dst = (sequency && i + 2 == ps.size()) ? scratch : v;
+        const int W = 1 << p.lw, RS = W > 1 ? W + 1 : 1;
+        const long long smem = (long long)(1 << p.nb) * RS * 8;
+        const long long blocks = batch * (1ll << (bits - p.lo - p.nb)) * (p.lo > p.lw ? 1ll << (p.lo - p.lw) : 1);
+        if (blocks > 0x7fffffffll) return cudaErrorInvalidValue;
+        k_fwht_pass<<<(unsigned)blocks, 256, smem, st>>>(src, dst, bits, p.lo, p.nb, p.lw, (sequency && last) ? 1 : 0);
+        src = dst;
     }
     return cudaGetLastError();
 }

@@ -2134,7 +2134,7 @@ cww_status cww_fwht(double* v, unsigned bits, size_t batch, int sequency, void* 
     cudaStream_t st = S_(stream);
     DevBuf scr;
     if (bits > 13 && sequency) CUDA_TRY(scr.alloc(size_t(batch) << bits, st));
-    Prof pr("fwht", st, bits <= 13 ? 1 : int(bits) + (sequency ? 1 : 0));
+    Prof pr("fwht", st, bits <= 13 ? 1 : 1 + (int(bits) - 13 + 9) / 10);
     CUDA_TRY(cww::launch_fwht(v, int(bits), (long long)batch, sequency, scr.p, st));
     return CWW_OK;
 }

@@ -334,7 +334,7 @@ def test_walsh_sign_rows_bit_exact(orc, cuda):
             assert np.array_equal(got[i], orc.sign_row(p, j))
 
 
-@pytest.mark.parametrize("bits", [3, 10, 13, 16])
+@pytest.mark.parametrize("bits", [3, 10, 13, 14, 16, 21, 23, 24])
 def test_fwht(orc, cuda, bits):
     cw = _cw()
     v = np.stack([orc.normals(bits + b, 1 << bits) for b in range(2)])
