@@ -863,8 +863,8 @@ cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
 // levels each.  The level-j samples land contiguously (M apart) in w0 or w1;
 // *xi points at them.
 cww_status synth_chain(const cww_op* op, const double* in, Layout lin, long long nvec, double* w0, double* w1,
-                       const double** xi, cudaStream_t st) {
-    const int j = int(op->j), nu = op->nu;
+                       const double** xi, cudaStream_t st, int jt = -1) {
+    const int j = jt < 0 ? int(op->j) : jt, nu = op->nu;
     const long long M = op->M;
     int bot = std::max(op->r0, std::min(kPyrSynBot, j - 1));
     const double* src = nullptr;  // level-bot coarse vector (nullptr: the op input)
@@ -911,7 +911,7 @@ cww_status synth_chain(const cww_op* op, const double* in, Layout lin, long long
         src_vs = M;
         bot = top;
     }
-    *xi = src;
+    *xi = src;  // nullptr: no level to synthesise (level j is the op input's coarse part)
     return CWW_OK;
 }
 
@@ -1021,14 +1021,24 @@ cww_status run_large_slice(const cww_op* op, const double* in, Layout lin, doubl
     a.use_idwt = op->d.use_idwt;
     a.vmp = op->vmp;
     if (!adj) {
+        // levels r0+1 .. j-1 by the pyramids and level j inside pass 1 (fuse_top)
+        // when the batch's xi would not stay L2-resident (> 32 MB); else the
+        // pyramids write xi and pass 1 reads it back from L2
         const double* xi = nullptr;
+        long long xi_vs = M;
+        const bool fuse = idwt && nvec * M * 8 > (32ll << 20);
         if (idwt) {
-            cww_status s = synth_chain(op, in, lin, nvec, B.w0.p, B.w1.p, &xi, st);
+            cww_status s = synth_chain(op, in, lin, nvec, B.w0.p, B.w1.p, &xi, st, int(op->j) - (fuse ? 1 : 0));
             if (s != CWW_OK) return s;
+            if (!xi) {  // r0 = j - 1 (fused): the input's first half is the level-(j-1) coarse vector
+                xi = in + lin.vbase(0);
+                xi_vs = lin.vbase(1) - lin.vbase(0);
+            }
         }
         a.xi = xi;
-        a.xi_vs = M;
+        a.xi_vs = xi_vs;
         a.xi_is_input = idwt ? 0 : 1;
+        a.fuse_top = fuse ? 1 : 0;
         {
             Prof pr("large_fwd1", st);
             CUDA_TRY(cww::launch_large(nu, 0, a, st));

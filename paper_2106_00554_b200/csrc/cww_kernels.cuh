@@ -1721,6 +1721,12 @@ __global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
     for (int i = tid; i < nc; i += RNT) out[i * es] = cur[i];
 }
 
+// fused finest synthesis level in forward pass 1: the chunk's coarse / detail
+// windows are staged in this many pieces; window length (doubles, even) of a
+// piece of `pairs` output pairs
+constexpr int kFusePieces = 4;
+__host__ __device__ constexpr int fuse_window(int pairs, int nu) { return (pairs + nu + 3) & ~1; }
+
 // ---------------------------------------------------------------------------
 // large path: two-pass Hadamard over K with an L2-resident intermediate
 // ---------------------------------------------------------------------------
@@ -1743,7 +1749,127 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p)
     const double* src = p.xi_is_input ? p.in + p.lin.vbase(p.v0 + v) : xi;  // large path: contiguous
     const long long cbase = (long long)chunk * R1 * B;
     const bool echunk = NU > 1 && (chunk == 0 || cbase + R1 * B >= M);  // holds edge positions
-    {
+    if (p.fuse_top) {
+        // the finest synthesis level (wavelet.cpp:447-483 gather form) straight
+        // into the tile.  The chunk's c_{j-1} / d_{j-1} windows are staged in
+        // kFusePieces pieces by bulk copies (TMA engine, one mbarrier phase per
+        // piece); pair m -> samples 2m, 2m+1 from window entries
+        // m-OFF .. m-OFF+NU; VMP edge samples / periodic wrap via idwt_one
+        // from global memory (first / last chunk only)
+        const FiltSmem<NU> F{p.tab + p.t.o_h};
+        const Taps<NU> tp(F);
+        const bool vmp = p.vmp != 0;
+        const int half = M >> 1;
+        const double* cv = p.xi + (long long)v * p.xi_vs;
+        const double* dv = p.in + p.lin.vbase(p.v0 + v) + half;
+        constexpr int OFF = (NU + 1) / 2, EL = FiltSmem<NU>::EL;
+        const int mlo = vmp ? (EL + 1) >> 1 : OFF, mhi = vmp ? (M - EL) >> 1 : half - (NU - OFF);
+        const int m0 = (int)(cbase >> 1);
+        const int ppairs = R1 * B / 2 / kFusePieces;
+        const int WP = fuse_window(ppairs, NU);
+        // two window buffers (ring): piece pc + 1 lands while piece pc is consumed
+        uint64_t* bar = reinterpret_cast<uint64_t*>(T + R1 * RS);  // [2]
+        double* Wb = T + R1 * RS + 2;                               // [2][C | D][WP]
+        const bool al = ((reinterpret_cast<uintptr_t>(cv) | reinterpret_cast<uintptr_t>(dv)) & 15) == 0;
+        auto win = [&](int pc, int& ws, int& len) {
+            const int mp = m0 + pc * ppairs;
+            ws = max(0, (mp - OFF) & ~1);
+            len = min(half, (mp + ppairs + NU - OFF + 1) & ~1) - ws;
+        };
+        auto issue = [&](int pc) {  // thread 0: bulk copies of piece pc into buffer pc & 1
+            int ws, len;
+            win(pc, ws, len);
+            double* Cw = Wb + (pc & 1) * 2 * WP;
+            mbar_arrive_expect(bar + (pc & 1), (unsigned)(2 * len * 8));
+            bulk_g2s(Cw, cv + ws, (unsigned)(len * 8), bar + (pc & 1));
+            bulk_g2s(Cw + WP, dv + ws, (unsigned)(len * 8), bar + (pc & 1));
+        };
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+        }
+        __syncthreads();
+        if (al && tid == 0) {
+            issue(0);
+            if (kFusePieces > 1) issue(1);
+        }
+        for (int pc = 0; pc < kFusePieces; ++pc) {
+            const int mp = m0 + pc * ppairs;
+            int ws, len;
+            win(pc, ws, len);
+            double* Cw = Wb + (pc & 1) * 2 * WP;
+            double* Dw = Cw + WP;
+            if (al) {
+                mbar_wait(bar + (pc & 1), (unsigned)((pc >> 1) & 1));
+            } else {  // caller's buffer only 8-byte aligned: element-wise async copies
+                for (int t = tid; t < len; t += NT) {
+                    cp_async8(Cw + t, cv + ws + t);
+                    cp_async8(Dw + t, dv + ws + t);
+                }
+                cp_async_wait_all();
+                __syncthreads();
+            }
+            for (int t = tid; t < ppairs; t += NT) {
+                const int m = mp + t;
+                double o0, o1;
+                if (m >= mlo && m < mhi) {
+                    const double* cw = Cw + (m - OFF - ws);
+                    const double* dw = Dw + (m - OFF - ws);
+                    double c[NU + 1], d[NU + 1];
+#pragma unroll
+                    for (int k = 0; k <= NU; ++k) {
+                        c[k] = cw[k];
+                        d[k] = dw[k];
+                    }
+                    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                    for (int u = -NU + 1; u <= NU; ++u) {
+                        if ((u & 1) == 0) {
+                            a0 = fma(tp.h[u + NU - 1], c[OFF - u / 2], a0);
+                            b0 = fma(tp.g[u + NU - 1], d[OFF - u / 2], b0);
+                        } else {
+                            a1 = fma(tp.h[u + NU - 1], c[OFF - (u - 1) / 2], a1);
+                            b1 = fma(tp.g[u + NU - 1], d[OFF - (u - 1) / 2], b1);
+                        }
+                    }
+                    o0 = a0 + b0;
+                    o1 = a1 + b1;
+                } else {
+                    o0 = idwt_one<NU>(F, cv, dv, M, 2 * m, vmp);
+                    o1 = idwt_one<NU>(F, cv, dv, M, 2 * m + 1, vmp);
+                }
+                const int pos = 2 * m, rl = (pos - (int)cbase) >> kLogB, col = pos & (B - 1);
+                double* dst = T + (int)brev_bits((unsigned)rl, kl) * RS + H + col;
+                if (echunk && (pos < NU || pos + 1 >= M - NU)) {  // edge positions: raw value to ev, 0 in the tile
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int q = pos + e;
+                        const double o = e ? o1 : o0;
+                        if (q < NU || q >= M - NU) {
+                            p.ev[(long long)v * 2 * NU + (q < NU ? q : NU + (q - (M - NU)))] = o;
+                            dst[e] = 0.0;
+                        } else {
+                            dst[e] = o;
+                        }
+                    }
+                } else {
+                    dst[0] = o0;
+                    dst[1] = o1;
+                }
+            }
+            __syncthreads();  // buffer pc & 1 is free: refill it with piece pc + 2
+            if (al && tid == 0 && pc + 2 < kFusePieces) issue(pc + 2);
+        }
+        if (H > 0 && tid < 2 * H) {  // outer halos: samples of the neighbouring chunks
+            const bool left = tid < H;
+            const int c = left ? tid : tid - H;
+            const long long pos = left ? cbase - H + c : cbase + (long long)R1 * B + c;
+            double* dst = left ? T + c : T + (int)brev_bits((unsigned)(R1 - 1), kl) * RS + B + H + c;
+            *dst = (pos >= 0 && pos < M && !(NU > 1 && (pos < NU || pos >= M - NU)))
+                       ? idwt_one<NU>(F, cv, dv, M, (int)pos, vmp)
+                       : 0.0;
+        }
+    } else {
         // each source sample once, into its row's own columns [H, B + H): one
         // warp per logical row, lane = column (coalesced, warp-uniform row math)
         const int lane = tid & 31;
@@ -1762,7 +1888,7 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p)
             else *dst = 0.0;
         }
     }
-    if (NU > 1 && tid < 2 * NU) {  // raw edge values (first / last chunk)
+    if (NU > 1 && !p.fuse_top && tid < 2 * NU) {  // raw edge values (first / last chunk)
         const int c = tid;
         const long long pos = c < NU ? c : (M - NU) + (c - NU);
         if ((int)((pos / B) / R1) == chunk)

@@ -51,6 +51,9 @@ struct LargeArgs {
     const double* xi;
     long long xi_vs;
     int xi_is_input;
+    // 1: xi holds the level-(j-1) coarse vector and pass 1 synthesises level j
+    // itself (details d_{j-1} = in[2^(j-1) : 2^j]), so xi never reaches HBM
+    int fuse_top;
     const double* in;
     Layout lin;
     // intermediate G: [nvec][A][CW]; edge values ev: [nvec][2nu]

@@ -76,6 +76,8 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
     long long s2a = s2 + (a.cta_red ? (CWW_NT / 32) * FE * 8 : 0);
     switch (which) {
         case 0: {
+            if (a.fuse_top)  // + mbarrier + the coarse / detail windows of one piece
+                s1 += (2 + 4ll * fuse_window(R1 * (1 << kLogB) / 2 / kFusePieces, CWW_NU)) * 8;  // 2 buffers
             auto k = k_large_fwd1<CWW_NU, CWW_NT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
             if (cudaError_t e = launch_k(k, g1, CWW_NT, s1, st, a); e != cudaSuccess) return e;

@@ -122,6 +122,39 @@ def test_parity_large(orc, cuda, case, use_idwt):
         assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL
 
 
+# Batches whose xi exceeds 32 MB take the fused routes: the finest synthesis
+# level inside forward pass 1, the finest analysis level inside adjoint pass 1
+# (chunk-boundary partial sums + fixup).  (family, nu, boundary, j, q, r0, batch)
+FUSED = [(0, 3, 1, 17, 2, 4, 40), (0, 2, 0, 17, 1, -1, 36), (0, 4, 1, 18, 1, 17, 20), (1, 5, 1, 19, 1, 6, 9),
+         (0, 6, 0, 18, 1, 12, 17)]
+
+
+@pytest.mark.parametrize("case", FUSED, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_r%d_B%d" % c)
+@pytest.mark.parametrize("offset", [0, 1])
+def test_parity_fused_levels(orc, cuda, case, offset):
+    """Fused finest wavelet level (large batches), 16-byte aligned buffers and
+    buffers one double off (element-wise staging instead of bulk copies)."""
+    import torch
+    fam, nu, bnd, j, q, r0, B = case
+    ref = orc.op(fam, nu, bnd, j, q, 1, r0)
+    op = make(fam, nu, bnd, j, q, 1, r0, True)
+    x = np.stack([orc.normals(700 + b, ref.nin) for b in range(B)])
+    y = np.stack([orc.normals(800 + b, ref.nout) for b in range(B)])
+    xb = torch.empty(B * ref.nin + offset, dtype=torch.float64, device="cuda")
+    yb = torch.empty(B * ref.nout + offset, dtype=torch.float64, device="cuda")
+    xv, yv = xb[offset:].view(B, ref.nin), yb[offset:].view(B, ref.nout)
+    xv.copy_(gpu(x))
+    yv.copy_(gpu(y))
+    fo = torch.empty(B * ref.nout + offset, dtype=torch.float64, device="cuda")[offset:].view(B, ref.nout)
+    ao = torch.empty(B * ref.nin + offset, dtype=torch.float64, device="cuda")[offset:].view(B, ref.nin)
+    op.forward(xv, fo)
+    op.adjoint(yv, ao)
+    fx, ay = host(fo), host(ao)
+    for b in (0, 1, B // 2, B - 1):
+        assert rel(fx[b], ref.forward(x[b], 1)) <= TOL
+        assert rel(ay[b], ref.adjoint(y[b], 1)) <= TOL
+
+
 # ---- subsampled ComposedOp (SamplingMask, fastop.cpp:231-281) --------------
 MASKED = [(0, 4, 1, 8, 2, 1, -1, 0.1), (0, 3, 1, 14, 2, 1, 4, 0.3), (1, 2, 0, 9, 1, 1, -1, 0.5),
           (0, 4, 1, 5, 1, 2, -1, 0.2), (0, 2, 1, 6, 1, 2, 3, 0.05), (0, 1, 0, 10, 1, 1, 1, 0.4)]
