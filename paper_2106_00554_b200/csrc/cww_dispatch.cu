@@ -53,6 +53,8 @@ cudaError_t launch_large(int nu, int which, const LargeArgs& a, cudaStream_t st)
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_ana_fixup(int nu, const LargeArgs& a, cudaStream_t st) { return launch_large(nu, 4, a, st); }
+
 cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st) {
 #define C(N) launch_wav_nu##N(w, st)
     SWITCH_NU(nu, C)

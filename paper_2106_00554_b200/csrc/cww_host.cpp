@@ -920,7 +920,7 @@ cww_status synth_chain(const cww_op* op, const double* in, Layout lin, long long
 // `lout`: chained warp pyramids of <= 3 steps; the launch that reaches level
 // <= 10 finishes the coarse levels in its last CTA per vector (atomic ticket).
 cww_status analysis_chain(const cww_op* op, double* w0, double* w1, double* out, Layout lout, long long nvec,
-                          cudaStream_t st) {
+                          cudaStream_t st, int top = -1) {
     const long long M = op->M;
     const int nu = op->nu;
     unsigned* cnt = nullptr;
@@ -931,7 +931,7 @@ cww_status analysis_chain(const cww_op* op, double* w0, double* w1, double* out,
         ~CntFree() { cudaFreeAsync(p, s); }
     } cnt_free{cnt, st};
     CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(nvec) * sizeof(unsigned), st));
-    int T = int(op->j);
+    int T = top < 0 ? int(op->j) : top;  // level of the samples in w0
     const double* src = w0;
     double* sink[2] = {w1, w0};
     for (int it = 0;; ++it) {
@@ -990,7 +990,7 @@ long long large_slice(const cww_op* op, long long nvec) {
 }
 
 struct LargeBufs {
-    DevBuf w0, w1, G, ev, epw;
+    DevBuf w0, w1, G, ev, epw, apart;
 };
 
 cww_status run_large_slice(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
@@ -1052,15 +1052,26 @@ cww_status run_large_slice(const cww_op* op, const double* in, Layout lin, doubl
         Prof pr("large_adj2", st);
         CUDA_TRY(cww::launch_large(nu, 2, a, st));
     }
-    a.xo = idwt ? B.w0.p : nullptr;
-    a.xo_vs = M;
+    // the finest analysis level inside pass 1 when the batch's xi would not
+    // stay L2-resident (> 32 MB): d_{j-1} straight to the output, c_{j-1} to
+    // the workspace (or, for r0 = j - 1, to the output's coarse half)
+    const bool fana = idwt && nvec * M * 8 > (32ll << 20);
+    const bool last = fana && op->r0 == int(op->j) - 1;
+    a.xo = last ? out : (idwt ? B.w0.p : nullptr);
+    a.xo_vs = last ? lout.vbase(1) - lout.vbase(0) : M;
     a.xo_is_output = idwt ? 0 : 1;
+    a.fuse_ana = fana ? 1 : 0;
+    a.apart = B.apart.p;
     {
         Prof pr("large_adj1", st);
         CUDA_TRY(cww::launch_large(nu, 3, a, st));
     }
-    if (!idwt) return CWW_OK;
-    return analysis_chain(op, B.w0.p, B.w1.p, out, lout, nvec, st);
+    if (fana && nu > 1) {
+        Prof pr("ana_fixup", st);
+        CUDA_TRY(cww::launch_ana_fixup(nu, a, st));
+    }
+    if (!idwt || last) return CWW_OK;
+    return analysis_chain(op, B.w0.p, B.w1.p, out, lout, nvec, st, fana ? int(op->j) - 1 : int(op->j));
 }
 
 // Forward (IDWT, pass 1, pass 2) or adjoint (pass 2, pass 1, DWT) of nvec
@@ -1083,7 +1094,10 @@ cww_status run_large(const cww_op* op, const double* in, Layout lin, double* out
         CUDA_TRY(B.w0.alloc(size_t(sl * M), st));
         CUDA_TRY(B.w1.alloc(size_t(sl * M), st));
     }
-    if (adj) CUDA_TRY(B.epw.alloc(size_t(sl * nslot * op->S * 2 * NP + 1), st));
+    if (adj) {
+        CUDA_TRY(B.epw.alloc(size_t(sl * nslot * op->S * 2 * NP + 1), st));
+        CUDA_TRY(B.apart.alloc(size_t(sl * (A >> pl.kl) * nu * 4 + 1), st));
+    }
     for (long long v0 = 0; v0 < nvec; v0 += sl) {
         const long long nv = std::min(sl, nvec - v0);
         cww_status s = run_large_slice(op, in + lin.vbase(v0), lin, out + lout.vbase(v0), lout, nv, adj, B, st);

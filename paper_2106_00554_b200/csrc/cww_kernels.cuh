@@ -2170,47 +2170,157 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
     const int hcol = lane < H ? B + H + lane : lane - (B - H);
     const double nbv = hside < 0 ? nb[lane] : (hside > 0 ? nb[H + lane - (B - H)] : 0.0);
     const long long base = (long long)chunk * R1 * B;
-    double* xw = p.xo_is_output ? nullptr : xo + base + lane;
-    if (!has_edge && xw) {  // interior chunks: four rows in flight per warp (independent chains)
+    const bool fana = p.fuse_ana != 0;
+    // xi of the chunk: to the workspace / output, or (fused analysis) in place
+    // into the tile's own columns [H, B + H) -- each (row, column) is read and
+    // written by one thread only, and the halo columns stay intact
+    double* xw = (p.xo_is_output || fana) ? nullptr : xo + base + lane;
+    if (!has_edge && (xw || fana)) {  // interior chunks: four rows in flight per warp (independent chains)
 #pragma unroll 4
         for (int rl = tid >> 5; rl < R1; rl += NT / 32) {
-            double val = T[(int)brev_bits((unsigned)rl, kl) * RS + lane + H];
+            const int ph = (int)brev_bits((unsigned)rl, kl);
+            double val = T[ph * RS + lane + H];
             if (hside != 0) {
                 const int rn = rl + hside;
                 val += (rn >= 0 && rn < R1) ? T[(int)brev_bits((unsigned)rn, kl) * RS + hcol] : nbv;
             }
-            xw[rl * B] = val;
+            if (fana) T[ph * RS + lane + H] = val;
+            else xw[rl * B] = val;
         }
-        return;
-    }
-    for (int rl = tid >> 5; rl < R1; rl += NT / 32) {  // logical local row K_lo, lane = column
-        const int ph = (int)brev_bits((unsigned)rl, kl);
-        double val = T[ph * RS + lane + H];
-        if (hside != 0) {  // overlap-add of the previous row's right / the next row's left halo
-            const int rn = rl + hside;
-            val += (rn >= 0 && rn < R1) ? T[(int)brev_bits((unsigned)rn, kl) * RS + hcol] : nbv;
-        }
-        if (has_edge) {
-            const long long pos = base + (long long)rl * B + lane;
-            const long long rpos = pos - lane;  // warp-uniform: does this row hold an edge position?
-            if ((rpos < NU || rpos + B > M - NU) && (pos < NU || pos >= M - NU)) {
-                const int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
-                const double* em = p.tab + p.t.o_em + c;
-                double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-                const int nsp = S * 2 * NP;
-                int sp = 0;
-                for (; sp + 4 <= nsp; sp += 4) {
-                    e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
-                    e1 += __ldg(em + (sp + 1) * 2 * NU) * Wv[sp + 1];
-                    e2 += __ldg(em + (sp + 2) * 2 * NU) * Wv[sp + 2];
-                    e3 += __ldg(em + (sp + 3) * 2 * NU) * Wv[sp + 3];
+    } else {
+        for (int rl = tid >> 5; rl < R1; rl += NT / 32) {  // logical local row K_lo, lane = column
+            const int ph = (int)brev_bits((unsigned)rl, kl);
+            double val = T[ph * RS + lane + H];
+            if (hside != 0) {  // overlap-add of the previous row's right / the next row's left halo
+                const int rn = rl + hside;
+                val += (rn >= 0 && rn < R1) ? T[(int)brev_bits((unsigned)rn, kl) * RS + hcol] : nbv;
+            }
+            if (has_edge) {
+                const long long pos = base + (long long)rl * B + lane;
+                const long long rpos = pos - lane;  // warp-uniform: does this row hold an edge position?
+                if ((rpos < NU || rpos + B > M - NU) && (pos < NU || pos >= M - NU)) {
+                    const int c = pos < NU ? (int)pos : NU + (int)(pos - (M - NU));
+                    const double* em = p.tab + p.t.o_em + c;
+                    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+                    const int nsp = S * 2 * NP;
+                    int sp = 0;
+                    for (; sp + 4 <= nsp; sp += 4) {
+                        e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
+                        e1 += __ldg(em + (sp + 1) * 2 * NU) * Wv[sp + 1];
+                        e2 += __ldg(em + (sp + 2) * 2 * NU) * Wv[sp + 2];
+                        e3 += __ldg(em + (sp + 3) * 2 * NU) * Wv[sp + 3];
+                    }
+                    for (; sp < nsp; ++sp) e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
+                    val = (e0 + e1) + (e2 + e3);
                 }
-                for (; sp < nsp; ++sp) e0 += __ldg(em + sp * 2 * NU) * Wv[sp];
-                val = (e0 + e1) + (e2 + e3);
+            }
+            if (fana) T[ph * RS + lane + H] = val;
+            else if (xw) xw[rl * B] = val;
+            else ob[p.lout.eoff(base + (long long)rl * B + lane)] = val;
+        }
+    }
+    if (!fana) return;
+    __syncthreads();
+    // finest analysis level (wavelet.cpp:403-445 gather form) from the chunk's xi:
+    // c[m] = sum_u hbar_u xi[2m+u], d[m] = sum_u gbar_u xi[2m+u], u = -NU+1..NU;
+    // VMP edge rows from the dense edge rows (chunk-local); rows whose window
+    // straddles a chunk boundary P (m in [P/2 - FL, P/2 - FL + NS)) get this
+    // chunk's partial sums, completed by k_ana_fixup
+    {
+        constexpr int FL = NU / 2, NS = NU / 2 + NU / 2;  // straddling rows per boundary
+        constexpr int EL = FiltSmem<NU>::EL;
+        const FiltSmem<NU> F{p.tab + p.t.o_h};
+        const Taps<NU> tp(F);
+        const bool vmp = p.vmp != 0;
+        const int half = M >> 1, CH = R1 * B, nch = M / CH;
+        const int m0 = (int)(base >> 1);
+        auto xiv = [&](int pos) -> double {  // pos inside this chunk
+            const int r = (pos - (int)base) >> kLogB;
+            return T[(int)brev_bits((unsigned)r, kl) * RS + H + (pos & (B - 1))];
+        };
+        const bool lb = !vmp || chunk > 0, rb = !vmp || chunk + 1 < nch;  // boundaries with partials
+        const int mlo = m0 + (lb ? NS - FL : 0), mhi = m0 + CH / 2 - (rb ? FL : 0);
+        double* cws = xo;  // c_{j-1}
+        double* dout = ob + half;
+        for (int m = mlo + tid; m < mhi; m += NT) {
+            double c, d;
+            if (vmp && (m < NU || m >= half - NU)) {
+                const int side = m < NU ? 0 : 1;
+                const int mm = side ? half - 1 - m : m;
+                const double* ra = F.ana(side, 0, mm);
+                const double* rb2 = F.ana(side, 1, mm);
+                double a0 = 0.0, b0 = 0.0;
+#pragma unroll
+                for (int k = 0; k < EL; ++k) {
+                    const double xv = xiv(side ? M - 1 - k : k);
+                    a0 = fma(ra[k], xv, a0);
+                    b0 = fma(rb2[k], xv, b0);
+                }
+                c = a0;
+                d = b0;
+            } else {
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int u = -NU + 1; u <= NU; ++u) {
+                    const double xv = xiv(2 * m + u);
+                    if (u & 1) {
+                        a1 = fma(tp.h[u + NU - 1], xv, a1);
+                        b1 = fma(tp.g[u + NU - 1], xv, b1);
+                    } else {
+                        a0 = fma(tp.h[u + NU - 1], xv, a0);
+                        b0 = fma(tp.g[u + NU - 1], xv, b0);
+                    }
+                }
+                c = a0 + a1;
+                d = b0 + b1;
+            }
+            cws[m] = c;
+            dout[m] = d;
+        }
+        // partial sums of the straddling rows: left boundary (this chunk is its
+        // right side) and right boundary (left side); unwrapped positions
+        if (tid < 2 * NS) {
+            const bool right = tid >= NS;
+            const int i = right ? tid - NS : tid;
+            if (right ? rb : lb) {
+                const int P = (int)base + (right ? CH : 0);
+                const int m = P / 2 - FL + i;
+                double a0 = 0.0, b0 = 0.0;
+#pragma unroll
+                for (int u = -NU + 1; u <= NU; ++u) {
+                    const int pos = 2 * m + u;
+                    if (pos >= (int)base && pos < (int)base + CH) {
+                        const double xv = xiv(pos);
+                        a0 = fma(tp.h[u + NU - 1], xv, a0);
+                        b0 = fma(tp.g[u + NU - 1], xv, b0);
+                    }
+                }
+                const int bidx = right ? (chunk + 1) % nch : chunk;  // boundary at P (P = M wraps to 0)
+                double* pp = p.apart + (((long long)v * nch + bidx) * NU + i) * 4 + (right ? 0 : 2);
+                pp[0] = a0;
+                pp[1] = b0;
             }
         }
-        if (xw) xw[rl * B] = val;
-        else ob[p.lout.eoff(base + (long long)rl * B + lane)] = val;
+    }
+}
+
+// Completes the finest-level analysis rows that straddle adjoint pass-1 chunk
+// boundaries: one thread per (vector, boundary, row); c / d = left + right
+// partial sums (fixed order).  VMP has no boundary at 0 / M.
+template <int NU>
+__global__ void k_ana_fixup(LargeArgs p) {
+    constexpr int FL = NU / 2, NS = NU / 2 + NU / 2;
+    const int M = 1 << p.j, half = M >> 1, CH = (1 << p.kl) << kLogB, nch = M / CH;
+    const long long tot = p.nvec * nch * NS;
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < tot; f += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(f % NS);
+        const int b = (int)((f / NS) % nch);
+        const long long v = f / ((long long)NS * nch);
+        if (p.vmp && b == 0) continue;
+        const double* pp = p.apart + ((v * nch + b) * NU + i) * 4;
+        const int m = (((b * CH) >> 1) - FL + i + half) & (half - 1);
+        p.xo[v * p.xo_vs + m] = pp[0] + pp[2];
+        (p.out + p.lout.vbase(p.v0 + v))[half + m] = pp[1] + pp[3];
     }
 }
 

@@ -69,6 +69,12 @@ struct LargeArgs {
     double* xo;  // adjoint pass-1 destination (workspace) unless xo_is_output
     long long xo_vs;
     int xo_is_output;
+    // 1: adjoint pass 1 runs the finest analysis level itself: d_{j-1} to the
+    // output, c_{j-1} to xo; the pairs whose filter window straddles a chunk
+    // boundary get per-side partial sums apart[nvec][2^kh][NU][2 sides][c, d],
+    // summed by launch_ana_fixup
+    int fuse_ana;
+    double* apart;
 };
 
 struct WavArgs {
@@ -210,6 +216,8 @@ inline int pyr_wmax_ana(int nu, int top, int bot, int cb, bool vmp, int* wm2 = n
 cudaError_t launch_small(int nu, const SmallArgs& a, bool adj, cudaStream_t st);
 long long small_smem_query(int nu, int V, int j, int q, bool adj, bool vf);
 cudaError_t launch_large(int nu, int which, const LargeArgs& a, cudaStream_t st);
+// finest-level analysis pairs straddling adjoint pass-1 chunk boundaries: c / d = left + right partials
+cudaError_t launch_ana_fixup(int nu, const LargeArgs& a, cudaStream_t st);
 long long large_nslot(int nu, int q, int j, int kl, int ng);
 // adj2 keeps per-warp edge sums in smem when they are small (<= 256 values)
 inline bool large_cta_red(int nu, int q) { return (2 * (2 * nu - 1)) << q <= 256; }

@@ -95,6 +95,13 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
             if (cudaError_t e = launch_k(k, g2, CWW_NT, s2a, st, a); e != cudaSuccess) return e;
             break;
         }
+        case 4: {  // straddling finest-level analysis rows (fused adjoint pass 1)
+            const long long tot = a.nvec * (R1 ? (1ll << a.j) / ((long long)R1 << kLogB) : 0) * (CWW_NU / 2) * 2;
+            if (tot == 0) return cudaSuccess;
+            const long long g = (tot + 255) / 256;
+            k_ana_fixup<CWW_NU><<<(unsigned)(g < 148 * 8 ? g : 148 * 8), 256, 0, st>>>(a);
+            break;
+        }
         default: {
             auto k = k_large_adj1<CWW_NU, CWW_NT>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1a);
