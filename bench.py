@@ -202,11 +202,11 @@ def algorithmic_bytes(cfg, kernel: str, nvec: int) -> float:
         return 16.0 * nvec * M * M * per_iter * iters
     if dim == 2:
         # small_fwd: row pass reads X (M^2), column pass writes Y (N^2); small_adj mirrored
-        return 8.0 * nvec * (M * M + N * N) if kernel in ("small_fwd", "small_adj") else 0.0
+        return 8.0 * nvec * (M * M + N * N) if kernel in ("small_fwd", "small_adj", "wv_fwd", "wv_adj") else 0.0
     lc = min(j - 1, 10)  # coarse synthesis levels <= 10 run in k_wav_coarse
     idwt = r0 < j
     per = {
-        "small_fwd": M + N, "small_adj": M + N,
+        "small_fwd": M + N, "small_adj": M + N, "wv_fwd": M + N, "wv_adj": M + N,
         "wav_coarse": (1 << lc) if idwt else 0,
         "idwt_pyr": M - (1 << lc),               # the detail coefficients above level lc
         "large_fwd1": 0 if idwt else M, "large_fwd": N if idwt else M + N,

@@ -13,6 +13,7 @@ namespace cww {
 
 #define DECL(N)                                                                     \
     cudaError_t launch_small_nu##N(const SmallArgs&, bool, cudaStream_t);           \
+    cudaError_t launch_wv_nu##N(const SmallArgs&, bool, cudaStream_t);              \
     long long small_smem_nu##N(int, int, int, bool, bool);                                \
     cudaError_t launch_large_nu##N(int, const LargeArgs&, cudaStream_t);            \
     cudaError_t launch_wav_nu##N(const WavArgs&, cudaStream_t);                    \
@@ -31,6 +32,13 @@ DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6)
         case 5: return call(5);              \
         case 6: return call(6);              \
     }
+
+cudaError_t launch_wv(int nu, const SmallArgs& a, bool adj, cudaStream_t st) {
+#define C(N) launch_wv_nu##N(a, adj, st)
+    SWITCH_NU(nu, C)
+#undef C
+    return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_small(int nu, const SmallArgs& a, bool adj, cudaStream_t st) {
 #define C(N) launch_small_nu##N(a, adj, st)

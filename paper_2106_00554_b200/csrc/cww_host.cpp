@@ -815,6 +815,12 @@ cww::SmallArgs small_args(const cww_op* op, const double* in, Layout lin, double
 cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
                      long long nvec, bool adj, cudaStream_t st, bool wav = true) {
     if (nvec == 0) return CWW_OK;
+    if (op->j == 10 && wav && !std::getenv("CWW_NO_WV")) {  // warp-per-vector kernels (cww_warp.cuh)
+        auto a = small_args(op, in, lin, out, lout, nvec, 8);
+        Prof pr(adj ? "wv_adj" : "wv_fwd", st);
+        CUDA_TRY(cww::launch_wv(op->nu, a, adj, st));
+        return CWW_OK;
+    }
     int V = small_V(op->M, nvec);
     const bool vf = adj ? lin.vfast() : lout.vfast();
     while (V > 1 && cww::small_smem_query(op->nu, V, int(op->j), int(op->q), adj, vf) > 200 * 1024) V /= 2;

@@ -214,6 +214,8 @@ inline int pyr_wmax_ana(int nu, int top, int bot, int cb, bool vmp, int* wm2 = n
     return wm[0] > wm[1] ? wm[0] : wm[1];
 }
 cudaError_t launch_small(int nu, const SmallArgs& a, bool adj, cudaStream_t st);
+// warp-per-vector kernels for M = 2^10 (cww_warp.cuh)
+cudaError_t launch_wv(int nu, const SmallArgs& a, bool adj, cudaStream_t st);
 long long small_smem_query(int nu, int V, int j, int q, bool adj, bool vf);
 cudaError_t launch_large(int nu, int which, const LargeArgs& a, cudaStream_t st);
 // finest-level analysis pairs straddling adjoint pass-1 chunk boundaries: c / d = left + right partials

@@ -3,6 +3,7 @@
 // translation unit (parallel build, bounded compile time).
 #pragma once
 #include "cww_kernels.cuh"
+#include "cww_warp.cuh"
 
 
 #ifndef CWW_NU
@@ -62,6 +63,23 @@ long long CWW_FN(small_smem_nu)(int V, int j, int q, bool adj, bool vf) {
         case 4: return small_smem_bytes<CWW_NU, 4>(V, j, q, adj, vf);
         default: return small_smem_bytes<CWW_NU, 5>(V, j, q, adj, vf);
     }
+}
+
+cudaError_t CWW_FN(launch_wv_nu)(const SmallArgs& a, bool adj, cudaStream_t st) {
+    if (a.j != kWvJ) return cudaErrorInvalidValue;
+    const int grid = (int)((a.nvec + kWvNT / 32 - 1) / (kWvNT / 32));
+    const long long smem = wv_smem_bytes<CWW_NU>(1 << a.q);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    if (adj) {
+        auto k = k_wv_adj<CWW_NU>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaError_t e = launch_k(k, grid, kWvNT, smem, st, a); e != cudaSuccess) return e;
+    } else {
+        auto k = k_wv_fwd<CWW_NU>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaError_t e = launch_k(k, grid, kWvNT, smem, st, a); e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t st) {
