@@ -27,7 +27,7 @@
 namespace cww {
 
 constexpr int kWvJ = 10;                     // M = 1024
-constexpr int kWvXS = (1 << kWvJ) + 32 + 2;  // per-warp region: 1024 + 32 pads (+16-byte slack)
+constexpr int kWvXS = 1060;  // per-warp region: 1024 + 32 pads (+4); = 4 (mod 16): the 8 regions' banks interleave
 constexpr int kWvNT = 256;                   // 8 warps = 8 vectors per CTA
 constexpr int kWvV = kWvNT / 32;
 #ifndef WV_MINB
