@@ -87,7 +87,14 @@ typedef struct {
      * table is bit-identical to the host computation (separately rounded
      * products and sums in the host's order). */
     int gpu_kernel_table;
+    /* I/O precision: CWW_FP64 (cww_forward / cww_adjoint on
+     * double buffers) or CWW_FP32 (cww_forward_f32 / cww_adjoint_f32 on float
+     * buffers; the arithmetic stays fp64, the results are rounded to fp32 once
+     * on output: relative error ~1e-7 against the fp64 path). */
+    int precision;
 } cww_op_desc;
+
+typedef enum { CWW_FP64 = 0, CWW_FP32 = 1 } cww_precision;
 
 typedef struct cww_op cww_op;
 
@@ -107,6 +114,13 @@ cww_status cww_forward(const cww_op* op, const double* x, size_t x_len, double* 
                        size_t y_len, size_t batch, void* stream);
 cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* x,
                        size_t x_len, size_t batch, void* stream);
+/* fp32 I/O (ops created with desc.precision = CWW_FP32): float device
+ * buffers, batch-major as above; converted to fp64 on entry and rounded to
+ * fp32 on exit around the fp64 kernels. */
+cww_status cww_forward_f32(const cww_op* op, const float* x, size_t x_len, float* y, size_t y_len,
+                           size_t batch, void* stream);
+cww_status cww_adjoint_f32(const cww_op* op, const float* y, size_t y_len, float* x, size_t x_len,
+                           size_t batch, void* stream);
 /* x <- (U* U)^iters x  (adjoint(forward(x)) repeated; the normal operator
  * of a least-squares / CG loop).  work: NULL or batch*output_size doubles. */
 cww_status cww_normal(const cww_op* op, double* x, size_t x_len, double* work,

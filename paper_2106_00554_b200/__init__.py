@@ -69,7 +69,7 @@ class _Desc(C.Structure):
                 ("q", C.c_uint), ("dim", C.c_int), ("min_level", C.c_int), ("use_idwt", C.c_int),
                 ("kernel_resolution", C.c_int), ("device", C.c_int), ("data_dir", C.c_char_p),
                 ("mask", C.c_void_p), ("mask_len", C.c_size_t), ("cache_dir", C.c_char_p),
-                ("gpu_kernel_table", C.c_int)]
+                ("gpu_kernel_table", C.c_int), ("precision", C.c_int)]
 
 
 _lib = None
@@ -98,6 +98,8 @@ def _load():
         getattr(L, name).argtypes = [vp, dp, sz, dp, sz, sz]
     L.cww_normal.argtypes = [vp, dp, sz, dp, sz, sz, C.c_int, vp]
     L.cww_forward_host_async.argtypes = [vp, dp, sz, dp, sz, sz, vp]
+    L.cww_forward_f32.argtypes = [vp, dp, sz, dp, sz, sz, vp]
+    L.cww_adjoint_f32.argtypes = [vp, dp, sz, dp, sz, sz, vp]
     L.cww_adjoint_host_async.argtypes = [vp, dp, sz, dp, sz, sz, vp]
     L.cww_gs_solve.argtypes = [vp, dp, sz, dp, sz, sz, C.c_double, C.c_int, C.c_int,
                                C.POINTER(C.c_int), dp, vp]
@@ -248,14 +250,15 @@ class _Handle:
     def __init__(self, spec: WaveletSpec, j: int, q: int, dim: int, min_level: int, use_idwt: bool,
                  kernel_resolution: int = 0, device: Optional[int] = None,
                  data_dir: Optional[str] = None, mask: Optional[np.ndarray] = None,
-                 cache_dir: Optional[str] = None, gpu_kernel_table: bool = False):
+                 cache_dir: Optional[str] = None, gpu_kernel_table: bool = False, precision: str = "fp64"):
         L = _load()
         m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint64)
         d = _Desc(int(spec.family), spec.nu, int(spec.boundary), j, q, dim, min_level,
                   1 if use_idwt else 0, kernel_resolution, -1 if device is None else device,
                   (data_dir or DATA_DIR).encode(), None if m is None else m.ctypes.data,
                   0 if m is None else m.size, None if cache_dir is None else cache_dir.encode(),
-                  1 if gpu_kernel_table else 0)
+                  1 if gpu_kernel_table else 0, 1 if precision == "fp32" else 0)
+        self.fp32 = precision == "fp32"
         h = C.c_void_p()
         _check(L.cww_op_create(C.byref(d), C.byref(h)))
         self.h = h
@@ -280,6 +283,20 @@ class _Handle:
 
     def _apply(self, inp, out, adjoint: bool):
         nin, nout = (self.nout, self.nin) if adjoint else (self.nin, self.nout)
+        if self.fp32:  # fp32 I/O: float32 CUDA tensors (cww_*_f32)
+            torch = _torch()
+            if not (_is_tensor(inp) and inp.is_cuda and inp.dtype == torch.float32):
+                raise CwwError("fp32 op: expected a float32 CUDA tensor", 1)
+            inp = inp.contiguous()
+            if inp.numel() % nin:
+                raise CwwError(("adjoint" if adjoint else "forward") + ": dimension mismatch", 2)
+            batch = inp.numel() // nin
+            shape = (nout,) if inp.dim() == 1 else tuple(inp.shape[:-1]) + (nout,)
+            if out is None:
+                out = torch.empty(shape, dtype=torch.float32, device=inp.device)
+            fn = self.L.cww_adjoint_f32 if adjoint else self.L.cww_forward_f32
+            _check(fn(self.h, inp.data_ptr(), inp.numel(), out.data_ptr(), out.numel(), batch, _stream_ptr(inp)))
+            return out
         if _is_tensor(inp):
             torch = _torch()
             if (not inp.is_cuda and inp.is_pinned() and _is_tensor(out) and not out.is_cuda and out.is_pinned()
@@ -345,13 +362,15 @@ class FastOp:
     def __init__(self, spec: WaveletSpec, j: int, q: int, dim: int = 1, *,
                  kernel_resolution: int = 0, device: Optional[int] = None,
                  data_dir: Optional[str] = None, cache_dir: Optional[str] = None,
-                 gpu_kernel_table: bool = False):
+                 gpu_kernel_table: bool = False, precision: str = "fp64"):
         spec.validate()
+        if precision not in ("fp64", "fp32"):
+            raise CwwError("precision must be 'fp64' or 'fp32'", 1)
         if spec.nu < 2:
             raise CwwError("FastOp requires nu >= 2; use HaarFullRankOp for Haar", 3)
         self._spec, self._j, self._q, self._dim = spec, int(j), int(q), int(dim)
         self._opts = dict(kernel_resolution=kernel_resolution, device=device, data_dir=data_dir,
-                          cache_dir=cache_dir, gpu_kernel_table=gpu_kernel_table)
+                          cache_dir=cache_dir, gpu_kernel_table=gpu_kernel_table, precision=precision)
         self._h = _Handle(spec, self._j, self._q, self._dim, -1, False, **self._opts)
 
     def M(self) -> int:

@@ -63,6 +63,27 @@ cudaError_t launch_large(int nu, int which, const LargeArgs& a, cudaStream_t st)
 
 cudaError_t launch_ana_fixup(int nu, const LargeArgs& a, cudaStream_t st) { return launch_large(nu, 4, a, st); }
 
+__global__ void k_f32_f64(const float* __restrict__ in, double* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
+}
+__global__ void k_f64_f32(const double* __restrict__ in, float* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = (float)in[i];  // round to nearest
+}
+static unsigned conv_grid(long long n) {
+    long long g = (n + 255) / 256;
+    return (unsigned)(g > 148 * 16 ? 148 * 16 : (g < 1 ? 1 : g));
+}
+cudaError_t launch_convert_f32_f64(const float* in, double* out, long long n, cudaStream_t st) {
+    k_f32_f64<<<conv_grid(n), 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_convert_f64_f32(const double* in, float* out, long long n, cudaStream_t st) {
+    k_f64_f32<<<conv_grid(n), 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_wav(int nu, const WavArgs& w, cudaStream_t st) {
 #define C(N) launch_wav_nu##N(w, st)
     SWITCH_NU(nu, C)

@@ -742,6 +742,7 @@ void build_edge_terms(cww_op& op) {
 }
 
 cww_status validate(const cww_op_desc* d) {
+    if (d->precision != CWW_FP64 && d->precision != CWW_FP32) return fail(CWW_ERR_INVALID_ARG, "precision must be CWW_FP64 or CWW_FP32");
     if (d->family != 0 && d->family != 1) return fail(CWW_ERR_INVALID_ARG, "bad family");
     if (d->boundary != 0 && d->boundary != 1) return fail(CWW_ERR_INVALID_ARG, "bad boundary");
     if (d->nu < 1 || d->nu > 6)
@@ -1245,6 +1246,7 @@ void cww_op_desc_init(cww_op_desc* d) {
     d->mask_len = 0;
     d->cache_dir = nullptr;
     d->gpu_kernel_table = 0;
+    d->precision = CWW_FP64;
 }
 
 cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
@@ -1349,6 +1351,7 @@ cww_status cww_forward(const cww_op* op, const double* x, size_t x_len, double* 
                        size_t batch, void* stream) {
     cww_status s = check_lens(op, x_len, y_len, batch, false, "forward");
     if (s != CWW_OK) return s;
+    if (op->d.precision != CWW_FP64) return fail(CWW_ERR_INVALID_ARG, "op created with precision fp32: use cww_forward_f32");
     if (batch == 0) return CWW_OK;
     if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     return run(op, x, y, (long long)batch, false, S_(stream));
@@ -1358,9 +1361,44 @@ cww_status cww_adjoint(const cww_op* op, const double* y, size_t y_len, double* 
                        size_t batch, void* stream) {
     cww_status s = check_lens(op, y_len, x_len, batch, true, "adjoint");
     if (s != CWW_OK) return s;
+    if (op->d.precision != CWW_FP64) return fail(CWW_ERR_INVALID_ARG, "op created with precision fp32: use cww_adjoint_f32");
     if (batch == 0) return CWW_OK;
     if (!x || !y) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     return run(op, y, x, (long long)batch, true, S_(stream));
+}
+
+// fp32 I/O: convert on entry, fp64 kernels, round once on exit
+static cww_status run_f32(const cww_op* op, const float* in, size_t in_len, float* out, size_t out_len,
+                          size_t batch, bool adj, void* stream) {
+    cww_status s = check_lens(op, in_len, out_len, batch, adj, adj ? "adjoint" : "forward");
+    if (s != CWW_OK) return s;
+    if (op->d.precision != CWW_FP32) return fail(CWW_ERR_INVALID_ARG, "op created with precision fp64: use cww_%s",
+                                                 adj ? "adjoint" : "forward");
+    if (batch == 0) return CWW_OK;
+    if (!in || !out) return fail(CWW_ERR_INVALID_ARG, "null buffer");
+    cudaStream_t st = S_(stream);
+    CUDA_TRY(cudaSetDevice(op->device));
+    DevBuf din, dout;
+    CUDA_TRY(din.alloc(in_len, st));
+    CUDA_TRY(dout.alloc(out_len, st));
+    {
+        Prof pr("f32_in", st);
+        CUDA_TRY(cww::launch_convert_f32_f64(in, din.p, (long long)in_len, st));
+    }
+    if ((s = run(op, din.p, dout.p, (long long)batch, adj, st)) != CWW_OK) return s;
+    Prof pr("f32_out", st);
+    CUDA_TRY(cww::launch_convert_f64_f32(dout.p, out, (long long)out_len, st));
+    return CWW_OK;
+}
+
+cww_status cww_forward_f32(const cww_op* op, const float* x, size_t x_len, float* y, size_t y_len, size_t batch,
+                           void* stream) {
+    return run_f32(op, x, x_len, y, y_len, batch, false, stream);
+}
+
+cww_status cww_adjoint_f32(const cww_op* op, const float* y, size_t y_len, float* x, size_t x_len, size_t batch,
+                           void* stream) {
+    return run_f32(op, y, y_len, x, x_len, batch, true, stream);
 }
 
 // ---- banded normal form (U* U along one axis) -----------------------------
@@ -1713,6 +1751,7 @@ static cww_status host_call(const cww_op* op, const double* in, size_t in_len, d
                             size_t out_len, size_t batch, bool adj) {
     cww_status s = check_lens(op, in_len, out_len, batch, adj, adj ? "adjoint" : "forward");
     if (s != CWW_OK) return s;
+    if (op->d.precision != CWW_FP64) return fail(CWW_ERR_INVALID_ARG, "op created with precision fp32: use the f32 entry points");
     if (batch == 0) return CWW_OK;
     CUDA_TRY(cudaSetDevice(op->device));
     cudaStream_t st;
@@ -1964,6 +2003,7 @@ static cww_status host_call_async(const cww_op* op, const double* in, size_t in_
                                   size_t out_len, size_t batch, bool adj, cudaStream_t st) {
     cww_status s = check_lens(op, in_len, out_len, batch, adj, adj ? "adjoint" : "forward");
     if (s != CWW_OK) return s;
+    if (op->d.precision != CWW_FP64) return fail(CWW_ERR_INVALID_ARG, "op created with precision fp32: use the f32 entry points");
     if (batch == 0) return CWW_OK;
     if (!in || !out) return fail(CWW_ERR_INVALID_ARG, "null buffer");
     if (!is_pinned(in) || !is_pinned(out)) return host_call(op, in, in_len, out, out_len, batch, adj);

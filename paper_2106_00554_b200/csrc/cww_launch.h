@@ -154,6 +154,9 @@ struct NormArgs {
     long long vpi, ivs, es;
 };
 cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st);
+// fp32 I/O conversions (grid-stride)
+cudaError_t launch_convert_f32_f64(const float* in, double* out, long long n, cudaStream_t st);
+cudaError_t launch_convert_f64_f32(const double* in, float* out, long long n, cudaStream_t st);
 // record an error message for cww_last_error() (host translation units)
 cww_status set_error(cww_status st, const char* msg);
 // add n kernel launches to cww_kernel_launches() (host translation units)

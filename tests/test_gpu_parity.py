@@ -484,3 +484,25 @@ def test_pinned_host_async_path(orc, cuda):
         fd = op.forward(x.cuda()).cpu()
         ad = op.adjoint(y.cuda()).cpu()
         assert torch.equal(fo, fd) and torch.equal(ao, ad)
+
+
+# ---- fp32 I/O mode (north_star: <= 1e-5 against the fp64 oracle) -----------
+@pytest.mark.parametrize("case", [(0, 4, 1, 10, 1, 2, 4), (0, 3, 1, 16, 2, 1, 4), (0, 2, 0, 9, 1, 1, -1),
+                                  (0, 4, 1, 8, 2, 1, 4)])
+def test_fp32_mode(orc, cuda, case):
+    import torch
+    cw = _cw()
+    fam, nu, bnd, j, q, dim, r0 = case
+    ref = orc.op(*case)
+    spec = cw.WaveletSpec(cw.Family(fam), nu, cw.Boundary(bnd))
+    op = cw.ComposedOp(cw.FastOp(spec, j, q, dim, precision="fp32"), None, True, None if r0 < 0 else r0)
+    x = np.stack([orc.normals(900 + b, ref.nin) for b in range(2)])
+    y = np.stack([orc.normals(950 + b, ref.nout) for b in range(2)])
+    fx = host(op.forward(torch.as_tensor(x, dtype=torch.float32, device="cuda")))
+    ay = host(op.adjoint(torch.as_tensor(y, dtype=torch.float32, device="cuda")))
+    assert fx.dtype == np.float32 and ay.dtype == np.float32
+    for b in range(2):
+        assert rel(fx[b], ref.forward(x[b].astype(np.float32).astype(np.float64))) <= 1e-5
+        assert rel(ay[b], ref.adjoint(y[b].astype(np.float32).astype(np.float64))) <= 1e-5
+    with pytest.raises(cw.CwwError):  # an fp32 op takes float32 buffers only
+        op.forward(torch.as_tensor(x, device="cuda"))
