@@ -61,7 +61,10 @@ __device__ long long cww_phase_buf[1 << 20];
 
 // Forward row: z = H_B( stencil_s(row) + edges ).  trow: physical tile row
 // (sw unused: odd row stride), kp: &kap[0][s] (stride S), es: edge contributions [2NP] or null.
-template <int NU, int LOGB>
+// VEC2: trow is 16-byte aligned and read as double2 pairs (the large strided
+// passes: row stride = 2 (mod 4) doubles makes 16-byte row-per-lane reads
+// bank-conflict free, where 8-byte ones would be 2-way conflicted)
+template <int NU, int LOGB, bool VEC2 = false>
 __device__ __forceinline__ void row_fwd(const double* trow, int sw, const double* kp, int S,
                                         const double* es, double sgR, double* z) {
     using G = Geo<NU, LOGB>;
@@ -71,9 +74,16 @@ __device__ __forceinline__ void row_fwd(const double* trow, int sw, const double
     for (int l = 0; l <= 2 * H; ++l) kap[l] = kp[l * S];
 #pragma unroll
     for (int k = 0; k < B; ++k) z[k] = 0.0;
+    double2 pr = make_double2(0.0, 0.0);
 #pragma unroll
     for (int e = 0; e < CW; ++e) {  // z[k] = sum_l kap[l] row[k - l + h], streamed over e
-        const double r = trow[e];
+        double r;
+        if constexpr (VEC2) {
+            if ((e & 1) == 0) pr = reinterpret_cast<const double2*>(trow)[e >> 1];
+            r = (e & 1) ? pr.y : pr.x;
+        } else {
+            r = trow[e];
+        }
 #pragma unroll
         for (int l = -H; l <= H; ++l) {
             const int k = e + l - H;
@@ -119,9 +129,12 @@ __device__ __forceinline__ void row_adj_accum_pf(double* trow, const double* kp,
                                                  const double* pe, const double* po, long long step) {
     using G = Geo<NU, LOGB>;
     constexpr int B = G::B, H = G::H, CW = G::CW;
+    static_assert(CW % 2 == 0, "double2 row pairs");
     double kap[2 * H + 1];
 #pragma unroll
     for (int l = 0; l <= 2 * H; ++l) kap[l] = kp[l * S];
+    double2* trow2 = reinterpret_cast<double2*>(trow);  // 16-byte aligned rows (row stride = 2 mod 4)
+    double accp = 0.0;
 #pragma unroll
     for (int e = 0; e < CW; ++e) {
         double acc = 0.0;
@@ -130,7 +143,14 @@ __device__ __forceinline__ void row_adj_accum_pf(double* trow, const double* kp,
             const int k = e - H + l;
             if (k >= 0 && k < B) acc += kap[l + H] * y[k];
         }
-        trow[e] = first ? acc : trow[e] + acc;
+        if (e & 1) {  // the pair (e - 1, e) as one 16-byte read-modify-write
+            double2 t = first ? make_double2(0.0, 0.0) : trow2[e >> 1];
+            t.x += accp;
+            t.y += acc;
+            trow2[e >> 1] = t;
+        } else {
+            accp = acc;
+        }
         const int kd = e - 2 * H;  // last use of y[kd] was this column
         if (kd >= 0 && kd < B && pe) {
             const unsigned xb = brev_c(kd, LOGB);
@@ -1963,7 +1983,7 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
         const int rho = rho0 + ng;  // = bitrev_kl(N_lo)
         const double sg = ((__popc(wlo) + __popc(rho)) & 1) ? -1.0 : 1.0;
         double z[B];
-        row_fwd<NU, kLogB>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S,
+        row_fwd<NU, kLogB, true>(T + ng * tst + wlo * RS, wlo, p.tab + p.t.o_kap + s, S,
                            NU > 1 ? ES + s * 2 * NP : nullptr, sg, z);
         // g = bitrev_j(N*B + n_lo) = bitrev5(n_lo)*A + bitrev_kl(N_lo)*R2 + bitrev_kh(N_hi)
         // element index gray_inv_hi(nl) ^ rw = (gx ^ rh) * A + (low a bits), with
