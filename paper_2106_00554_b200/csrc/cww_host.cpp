@@ -816,7 +816,10 @@ cww::SmallArgs small_args(const cww_op* op, const double* in, Layout lin, double
 cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out, Layout lout,
                      long long nvec, bool adj, cudaStream_t st, bool wav = true) {
     if (nvec == 0) return CWW_OK;
-    if (op->j == 10 && wav && !std::getenv("CWW_NO_WV")) {  // warp-per-vector kernels (cww_warp.cuh)
+    // warp-per-vector kernels (cww_warp.cuh) for large batches of 2^10-point
+    // vectors; a few vectors run faster on the CTA-per-group kernels (every
+    // thread of the CTA on one vector: cfg1 0.014 vs 0.018 ms)
+    if (op->j == 10 && wav && nvec >= 256) {
         auto a = small_args(op, in, lin, out, lout, nvec, 8);
         Prof pr(adj ? "wv_adj" : "wv_fwd", st);
         CUDA_TRY(cww::launch_wv(op->nu, a, adj, st));

@@ -228,9 +228,13 @@ __device__ __forceinline__ void wv_idwt_level(const FiltSmem<NU>& F, const Taps<
         const int m = mlo + lane + 32 * k;
         if (m < mhi) idwt_pair_inner<NU>(tp, x, x + np, n, m, vmp, o[2 * k], o[2 * k + 1]);
     }
-    const int nl = 2 * mlo, nr = n - 2 * mhi;  // VMP edge samples (< 32 of them)
-    double oe = 0.0;
-    if (lane < nl + nr) oe = idwt_one<NU>(F, x, x + np, n, lane < nl ? lane : 2 * mhi + (lane - nl), true);
+    const int nl = 2 * mlo, nr = n - 2 * mhi;  // VMP edge samples (<= 36 of them: up to 2 per lane)
+    double oe[2] = {0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int k = lane + 32 * r;
+        if (k < nl + nr) oe[r] = idwt_one<NU>(F, x, x + np, n, k < nl ? k : 2 * mhi + (k - nl), true);
+    }
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
@@ -240,7 +244,11 @@ __device__ __forceinline__ void wv_idwt_level(const FiltSmem<NU>& F, const Taps<
             dst(2 * m + 1) = o[2 * k + 1];
         }
     }
-    if (lane < nl + nr) dst(lane < nl ? lane : 2 * mhi + (lane - nl)) = oe;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int k = lane + 32 * r;
+        if (k < nl + nr) dst(k < nl ? k : 2 * mhi + (k - nl)) = oe[r];
+    }
     __syncwarp();
 }
 

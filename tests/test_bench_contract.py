@@ -15,8 +15,8 @@ sys.path.insert(0, REPO)
 
 def _kernels(cfg):
     fam, nu, bnd, j, q, dim = cfg[:6]
-    if j == 10:
-        return ["wv_fwd", "wv_adj"]  # warp-per-vector kernels (M = 2^10)
+    if j == 10 and dim == 2:
+        return ["wv_fwd", "wv_adj"]  # warp-per-vector kernels (M = 2^10, large batches)
     if dim == 2 or j <= 12:
         return ["small_fwd", "small_adj"]
     return ["wav_coarse", "idwt_pyr", "large_fwd1", "large_fwd2", "large_adj2", "large_adj1", "dwt_pyr"]

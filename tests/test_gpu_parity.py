@@ -486,6 +486,25 @@ def test_pinned_host_async_path(orc, cuda):
         assert torch.equal(fo, fd) and torch.equal(ao, ad)
 
 
+# ---- warp-per-vector kernels (M = 2^10, batches >= 256: the 2D passes) ------
+WV = [(0, 4, 1, 10, 1, 1, 4, 1), (0, 2, 0, 10, 2, 1, -1, 1), (1, 6, 1, 10, 1, 1, 9, 1), (0, 3, 1, 10, 3, 1, 5, 1),
+      (0, 1, 0, 10, 1, 1, 1, 1), (0, 5, 0, 10, 1, 1, 4, 0), (0, 4, 1, 10, 2, 1, 4, 0)]
+
+
+@pytest.mark.parametrize("case", WV, ids=lambda c: "f%d_nu%d_b%d_j%d_q%d_d%d_r%d_i%d" % c)
+def test_parity_warp_kernels(orc, cuda, case):
+    fam, nu, bnd, j, q, dim, r0, use_idwt = case
+    ref = orc.op(fam, nu, bnd, j, q, dim, r0)
+    op = make(fam, nu, bnd, j, q, dim, r0, bool(use_idwt))
+    Bn = 300
+    x = np.stack([orc.normals(1100 + b % 7, ref.nin) * (1 + b) for b in range(Bn)])
+    y = np.stack([orc.normals(1200 + b % 7, ref.nout) * (1 + b) for b in range(Bn)])
+    fx, ay = host(op.forward(gpu(x))), host(op.adjoint(gpu(y)))
+    for b in (0, 1, 150, Bn - 1):
+        assert rel(fx[b], ref.forward(x[b], use_idwt)) <= TOL
+        assert rel(ay[b], ref.adjoint(y[b], use_idwt)) <= TOL
+
+
 # ---- fp32 I/O mode (north_star: <= 1e-5 against the fp64 oracle) -----------
 @pytest.mark.parametrize("case", [(0, 4, 1, 10, 1, 2, 4), (0, 3, 1, 16, 2, 1, 4), (0, 2, 0, 9, 1, 1, -1),
                                   (0, 4, 1, 8, 2, 1, 4)])
