@@ -1051,7 +1051,10 @@ cww_status run_large_slice(const cww_op* op, const double* in, Layout lin, doubl
         a.fuse_top = fuse ? 1 : 0;
         {
             Prof pr("large_fwd1", st);
-            CUDA_TRY(cww::launch_large(nu, 0, a, st));
+            // fused: the persistent ring kernel when the detail windows can be bulk-copied
+            const bool al = fuse && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(xi)) & 15) == 0 &&
+                            (lin.vbase(1) - lin.vbase(0)) % 2 == 0 && xi_vs % 2 == 0;
+            CUDA_TRY(cww::launch_large(nu, al ? 5 : 0, a, st));
         }
         Prof pr("large_fwd2", st);
         CUDA_TRY(cww::launch_large(nu, 1, a, st));

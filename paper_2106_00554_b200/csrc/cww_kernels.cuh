@@ -1939,6 +1939,153 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p)
     }
 }
 
+// Persistent variant of the fused forward pass 1 (16-byte aligned inputs):
+// every CTA walks tasks (vector, chunk) blockIdx.x, +gridDim.x, ...; the
+// window pieces form one ring across the CTA's tasks, so the next task's
+// first two pieces land during this task's halo / Hadamard / store phases,
+// and the G block's bulk store overlaps the next task's first piece.
+template <int NU, int NT>
+__global__ void __launch_bounds__(NT, 2) k_large_fwd1_fz(LargeArgs p) {
+    using Gm = Geo<NU, kLogB>;
+    constexpr int B = Gm::B, H = Gm::H, CW = Gm::CW, RS = CW;
+    constexpr int OFF = (NU + 1) / 2, EL = FiltSmem<NU>::EL, KP = kFusePieces;
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x;
+    const int j = p.j, M = 1 << j, a = j - kLogB, A = 1 << a, half = M >> 1;
+    const int kl = p.kl, R1 = 1 << kl, nch = A >> kl;
+    const long long ntask = (long long)nch * p.nvec;
+    double* T = sm;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(T + R1 * RS);  // [2]
+    double* Wb = T + R1 * RS + 2;                               // [2][C | D][WP]
+    const int ppairs = R1 * B / 2 / KP;
+    const int WP = fuse_window(ppairs, NU);
+    const FiltSmem<NU> F{p.tab + p.t.o_h};
+    const Taps<NU> tp(F);
+    const bool vmp = p.vmp != 0;
+    const int mlo = vmp ? (EL + 1) >> 1 : OFF, mhi = vmp ? (M - EL) >> 1 : half - (NU - OFF);
+    auto task_of = [&](long long lp) { return (long long)blockIdx.x + (lp / KP) * gridDim.x; };
+    // thread 0: bulk copies of this CTA's ring piece lp into buffer lp & 1
+    auto issue = [&](long long lp) {
+        const long long t = task_of(lp);
+        if (t >= ntask) return;
+        const int v = (int)(t / nch), chunk = (int)(t % nch), pc = (int)(lp % KP);
+        const double* cv = p.xi + (long long)v * p.xi_vs;
+        const double* dv = p.in + p.lin.vbase(p.v0 + v) + half;
+        const int mp = chunk * R1 * B / 2 + pc * ppairs;
+        const int ws = max(0, (mp - OFF) & ~1);
+        const int len = min(half, (mp + ppairs + NU - OFF + 1) & ~1) - ws;
+        double* Cw = Wb + (lp & 1) * 2 * WP;
+        mbar_arrive_expect(bar + (lp & 1), (unsigned)(2 * len * 8));
+        bulk_g2s(Cw, cv + ws, (unsigned)(len * 8), bar + (lp & 1));
+        bulk_g2s(Cw + WP, dv + ws, (unsigned)(len * 8), bar + (lp & 1));
+    };
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        issue(0);
+        issue(1);
+    }
+    long long lp = 0;
+    for (long long t = blockIdx.x; t < ntask; t += gridDim.x) {
+        const int v = (int)(t / nch), chunk = (int)(t % nch);
+        const double* cv = p.xi + (long long)v * p.xi_vs;
+        const double* dv = p.in + p.lin.vbase(p.v0 + v) + half;
+        const long long cbase = (long long)chunk * R1 * B;
+        const bool echunk = NU > 1 && (chunk == 0 || cbase + R1 * B >= M);
+        const int m0 = (int)(cbase >> 1);
+        if (tid == 0) bulk_wait_read();  // the previous task's G store has read the tile
+        __syncthreads();
+        for (int pc = 0; pc < KP; ++pc, ++lp) {
+            const int mp = m0 + pc * ppairs;
+            const int ws = max(0, (mp - OFF) & ~1);
+            const double* Cw = Wb + (lp & 1) * 2 * WP;
+            const double* Dw = Cw + WP;
+            mbar_wait(bar + (lp & 1), (unsigned)((lp >> 1) & 1));
+            for (int q = tid; q < ppairs; q += NT) {
+                const int m = mp + q;
+                double o0, o1;
+                if (m >= mlo && m < mhi) {
+                    const double* cw = Cw + (m - OFF - ws);
+                    const double* dw = Dw + (m - OFF - ws);
+                    double c[NU + 1], d[NU + 1];
+#pragma unroll
+                    for (int k = 0; k <= NU; ++k) {
+                        c[k] = cw[k];
+                        d[k] = dw[k];
+                    }
+                    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                    for (int u = -NU + 1; u <= NU; ++u) {
+                        if ((u & 1) == 0) {
+                            a0 = fma(tp.h[u + NU - 1], c[OFF - u / 2], a0);
+                            b0 = fma(tp.g[u + NU - 1], d[OFF - u / 2], b0);
+                        } else {
+                            a1 = fma(tp.h[u + NU - 1], c[OFF - (u - 1) / 2], a1);
+                            b1 = fma(tp.g[u + NU - 1], d[OFF - (u - 1) / 2], b1);
+                        }
+                    }
+                    o0 = a0 + b0;
+                    o1 = a1 + b1;
+                } else {
+                    o0 = idwt_one<NU>(F, cv, dv, M, 2 * m, vmp);
+                    o1 = idwt_one<NU>(F, cv, dv, M, 2 * m + 1, vmp);
+                }
+                const int pos = 2 * m, rl = (pos - (int)cbase) >> kLogB, col = pos & (B - 1);
+                double* dst = T + (int)brev_bits((unsigned)rl, kl) * RS + H + col;
+                if (echunk && (pos < NU || pos + 1 >= M - NU)) {
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int q2 = pos + e;
+                        const double o = e ? o1 : o0;
+                        if (q2 < NU || q2 >= M - NU) {
+                            p.ev[(long long)v * 2 * NU + (q2 < NU ? q2 : NU + (q2 - (M - NU)))] = o;
+                            dst[e] = 0.0;
+                        } else {
+                            dst[e] = o;
+                        }
+                    }
+                } else {
+                    dst[0] = o0;
+                    dst[1] = o1;
+                }
+            }
+            __syncthreads();  // buffer lp & 1 is free: refill it with ring piece lp + 2
+            if (tid == 0) issue(lp + 2);
+        }
+        if (H > 0 && tid < 2 * H) {  // outer halos: samples of the neighbouring chunks
+            const bool left = tid < H;
+            const int c = left ? tid : tid - H;
+            const long long pos = left ? cbase - H + c : cbase + (long long)R1 * B + c;
+            double* dst = left ? T + c : T + (int)brev_bits((unsigned)(R1 - 1), kl) * RS + B + H + c;
+            *dst = (pos >= 0 && pos < M && !(NU > 1 && (pos < NU || pos >= M - NU)))
+                       ? idwt_one<NU>(F, cv, dv, M, (int)pos, vmp)
+                       : 0.0;
+        }
+        __syncthreads();
+        if (H > 0) {  // inner halos: copies of the neighbouring rows' own columns
+            for (int f = tid; f < (R1 - 1) * 2 * H; f += NT) {
+                const int K = f / (2 * H), c = f % (2 * H);
+                const int p0 = (int)brev_bits((unsigned)K, kl) * RS, p1 = (int)brev_bits((unsigned)(K + 1), kl) * RS;
+                if (c < H) T[p0 + B + H + c] = T[p1 + H + c];
+                else T[p1 + (c - H)] = T[p0 + B + (c - H)];
+            }
+            __syncthreads();
+        }
+        tile_hadamard_inl<CW, RS, CWW_CONTIG_MAXR>(T, 1, kl, 0, kl, 0, tid, NT);
+        double* g = p.G + (long long)v * A * CW + (long long)chunk * R1 * CW;
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            bulk_s2g(g, T, (unsigned)(R1 * CW * 8));
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait_read();
+}
+
 template <int NU, int NT>
 __global__ void __launch_bounds__(NT, 2) k_large_fwd2(LargeArgs p) {
     using Gm = Geo<NU, kLogB>;

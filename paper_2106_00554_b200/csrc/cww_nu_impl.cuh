@@ -113,6 +113,20 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
             if (cudaError_t e = launch_k(k, g2, CWW_NT, s2a, st, a); e != cudaSuccess) return e;
             break;
         }
+        case 5: {  // persistent fused forward pass 1: as many CTAs as fit on the device
+            s1 += (2 + 4ll * fuse_window(R1 * (1 << kLogB) / 2 / kFusePieces, CWW_NU)) * 8;
+            auto k = k_large_fwd1_fz<CWW_NU, CWW_NT>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+            int dev = 0, nsm = 0, per = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, CWW_NT, (size_t)s1);
+            const long long ntask = (long long)(1 << kh) * a.nvec;
+            long long grid = (long long)nsm * (per > 0 ? per : 1);
+            if (grid > ntask) grid = ntask;
+            if (cudaError_t e = launch_k(k, (int)grid, CWW_NT, s1, st, a); e != cudaSuccess) return e;
+            break;
+        }
         case 4: {  // straddling finest-level analysis rows (fused adjoint pass 1)
             const long long tot = a.nvec * (R1 ? (1ll << a.j) / ((long long)R1 << kLogB) : 0) * (CWW_NU / 2) * 2;
             if (tot == 0) return cudaSuccess;
