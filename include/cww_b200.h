@@ -176,8 +176,8 @@ cww_status cww_adjoint_host(const cww_op* op, const double* y, size_t y_len, dou
  * / cudaHostRegister; pageable buffers take the synchronous path): the batch
  * is split into chunks whose host-to-device copy, compute and device-to-host
  * copy run on three streams, so copies in both PCIe directions overlap the
- * compute and each other.  Tiny transforms (input + output <= 256 KB, env
- * CWW_ZERO_COPY_KB; small path only) skip the copies: the kernels read and
+ * compute and each other.  Tiny transforms (input + output <= 256 KB,
+ * small path only) skip the copies: the kernels read and
  * write the pinned buffers over PCIe directly (zero-copy).  Enqueued behind
  * `stream`, which is made to wait for the last copy; returns without
  * synchronising. */

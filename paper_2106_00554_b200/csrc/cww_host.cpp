@@ -774,7 +774,6 @@ cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
 Layout lay_contig(long long len) { return Layout{0, len, 0, 1, 62, 62}; }
 
 // largest power of two V <= cap with V*M <= 4096 (one small-path CTA)
-int env_int(const char* name, int dflt);
 
 int small_V(long long M, long long nvec, int cap = 32) {
     int V = 1;
@@ -847,10 +846,6 @@ cww_status run_small(const cww_op* op, const double* in, Layout lin, double* out
     return CWW_OK;
 }
 
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e && *e ? std::atoi(e) : dflt;
-}
 
 // Wavelet pyramid plan of the large path
 constexpr int kPyrSynBot = 10;      // coarse levels <= 10: k_wav_coarse (one CTA per vector)
