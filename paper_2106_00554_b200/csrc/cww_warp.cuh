@@ -223,11 +223,19 @@ __device__ __forceinline__ void wv_idwt_level(const FiltSmem<NU>& F, const Taps<
     }
     const int mlo = vmp ? (EL + 1) >> 1 : 0, mhi = vmp ? (n - EL) >> 1 : np;
     double o[2 * KP];
+    // interior pairs as quads (pairs m, m + 1 from one window of nu + 2 samples,
+    // read as 16-byte pairs when the window start m - OFF is even): lane l takes
+    // quads l, l + 32, ...; an odd pair count leaves one pair for the last lane
+    constexpr int KQ = KP / 2;
+    const int nq = (mhi - mlo) >> 1;
+    const bool odd = ((mhi - mlo) & 1) != 0;
 #pragma unroll
-    for (int k = 0; k < KP; ++k) {
-        const int m = mlo + lane + 32 * k;
-        if (m < mhi) idwt_pair_inner<NU>(tp, x, x + np, n, m, vmp, o[2 * k], o[2 * k + 1]);
+    for (int k = 0; k < KQ; ++k) {
+        const int q = lane + 32 * k;
+        if (q < nq) idwt_quad_inner<NU>(tp, x, x + np, n, mlo + 2 * q, vmp, o + 4 * k);
     }
+    double ol0 = 0.0, ol1 = 0.0;
+    if (odd && lane == 31) idwt_pair_inner<NU>(tp, x, x + np, n, mhi - 1, vmp, ol0, ol1);
     const int nl = 2 * mlo, nr = n - 2 * mhi;  // VMP edge samples (<= 36 of them: up to 2 per lane)
     double oe[2] = {0.0, 0.0};
 #pragma unroll
@@ -237,12 +245,19 @@ __device__ __forceinline__ void wv_idwt_level(const FiltSmem<NU>& F, const Taps<
     }
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < KP; ++k) {
-        const int m = mlo + lane + 32 * k;
-        if (m < mhi) {
-            dst(2 * m) = o[2 * k];
-            dst(2 * m + 1) = o[2 * k + 1];
+    for (int k = 0; k < KQ; ++k) {
+        const int q = lane + 32 * k;
+        if (q < nq) {
+            const int m = mlo + 2 * q;
+            dst(2 * m) = o[4 * k];
+            dst(2 * m + 1) = o[4 * k + 1];
+            dst(2 * m + 2) = o[4 * k + 2];
+            dst(2 * m + 3) = o[4 * k + 3];
         }
+    }
+    if (odd && lane == 31) {
+        dst(2 * (mhi - 1)) = ol0;
+        dst(2 * (mhi - 1) + 1) = ol1;
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
