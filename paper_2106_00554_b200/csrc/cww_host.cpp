@@ -755,6 +755,9 @@ cww_status validate(const cww_op_desc* d) {
     if (int(d->j) < J0) return fail(CWW_ERR_SPEC, "FastOp: j must be >= ceil(log2(2 nu))");
     if (d->nu >= 2 && d->q < 1) return fail(CWW_ERR_SPEC, "FastOp: q must be >= 1");
     if (d->j + d->q > 30) return fail(CWW_ERR_UNSUPPORTED, "j + q must be <= 30");
+    // the two-pass large path holds 2^(j-5) tile rows in two shared-memory
+    // passes of <= 512 rows each (one 2^23-point vector per pass pair)
+    if (d->j > 23) return fail(CWW_ERR_UNSUPPORTED, "j must be <= 23 (M = 2^23 wavelet coefficients per axis)");
     if (d->j < 1) return fail(CWW_ERR_UNSUPPORTED, "j must be >= 1 (M = 1 is not supported)");
     if (d->q > 10) return fail(CWW_ERR_UNSUPPORTED, "q must be <= 10");
     if (d->dim == 2 && d->j + d->q > 17)
@@ -975,7 +978,8 @@ struct LargePlan {
 LargePlan large_plan(unsigned j) {
     int a = int(j) - cww::kLogB;
     int kl = (a + 1) / 2;
-    if (kl > 8) kl = 8;
+    if (kl > 8) kl = 8;    // pass-1 tiles of 256 rows (3 CTAs per SM) ...
+    if (a - kl > 9) kl = a - 9;  // ... unless pass 2 would exceed 512 rows (j = 23: 512 x 512 rows)
     int kh = a - kl;
     int ng = 1;
     while (ng * (1 << kh) < 128 && ng * 2 <= (1 << kl)) ng *= 2;

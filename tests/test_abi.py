@@ -42,6 +42,7 @@ def _desc(**kw):
     (dict(nu=7), 3), (dict(nu=0), 3), (dict(nu=1, boundary=1), 3), (dict(nu=1, family=1, boundary=0), 3),
     (dict(nu=4, j=2), 3), (dict(nu=2, q=0), 3), (dict(dim=3), 3), (dict(nu=4, j=6, min_level=2), 3),
     (dict(nu=2, j=5, min_level=6), 3), (dict(family=5), 1), (dict(nu=2, j=17, q=1, dim=2), 7),
+    (dict(nu=3, j=24, q=1), 7), (dict(nu=3, j=20, q=2, precision=2), 1),
 ])
 def test_spec_validation(kw, status):
     import paper_2106_00554_b200 as cw
