@@ -65,7 +65,7 @@ __device__ __forceinline__ void lane_hadamard(double (&r)[N], int lane) {
 __device__ __forceinline__ void wv_coop_load(double* XB, const double* in, const Layout& L, long long v0, int nv,
                                              long long off, int cnt, int tid) {
     constexpr int U = 8;
-    const int v = tid & (kWvV - 1), k0 = tid >> 3;
+    const int v = tid & (kWvV - 1), k0 = tid / kWvV;
     double* xb = XB + v * kWvXS;
     if (v >= nv) return;
     if (L.esh >= 62) {
@@ -84,7 +84,7 @@ __device__ __forceinline__ void wv_coop_load(double* XB, const double* in, const
 }
 __device__ __forceinline__ void wv_coop_store(const double* XB, double* out, const Layout& L, long long v0, int nv,
                                               long long off, int cnt, int tid) {
-    const int v = tid & (kWvV - 1), k0 = tid >> 3;
+    const int v = tid & (kWvV - 1), k0 = tid / kWvV;
     const double* xb = XB + v * kWvXS;
     if (v >= nv) return;
     if (L.esh >= 62) {
