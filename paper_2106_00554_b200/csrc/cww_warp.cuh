@@ -27,7 +27,7 @@
 namespace cww {
 
 constexpr int kWvJ = 10;                     // M = 1024
-constexpr int kWvXS = 1060;  // per-warp region: 1024 + 32 pads (+4); = 4 (mod 16): the 8 regions' banks interleave
+constexpr int kWvXS = 1092;  // per-warp region: 1024 + 64 pads (+4); = 4 (mod 16): the 8 regions' banks interleave
 constexpr int kWvNT = 256;                   // 8 warps = 8 vectors per CTA
 constexpr int kWvV = kWvNT / 32;
 #ifndef WV_MINB
@@ -36,6 +36,33 @@ constexpr int kWvV = kWvNT / 32;
 
 // padded position: one pad per 32 so that lane l's row (33 l + c) is conflict free
 __device__ __forceinline__ int wv_pad(int p) { return p + (p >> 5); }
+// the adjoint's coefficient vector: one pad per 16, conflict free for every
+// lane stride up to 16 (the register level's 16-row segments per lane)
+__device__ __forceinline__ int p16(int k) { return k + (k >> 4); }
+
+// element REL (compile time, may be < 0 or >= P) relative to this lane's first
+// sample of a level distributed P per lane (wrapping across lanes 31 <-> 0)
+template <int P, int REL>
+__device__ __forceinline__ double lane_rel(const double (&c)[P], int lane) {
+    if constexpr (REL >= 0 && REL < P) {
+        return c[REL];
+    } else if constexpr (REL < 0) {
+        constexpr int SO = (-REL + P - 1) / P, IDX = REL + SO * P;
+        return __shfl_sync(0xffffffffu, c[IDX], (lane - SO) & 31);
+    } else {
+        constexpr int SO = REL / P, IDX = REL - SO * P;
+        return __shfl_sync(0xffffffffu, c[IDX], (lane + SO) & 31);
+    }
+}
+
+// w[i] = element T0 + i relative to this lane's first sample, i < N
+template <int P, int T0, int N, int I = 0>
+__device__ __forceinline__ void lane_window(const double (&c)[P], double (&w)[N], int lane) {
+    if constexpr (I < N) {
+        w[I] = lane_rel<P, T0 + I>(c, lane);
+        lane_window<P, T0, N, I + 1>(c, w, lane);
+    }
+}
 
 template <int NU>
 inline long long wv_smem_bytes(int S) {
@@ -82,6 +109,7 @@ __device__ __forceinline__ void wv_coop_load(double* XB, const double* in, const
     }
     for (int k = k0; k < cnt; k += 32) xb[k] = __ldg(in + L.at(v0 + v, off + k));
 }
+template <bool PAD = false>
 __device__ __forceinline__ void wv_coop_store(const double* XB, double* out, const Layout& L, long long v0, int nv,
                                               long long off, int cnt, int tid) {
     const int v = tid & (kWvV - 1), k0 = tid / kWvV;
@@ -91,10 +119,10 @@ __device__ __forceinline__ void wv_coop_store(const double* XB, double* out, con
         double* dst = out + L.vbase(v0 + v) + (off + k0) * L.es;
         const long long st = 32 * L.es;
 #pragma unroll 8
-        for (int i = 0; i < cnt / 32; ++i) dst[i * st] = xb[k0 + 32 * i];
+        for (int i = 0; i < cnt / 32; ++i) dst[i * st] = xb[PAD ? p16(k0 + 32 * i) : k0 + 32 * i];
         return;
     }
-    for (int k = k0; k < cnt; k += 32) out[L.at(v0 + v, off + k)] = xb[k];
+    for (int k = k0; k < cnt; k += 32) out[L.at(v0 + v, off + k)] = xb[PAD ? p16(k) : k];
 }
 // one vector's elements [off, off + cnt) by its own warp (lanes over k):
 // contiguous layouts as 16-byte loads, others element-wise
@@ -124,15 +152,15 @@ __device__ __forceinline__ void wv_warp_load(double* X, const double* vb, const 
     }
 }
 
-// one analysis level n -> n/2 in place (c to x[0:n/2], d to x[n/2:n]), reading
-// the padded xi when PADDED; register-staged (read all, __syncwarp, write)
-template <int NU, bool PADDED>
+// one analysis level n -> n/2 (n <= 512) in place in the p16-padded
+// coefficient vector (c to [0:n/2], d to [n/2:n]); register-staged
+template <int NU>
 __device__ __forceinline__ void wv_dwt_level(const FiltSmem<NU>& F, const Taps<NU>& tp, double* X, int n, bool vmp,
                                              int lane) {
     constexpr int EL = FiltSmem<NU>::EL;
-    constexpr int KM = (PADDED ? (1 << kWvJ) : (1 << (kWvJ - 1))) / 2 / 32;
+    constexpr int KM = (1 << (kWvJ - 1)) / 2 / 32;
     const int half = n >> 1;
-    auto xv = [&](int i) { return X[PADDED ? wv_pad(i) : i]; };
+    auto xv = [&](int i) { return X[p16(i)]; };
     double cc[KM], dd[KM];
     const int rlo = vmp ? NU : 0, rhi = vmp ? half - NU : half;
 #pragma unroll
@@ -141,29 +169,16 @@ __device__ __forceinline__ void wv_dwt_level(const FiltSmem<NU>& F, const Taps<N
         if (mm < rhi) {
             double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
             const int i0 = 2 * mm - NU + 1;
-            if (vmp || (i0 >= 0 && i0 + 2 * NU <= n)) {  // no wrap
+            const bool wrap = !vmp && !(i0 >= 0 && i0 + 2 * NU <= n);
 #pragma unroll
-                for (int u = 0; u < 2 * NU; ++u) {
-                    const double x = xv(i0 + u);
-                    if (u & 1) {
-                        a1 = fma(tp.h[u], x, a1);
-                        b1 = fma(tp.g[u], x, b1);
-                    } else {
-                        a0 = fma(tp.h[u], x, a0);
-                        b0 = fma(tp.g[u], x, b0);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < 2 * NU; ++u) {
-                    const double x = xv((i0 + u) & (n - 1));
-                    if (u & 1) {
-                        a1 = fma(tp.h[u], x, a1);
-                        b1 = fma(tp.g[u], x, b1);
-                    } else {
-                        a0 = fma(tp.h[u], x, a0);
-                        b0 = fma(tp.g[u], x, b0);
-                    }
+            for (int u = 0; u < 2 * NU; ++u) {
+                const double x = xv(wrap ? ((i0 + u) & (n - 1)) : i0 + u);
+                if (u & 1) {
+                    a1 = fma(tp.h[u], x, a1);
+                    b1 = fma(tp.g[u], x, b1);
+                } else {
+                    a0 = fma(tp.h[u], x, a0);
+                    b0 = fma(tp.g[u], x, b0);
                 }
             }
             cc[k] = a0 + a1;
@@ -188,14 +203,14 @@ __device__ __forceinline__ void wv_dwt_level(const FiltSmem<NU>& F, const Taps<N
     for (int k = 0; k < KM; ++k) {
         const int mm = rlo + lane + 32 * k;
         if (mm < rhi) {
-            X[mm] = cc[k];
-            X[half + mm] = dd[k];
+            X[p16(mm)] = cc[k];
+            X[p16(half + mm)] = dd[k];
         }
     }
     if (vmp && lane < 2 * NU) {
         const int mm = lane < NU ? lane : half - 1 - (lane - NU);
-        X[mm] = ce;
-        X[half + mm] = de;
+        X[p16(mm)] = ce;
+        X[p16(half + mm)] = de;
     }
     __syncwarp();
 }
@@ -465,36 +480,70 @@ __global__ void __launch_bounds__(kWvNT, WV_MINB) k_wv_adj(SmallArgs p) {
                 xi[lane == 0 ? k : B - NU + k] = e0 + e1;
             }
         }
-#pragma unroll
-        for (int c = 0; c < B; ++c) X[wv_pad(lane * B + c)] = xi[c];
-        __syncwarp();
         const bool dwt = p.use_idwt && p.r0 < kWvJ;
-        if (!dwt) {  // FastOp adjoint: xi is the output (unpadded into the region)
-            double o[32];
+        if (!dwt) {  // FastOp adjoint: xi is the output
 #pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] = X[wv_pad(lane + 32 * k)];
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 32; ++k) X[lane + 32 * k] = o[k];
-            __syncwarp();
+            for (int c = 0; c < B; ++c) X[p16(lane * B + c)] = xi[c];
         } else {
-            // DWT levels in place: level n -> c to x[0:n/2], d to x[n/2:n] (register
-            // staged); level 10 reads the padded xi.  The region ends as
-            // [c_r0 | d_r0 | ... | d_9], the output layout.
+            // level 10 -> 9 straight from the rows in registers (lane l: rows 16 l ..
+            // 16 l + 15 from xi[32 l - NU + 1 .. 32 l + 31 + NU], halos by shuffles),
+            // c_9 and d_9 into the p16-padded coefficient vector; then levels
+            // 9 .. r0 + 1 in place there, which ends as [c_r0 | d_r0 | ... | d_9]
             const Taps<NU> tp(F);
-            wv_dwt_level<NU, true>(F, tp, X, M, vmp, lane);
-            for (int n = M / 2; n > (1 << p.r0); n >>= 1) wv_dwt_level<NU, false>(F, tp, X, n, vmp, lane);
+            constexpr int WN = B + 2 * NU - 2;
+            double xw[WN];
+            lane_window<B, -NU + 1, WN>(xi, xw, lane);
+#pragma unroll
+            for (int t = 0; t < B / 2; ++t) {
+                const int mm = (B / 2) * lane + t;
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int u = 0; u < 2 * NU; ++u) {
+                    const double x = xw[2 * t + u];
+                    if (u & 1) {
+                        a1 = fma(tp.h[u], x, a1);
+                        b1 = fma(tp.g[u], x, b1);
+                    } else {
+                        a0 = fma(tp.h[u], x, a0);
+                        b0 = fma(tp.g[u], x, b0);
+                    }
+                }
+                X[p16(mm)] = a0 + a1;
+                X[p16(M / 2 + mm)] = b0 + b1;
+            }
+            if (vmp && (lane == 0 || lane == A - 1)) {  // VMP edge rows: dense rows over this lane's own samples
+                const int side = lane == 0 ? 0 : 1;
+                constexpr int EL = FiltSmem<NU>::EL;
+#pragma unroll
+                for (int m = 0; m < NU; ++m) {
+                    const double* ra = F.ana(side, 0, m);
+                    const double* rb = F.ana(side, 1, m);
+                    double ce = 0.0, de = 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < EL; ++kk) {
+                        const double x = side ? xi[B - 1 - kk] : xi[kk];
+                        ce = fma(ra[kk], x, ce);
+                        de = fma(rb[kk], x, de);
+                    }
+                    const int mm = side ? M / 2 - 1 - m : m;
+                    X[p16(mm)] = ce;
+                    X[p16(M / 2 + mm)] = de;
+                }
+            }
+            __syncwarp();
+            for (int n = M / 2; n > (1 << p.r0); n >>= 1) wv_dwt_level<NU>(F, tp, X, n, vmp, lane);
         }
+        __syncwarp();
     }
     if (!ovf) {
         if (act) {
 #pragma unroll 8
-            for (int k = lane; k < M; k += 32) ob[p.lout.eoff(k)] = X[k];
+            for (int k = lane; k < M; k += 32) ob[p.lout.eoff(k)] = X[p16(k)];
         }
         return;
     }
     __syncthreads();
-    wv_coop_store(XB, p.out, p.lout, v0, nv, 0, M, tid);
+    wv_coop_store<true>(XB, p.out, p.lout, v0, nv, 0, M, tid);
 }
 
 }  // namespace cww
