@@ -998,6 +998,16 @@ long long large_slice(const cww_op* op, long long nvec) {
     return std::max(1ll, std::min(nvec, (4ll << 30) / per));
 }
 
+static int pf_dist() {
+    static int v = [] { const char* e = getenv("CWW_PFD"); return e ? atoi(e) : 32; }();
+    return v;
+}
+
+static int pf_dist1() {
+    static int v = [] { const char* e = getenv("CWW_PFD1"); return e ? atoi(e) : 111; }();
+    return v;
+}
+
 struct LargeBufs {
     DevBuf w0, w1, G, ev, epw, apart;
 };
@@ -1029,6 +1039,9 @@ cww_status run_large_slice(const cww_op* op, const double* in, Layout lin, doubl
     a.r0 = op->r0;
     a.use_idwt = op->d.use_idwt;
     a.vmp = op->vmp;
+    a.pfd = pf_dist();
+    a.pfd1 = pf_dist1();
+    { const char* e = getenv("CWW_PFS"); a.pfs = e ? atoi(e) : 1; }
     if (!adj) {
         // levels r0+1 .. j-1 by the pyramids and level j inside pass 1 (fuse_top)
         // when the batch's xi would not stay L2-resident (> 32 MB); else the

@@ -2192,6 +2192,29 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 #pragma unroll
             for (int nl = 0; nl < B; ++nl) y[nl] = 0.0;
         }
+        // L2 prefetch of the first sequency block of the CTA that will take this
+        // one's place (linear block index + pfd, CTAs dispatch in order): 32
+        // contiguous runs of R2 doubles per sub-tile, one per lane
+        if (it == 0 && p.pfd > 0 && tid < 32) {
+            const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + p.pfd;
+            if (lin < (long long)gridDim.x * gridDim.y) {
+                const int bx = (int)(lin % gridDim.x);
+                const long long vy = lin / gridDim.x;
+                const double* ibn = p.in + p.lin.vbase(p.v0 + vy);
+                const unsigned x = brev_bits((unsigned)tid, kLogB);
+                const long long gx = (long long)gray_inv(x);
+                for (int g2 = 0; g2 < NG; ++g2) {
+                    const unsigned gl0 = (unsigned)(bx * NG + g2) << kh;
+                    unsigned rl0 = gray_inv(gl0) & (unsigned)(A - 1);
+                    if (__popc(x) & 1) rl0 ^= (unsigned)(A - 1);
+                    rl0 &= ~(unsigned)(R2 - 1);
+                    l2_prefetch(ibn + gx * A + rl0, (unsigned)(R2 * 8));
+                    for (int s2 = 1; s2 < p.pfs; ++s2)  // later blocks: odd ones mirrored (index ^ (M - 1))
+                        l2_prefetch(ibn + (long long)s2 * M + (((gx * A + rl0) ^ ((s2 & 1) ? (long long)(M - 1) : 0ll)) & ~(long long)(R2 - 1)),
+                                    (unsigned)(R2 * 8));
+                }
+            }
+        }
         for (int s = 0; s < S; ++s) {
             hadamard_reg<kLogB>(y);
             if (NU > 1) {  // per-warp partial sums, one slot per (CTA, iteration, warp)
@@ -2265,6 +2288,10 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
         mbar_init(bar, 1);
         mbar_arrive_expect(bar, (unsigned)(R1 * CW * 8));
         bulk_g2s(T, g + (long long)chunk * R1 * CW, (unsigned)(R1 * CW * 8), bar);
+        // L2 prefetch of the G block of the CTA that will take this one's place
+        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + p.pfd1;
+        if (p.pfd1 > 0 && lin < (long long)gridDim.x * gridDim.y)
+            l2_prefetch(p.G + ((lin / gridDim.x) * A + (lin % gridDim.x) * R1) * CW, (unsigned)(R1 * CW * 8));
     }
     // halo contributions from the neighbouring chunks' boundary rows (sums over
     // the physical rows rho of their Hadamard rows; popc is bit-reversal invariant):
@@ -2342,7 +2369,24 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
     // into the tile's own columns [H, B + H) -- each (row, column) is read and
     // written by one thread only, and the halo columns stay intact
     double* xw = (p.xo_is_output || fana) ? nullptr : xo + base + lane;
-    if (!has_edge && (xw || fana)) {  // interior chunks: four rows in flight per warp (independent chains)
+    if (!has_edge && fana) {
+        // fused analysis, interior chunks: the tile's columns [H, B + H) already
+        // hold xi except for the 2H columns per row that receive a neighbour
+        // row's halo: (row, halo column) per thread, in place (the halo columns
+        // themselves are never written)
+        if (NU > 1) {
+            for (int idx = tid; idx < R1 * 2 * H; idx += NT) {
+                const int r = idx / (2 * H), hh = idx - r * 2 * H;
+                const bool left = hh < H;
+                const int c = left ? hh : B - 2 * H + hh;  // xi column
+                const int rn = left ? r - 1 : r + 1;
+                const double add = (rn >= 0 && rn < R1)
+                                       ? T[(int)brev_bits((unsigned)rn, kl) * RS + (left ? B + H + c : c - (B - H))]
+                                       : nb[hh];
+                T[(int)brev_bits((unsigned)r, kl) * RS + H + c] += add;
+            }
+        }
+    } else if (!has_edge && (xw || fana)) {  // interior chunks: four rows in flight per warp (independent chains)
 #pragma unroll 4
         for (int rl = tid >> 5; rl < R1; rl += NT / 32) {
             const int ph = (int)brev_bits((unsigned)rl, kl);
@@ -2409,6 +2453,51 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
         const int mlo = m0 + (lb ? NS - FL : 0), mhi = m0 + CH / 2 - (rb ? FL : 0);
         double* cws = xo;  // c_{j-1}
         double* dout = ob + half;
+        if (!has_edge) {
+            // interior chunks: 16 pairs per tile row, thread = (row, pair t); the
+            // window xi[32 r + 2t - H .. + 2nu) is the row's extended columns
+            // e = 2t .. 2t + 2nu - 1 (nu aligned 16-byte loads), except e < H
+            // (previous row's last columns) and e >= B + H (next row's first)
+            static_assert(B == 32, "16 pairs per row");
+            const int t = tid & 15;
+            const bool lo_x = NU > 1 && 2 * t < H, hi_x = NU > 1 && 2 * t + 2 * NU - 1 >= B + H;
+            for (int r = tid >> 4; r < R1; r += NT / 16) {
+                const int m = m0 + 16 * r + t;
+                const double* row = T + (int)brev_bits((unsigned)r, kl) * RS;
+                const double2* rp = reinterpret_cast<const double2*>(row + 2 * t);
+                double x[2 * NU];
+#pragma unroll
+                for (int i = 0; i < NU; ++i) {
+                    const double2 pr = rp[i];
+                    x[2 * i] = pr.x;
+                    x[2 * i + 1] = pr.y;
+                }
+                if (lo_x && r > 0) {
+                    const double* rq = T + (int)brev_bits((unsigned)(r - 1), kl) * RS + B;
+#pragma unroll
+                    for (int k = 0; k < H; ++k)
+                        if (2 * t + k < H) x[k] = rq[2 * t + k];
+                }
+                if (hi_x && r + 1 < R1) {
+                    const double* rq = T + (int)brev_bits((unsigned)(r + 1), kl) * RS - B;
+#pragma unroll
+                    for (int k = 2 * NU - H; k < 2 * NU; ++k)
+                        if (2 * t + k >= B + H) x[k] = rq[2 * t + k];
+                }
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < 2 * NU; k += 2) {
+                    a0 = fma(tp.h[k], x[k], a0);
+                    b0 = fma(tp.g[k], x[k], b0);
+                    a1 = fma(tp.h[k + 1], x[k + 1], a1);
+                    b1 = fma(tp.g[k + 1], x[k + 1], b1);
+                }
+                if (m >= mlo && m < mhi) {
+                    cws[m] = a0 + a1;
+                    dout[m] = b0 + b1;
+                }
+            }
+        } else
         for (int m = mlo + tid; m < mhi; m += NT) {
             double c, d;
             if (vmp && (m < NU || m >= half - NU)) {

@@ -75,6 +75,9 @@ struct LargeArgs {
     // summed by launch_ana_fixup
     int fuse_ana;
     double* apart;
+    // L2 prefetch distance in CTAs (0: off): a CTA prefetches the first loads of
+    // the CTA pfd linear block indices ahead (the one that will replace it)
+    int pfd, pfd1, pfs;  // adjoint pass 2 / pass 1
 };
 
 struct WavArgs {
