@@ -595,6 +595,16 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned 
 __device__ __forceinline__ void l2_prefetch(const void* gsrc, unsigned bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gsrc), "r"(bytes) : "memory");
 }
+// L2 prefetch of the doubles [src, src + n) clipped to [lim_lo, lim_hi) and
+// widened to 16-byte granules inside those limits
+__device__ __forceinline__ void l2_prefetch_span(const double* src, int n, const double* lim_lo,
+                                                 const double* lim_hi) {
+    uintptr_t a = reinterpret_cast<uintptr_t>(src < lim_lo ? lim_lo : src);
+    uintptr_t b = reinterpret_cast<uintptr_t>(src + n > lim_hi ? lim_hi : src + n);
+    a = (a + 15) & ~uintptr_t(15);
+    b &= ~uintptr_t(15);
+    if (b > a) l2_prefetch(reinterpret_cast<const void*>(a), (unsigned)(b - a));
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // this thread's bulk stores have finished READING shared memory
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }

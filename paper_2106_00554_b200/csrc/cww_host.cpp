@@ -598,6 +598,7 @@ struct EdgeTerm {
 struct cww_op {
     cww_op_desc d{};
     int nu = 1, vmp = 0, r0 = 0, dim = 1, device = 0;
+    int nsm = 148;  // SM count of the device (L2 prefetch distances)
     unsigned j = 0, q = 0;
     long long M = 1, N = 1, S = 1;
     Filters f;
@@ -862,6 +863,7 @@ cww::PyrArgs pyr_args(const cww_op* op, long long nvec) {
     y.nvec = nvec;
     y.vmp = op->vmp;
     y.r0 = op->r0;
+    y.pfd = 3 * op->nsm / 2;  // L2 prefetch 1.5 waves of CTAs ahead (measured at config 3)
     return y;
 }
 
@@ -998,16 +1000,6 @@ long long large_slice(const cww_op* op, long long nvec) {
     return std::max(1ll, std::min(nvec, (4ll << 30) / per));
 }
 
-static int pf_dist() {
-    static int v = [] { const char* e = getenv("CWW_PFD"); return e ? atoi(e) : 32; }();
-    return v;
-}
-
-static int pf_dist1() {
-    static int v = [] { const char* e = getenv("CWW_PFD1"); return e ? atoi(e) : 111; }();
-    return v;
-}
-
 struct LargeBufs {
     DevBuf w0, w1, G, ev, epw, apart;
 };
@@ -1039,9 +1031,10 @@ cww_status run_large_slice(const cww_op* op, const double* in, Layout lin, doubl
     a.r0 = op->r0;
     a.use_idwt = op->d.use_idwt;
     a.vmp = op->vmp;
-    a.pfd = pf_dist();
-    a.pfd1 = pf_dist1();
-    { const char* e = getenv("CWW_PFS"); a.pfs = e ? atoi(e) : 1; }
+    // L2 prefetch distances (measured at config 3: 3/4 of a wave ahead for the
+    // contiguous pass, one sequency block ahead in the strided pass)
+    a.pfd1 = 3 * op->nsm / 4;
+    a.pfs = pl.ng_adj == 1 ? 1 : 0;  // (sub-tiled CTAs: many short runs, the prefetches cost more than they hide)
     if (!adj) {
         // levels r0+1 .. j-1 by the pyramids and level j inside pass 1 (fuse_top)
         // when the batch's xi would not stay L2-resident (> 32 MB); else the
@@ -1303,6 +1296,7 @@ cww_status cww_op_create(const cww_op_desc* desc, cww_op** out) {
         CUDA_TRY(cudaGetDevice(&op->device));
     }
     CUDA_TRY(cudaSetDevice(op->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&op->nsm, cudaDevAttrMultiProcessorCount, op->device));
     if ((s = load_filters(desc->family, desc->nu, op->data_dir.c_str(), op->f)) != CWW_OK) return s;
     int R = desc->kernel_resolution > 0 ? desc->kernel_resolution : 14;
     g_gpu_cascade = desc->gpu_kernel_table != 0;

@@ -1091,6 +1091,24 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
         // (16-byte window copies measured slower here: cfg2 49.8 vs 47.3 us)
         for (int t = lane; t < w; t += 32) cp_async8(dd + t, ds + (vmp ? lo + t : ((lo + t) & (hf - 1))));
     }
+    if (p.pfd > 0) {
+        // L2 prefetch of the windows of the warp with this index in the CTA pfd
+        // linear block indices ahead (this warp's windows shifted by whole chunks)
+        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + p.pfd;
+        if (lin < (long long)gridDim.x * gridDim.y && lane <= p.top - p.bot) {
+            const long long v2 = lin / gridDim.x;
+            const long long dc = ((long long)(lin % gridDim.x) - (long long)blockIdx.x) * (blockDim.x >> 5);
+            const double* xb2 = p.x + p.lx.vbase(p.xv0 + v2);
+            const int L = p.bot + lane - 1;  // lane 0: the coarse window of level bot; lane i: details d_{bot+i-1}
+            const int LL = lane == 0 ? p.bot : L, sh = p.cb - (p.top - LL);
+            if (sh >= 0) {
+                const long long lo2 = wlo[LL] + dc * (1ll << sh);
+                const int w = whi[LL] - wlo[LL];
+                const double* b0 = lane == 0 ? (p.src_is_x ? xb2 : p.src + v2 * p.src_vs) : xb2 + (1ll << LL);
+                l2_prefetch_span(b0 + lo2, w, b0, b0 + (1ll << LL));
+            }
+        }
+    }
     cp_async_wait_all();
     __syncwarp();
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {
@@ -1241,6 +1259,15 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
         if (vmp) warp_copy_span(X, src + lo, w, lane);  // 16-byte copies when the phases agree
         else
             for (int t = lane; t < w; t += 32) cp_async8(X + t, src + ((lo + t) & (n - 1)));
+    }
+    if (p.pfd > 0 && lane == 0) {  // L2 prefetch of the window of this warp index in the CTA pfd blocks ahead
+        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + p.pfd;
+        if (lin < (long long)gridDim.x * gridDim.y) {
+            const long long v2 = lin / gridDim.x;
+            const long long dc = ((long long)(lin % gridDim.x) - (long long)blockIdx.x) * nw;
+            const double* s2 = p.src + v2 * p.src_vs;
+            l2_prefetch_span(s2 + xlo[p.top] + dc * (1ll << p.cb), xhi[p.top] - xlo[p.top], s2, s2 + (1ll << p.top));
+        }
     }
     cp_async_wait_all();
     __syncwarp();
@@ -2192,30 +2219,28 @@ __global__ void __launch_bounds__(NT, 2) k_large_adj2(LargeArgs p) {
 #pragma unroll
             for (int nl = 0; nl < B; ++nl) y[nl] = 0.0;
         }
-        // L2 prefetch of the first sequency block of the CTA that will take this
-        // one's place (linear block index + pfd, CTAs dispatch in order): 32
-        // contiguous runs of R2 doubles per sub-tile, one per lane
-        if (it == 0 && p.pfd > 0 && tid < 32) {
-            const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + p.pfd;
-            if (lin < (long long)gridDim.x * gridDim.y) {
-                const int bx = (int)(lin % gridDim.x);
-                const long long vy = lin / gridDim.x;
-                const double* ibn = p.in + p.lin.vbase(p.v0 + vy);
-                const unsigned x = brev_bits((unsigned)tid, kLogB);
-                const long long gx = (long long)gray_inv(x);
-                for (int g2 = 0; g2 < NG; ++g2) {
-                    const unsigned gl0 = (unsigned)(bx * NG + g2) << kh;
-                    unsigned rl0 = gray_inv(gl0) & (unsigned)(A - 1);
-                    if (__popc(x) & 1) rl0 ^= (unsigned)(A - 1);
-                    rl0 &= ~(unsigned)(R2 - 1);
-                    l2_prefetch(ibn + gx * A + rl0, (unsigned)(R2 * 8));
-                    for (int s2 = 1; s2 < p.pfs; ++s2)  // later blocks: odd ones mirrored (index ^ (M - 1))
-                        l2_prefetch(ibn + (long long)s2 * M + (((gx * A + rl0) ^ ((s2 & 1) ? (long long)(M - 1) : 0ll)) & ~(long long)(R2 - 1)),
-                                    (unsigned)(R2 * 8));
-                }
+        // L2 prefetches (warp 0, one 2^kh-double run per lane and sub-tile) of this
+        // CTA's later blocks, p.pfs blocks ahead of the row stage's register loads
+        auto pf_block = [&](const double* ibn, int bx, int s2) {
+            const unsigned x = brev_bits((unsigned)tid, kLogB);
+            const long long gx = (long long)gray_inv(x);
+            for (int g2 = 0; g2 < NG; ++g2) {
+                const unsigned gl0 = (unsigned)(bx * NG + g2) << kh;
+                unsigned rl0 = gray_inv(gl0) & (unsigned)(A - 1);
+                if (__popc(x) & 1) rl0 ^= (unsigned)(A - 1);
+                long long idx = gx * A + rl0;
+                if (s2 & 1) idx ^= (long long)(M - 1);  // odd blocks are mirrored
+                // (an 8-byte aligned input: the 16-byte granules from the one holding the run's start)
+                l2_prefetch(reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(
+                                ibn + (long long)s2 * M + (idx & ~(long long)(R2 - 1))) & ~uintptr_t(15)),
+                            (unsigned)(R2 * 8));
             }
+        };
+        if (it == 0 && tid < 32) {
+            for (int s2 = 1; s2 <= p.pfs && s2 < S; ++s2) pf_block(ib, (int)blockIdx.x, s2);
         }
         for (int s = 0; s < S; ++s) {
+            if (it == 0 && tid < 32 && p.pfs > 0 && s > 0 && s + p.pfs < S) pf_block(ib, (int)blockIdx.x, s + p.pfs);
             hadamard_reg<kLogB>(y);
             if (NU > 1) {  // per-warp partial sums, one slot per (CTA, iteration, warp)
                 constexpr int R = 2 * NP <= 16 ? 16 : 32;

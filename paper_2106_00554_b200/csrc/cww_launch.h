@@ -75,9 +75,9 @@ struct LargeArgs {
     // summed by launch_ana_fixup
     int fuse_ana;
     double* apart;
-    // L2 prefetch distance in CTAs (0: off): a CTA prefetches the first loads of
-    // the CTA pfd linear block indices ahead (the one that will replace it)
-    int pfd, pfd1, pfs;  // adjoint pass 2 / pass 1
+    // L2 prefetches: adjoint pass 1 prefetches the G block of the CTA pfd1 linear
+    // block indices ahead; adjoint pass 2 its own sequency blocks pfs ahead (0: off)
+    int pfd1, pfs;
 };
 
 struct WavArgs {
@@ -132,6 +132,7 @@ struct PyrArgs {
     double* cws;
     long long cws_vs;
     unsigned* cnt;
+    int pfd;  // L2 prefetch distance in CTAs (0: off)
 };
 
 cudaError_t launch_pyr(int nu, bool analysis, const PyrArgs& a, cudaStream_t st);
