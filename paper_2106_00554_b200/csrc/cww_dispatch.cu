@@ -337,7 +337,7 @@ cudaError_t launch_fwht(double* v, int bits, long long batch, int sequency, doub
                         cudaStream_t st) {
     if (bits <= 13) {
         long long smem = (1ll << bits) * 8;
-        cudaFuncSetAttribute(k_fwht_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        opt_in_smem(reinterpret_cast<const void*>(k_fwht_small));
         k_fwht_small<<<(unsigned)batch, 256, smem, st>>>(v, bits, sequency);
         return cudaGetLastError();
     }

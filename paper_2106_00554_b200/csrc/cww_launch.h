@@ -5,6 +5,8 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <set>
 #include <utility>
 #include <vector>
 
@@ -39,6 +41,27 @@ struct SmallArgs {
     int in_block;  // 1: a CTA's V input vectors are one contiguous block; 2: an
                    // interleaved [M][V] block (column panel); 0: generic layout
 };
+
+// Opts kernel k in to the device's full dynamic shared memory (227 KB minus the
+// kernel's static part), once per (kernel, device).  The attribute is per
+// kernel and process-wide: setting it to each launch's own footprint would
+// race between host threads launching the same kernel with different sizes.
+inline cudaError_t opt_in_smem(const void* k) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({k, dev})) return cudaSuccess;
+    cudaFuncAttributes fa{};
+    if (cudaError_t e = cudaFuncGetAttributes(&fa, k); e != cudaSuccess) return e;
+    if (cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024 - (int)fa.sharedSizeBytes);
+        e != cudaSuccess)
+        return e;
+    done.insert({k, dev});
+    return cudaSuccess;
+}
 
 struct LargeArgs {
     const double* tab;

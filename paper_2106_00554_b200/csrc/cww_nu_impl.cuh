@@ -31,11 +31,11 @@ cudaError_t small_t(const SmallArgs& a, bool adj, cudaStream_t st) {
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         if (adj) {
             auto k = k_small_adj<CWW_NU, LOGB, kSmallNT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            opt_in_smem(reinterpret_cast<const void*>(k));
             if (cudaError_t e = launch_k(k, grid, kSmallNT, smem, st, a); e != cudaSuccess) return e;
         } else {
             auto k = k_small_fwd<CWW_NU, LOGB, kSmallNT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            opt_in_smem(reinterpret_cast<const void*>(k));
             if (cudaError_t e = launch_k(k, grid, kSmallNT, smem, st, a); e != cudaSuccess) return e;
         }
         return cudaGetLastError();
@@ -72,11 +72,11 @@ cudaError_t CWW_FN(launch_wv_nu)(const SmallArgs& a, bool adj, cudaStream_t st) 
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     if (adj) {
         auto k = k_wv_adj<CWW_NU>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        opt_in_smem(reinterpret_cast<const void*>(k));
         if (cudaError_t e = launch_k(k, grid, kWvNT, smem, st, a); e != cudaSuccess) return e;
     } else {
         auto k = k_wv_fwd<CWW_NU>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        opt_in_smem(reinterpret_cast<const void*>(k));
         if (cudaError_t e = launch_k(k, grid, kWvNT, smem, st, a); e != cudaSuccess) return e;
     }
     return cudaGetLastError();
@@ -97,26 +97,26 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
             if (a.fuse_top)  // + mbarrier + the coarse / detail windows of one piece
                 s1 += (2 + 4ll * fuse_window(R1 * (1 << kLogB) / 2 / kFusePieces, CWW_NU)) * 8;  // 2 buffers
             auto k = k_large_fwd1<CWW_NU, CWW_NT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+            opt_in_smem(reinterpret_cast<const void*>(k));
             if (cudaError_t e = launch_k(k, g1, CWW_NT, s1, st, a); e != cudaSuccess) return e;
             break;
         }
         case 1: {
             auto k = k_large_fwd2<CWW_NU, CWW_NT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+            opt_in_smem(reinterpret_cast<const void*>(k));
             if (cudaError_t e = launch_k(k, g2, CWW_NT, s2, st, a); e != cudaSuccess) return e;
             break;
         }
         case 2: {
             auto k = k_large_adj2<CWW_NU, CWW_NT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2a);
+            opt_in_smem(reinterpret_cast<const void*>(k));
             if (cudaError_t e = launch_k(k, g2, CWW_NT, s2a, st, a); e != cudaSuccess) return e;
             break;
         }
         case 5: {  // persistent fused forward pass 1: as many CTAs as fit on the device
             s1 += (2 + 4ll * fuse_window(R1 * (1 << kLogB) / 2 / kFusePieces, CWW_NU)) * 8;
             auto k = k_large_fwd1_fz<CWW_NU, CWW_NT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+            opt_in_smem(reinterpret_cast<const void*>(k));
             int dev = 0, nsm = 0, per = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -136,7 +136,7 @@ cudaError_t CWW_FN(launch_large_nu)(int which, const LargeArgs& a, cudaStream_t 
         }
         default: {
             auto k = k_large_adj1<CWW_NU, CWW_NT>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1a);
+            opt_in_smem(reinterpret_cast<const void*>(k));
             if (cudaError_t e = launch_k(k, g1, CWW_NT, s1a, st, a); e != cudaSuccess) return e;
             break;
         }
@@ -155,13 +155,13 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
         const long long smem = (FS + nb) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_dwt_wpyr<CWW_NU>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        opt_in_smem(reinterpret_cast<const void*>(k));
         if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     } else {
         const long long smem = (FS + (long long)nw * (48ll + a.wmax + a.wmax2 + a.dsum)) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_idwt_wpyr<CWW_NU>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        opt_in_smem(reinterpret_cast<const void*>(k));
         if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     }
     return cudaGetLastError();
@@ -172,7 +172,7 @@ cudaError_t CWW_FN(launch_normal_rows_nu)(const NormArgs& a, cudaStream_t st) {
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     const unsigned grid = (unsigned)((a.nvec + a.V - 1) / a.V);
     auto k = k_normal_rows<CWW_NU, 256>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    opt_in_smem(reinterpret_cast<const void*>(k));
     if (cudaError_t e = launch_k(k, grid, 256, smem, st, a); e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -184,7 +184,7 @@ cudaError_t normal_reg_t(const NormArgs& a, cudaStream_t st) {
     const long long smem = (FiltSmem<CWW_NU>::SIZE + 2ll * a.E * (4 * CWW_NU - 3) +
                             3ll * ((1 << J) + (1 << J) / 32) + 3ll * (1 << RLOG)) * 8;
     auto k = k_normal_rows_reg<CWW_NU, J, RNT>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    opt_in_smem(reinterpret_cast<const void*>(k));
     if (cudaError_t e = launch_k(k, dim3((unsigned)a.nvec), dim3(RNT), (size_t)smem, st, a); e != cudaSuccess)
         return e;
     return cudaGetLastError();
@@ -207,7 +207,7 @@ cudaError_t CWW_FN(launch_wav_nu)(const WavArgs& w, cudaStream_t st) {
     if (w.kind == 0) {
         long long smem = (FiltSmem<CWW_NU>::SIZE + 3 * (1ll << w.lev)) * 8;
         auto k = k_wav_coarse<CWW_NU>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        opt_in_smem(reinterpret_cast<const void*>(k));
         if (cudaError_t e = launch_k(k, dim3((unsigned)w.nvec), dim3(nt), (size_t)smem, st, w.tab, w.t, w.src, w.ls,
                                      w.sv0, w.src_vs, w.dst, w.ld, w.dv0, w.dst_vs, w.r0, w.lev, w.inverse, w.vmp);
             e != cudaSuccess)
