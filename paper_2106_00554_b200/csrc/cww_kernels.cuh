@@ -1944,11 +1944,16 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_fwd1(LargeArgs p)
     cp_async_wait_all();
     __syncthreads();
     if (H > 0) {  // inner halos: copies of the neighbouring rows' own columns
-        for (int f = tid; f < (R1 - 1) * 2 * H; f += NT) {
-            const int K = f / (2 * H), c = f % (2 * H);  // boundary between logical rows K and K + 1
-            const int p0 = (int)brev_bits((unsigned)K, kl) * RS, p1 = (int)brev_bits((unsigned)(K + 1), kl) * RS;
-            if (c < H) T[p0 + B + H + c] = T[p1 + H + c];  // right halo of K <- own column c of K + 1
-            else T[p1 + (c - H)] = T[p0 + B + (c - H)];    // left halo of K + 1 <- own column B - H + c' of K
+        // (thread = (physical row, halo column): consecutive lanes walk consecutive
+        // physical rows, whose 36-double stride spreads them over the banks)
+        for (int f = tid; f < R1 * 2 * H; f += NT) {
+            const int ph = f / (2 * H), c = f % (2 * H);
+            const int K = (int)brev_bits((unsigned)ph, kl);  // this row's halos from its neighbours
+            if (c < H) {  // right halo: the next row's first columns
+                if (K + 1 < R1) T[ph * RS + B + H + c] = T[(int)brev_bits((unsigned)(K + 1), kl) * RS + H + c];
+            } else {      // left halo: the previous row's last columns
+                if (K > 0) T[ph * RS + (c - H)] = T[(int)brev_bits((unsigned)(K - 1), kl) * RS + B + (c - H)];
+            }
         }
         __syncthreads();
     }
@@ -2093,11 +2098,16 @@ __global__ void __launch_bounds__(NT, 2) k_large_fwd1_fz(LargeArgs p) {
         }
         __syncthreads();
         if (H > 0) {  // inner halos: copies of the neighbouring rows' own columns
-            for (int f = tid; f < (R1 - 1) * 2 * H; f += NT) {
-                const int K = f / (2 * H), c = f % (2 * H);
-                const int p0 = (int)brev_bits((unsigned)K, kl) * RS, p1 = (int)brev_bits((unsigned)(K + 1), kl) * RS;
-                if (c < H) T[p0 + B + H + c] = T[p1 + H + c];
-                else T[p1 + (c - H)] = T[p0 + B + (c - H)];
+            // (thread = (physical row, halo column): consecutive lanes walk consecutive
+            // physical rows, whose 36-double stride spreads them over the banks)
+            for (int f = tid; f < R1 * 2 * H; f += NT) {
+                const int ph = f / (2 * H), c = f % (2 * H);
+                const int K = (int)brev_bits((unsigned)ph, kl);  // this row's halos from its neighbours
+                if (c < H) {  // right halo: the next row's first columns
+                    if (K + 1 < R1) T[ph * RS + B + H + c] = T[(int)brev_bits((unsigned)(K + 1), kl) * RS + H + c];
+                } else {      // left halo: the previous row's last columns
+                    if (K > 0) T[ph * RS + (c - H)] = T[(int)brev_bits((unsigned)(K - 1), kl) * RS + B + (c - H)];
+                }
             }
             __syncthreads();
         }
@@ -2400,15 +2410,18 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
         // row's halo: (row, halo column) per thread, in place (the halo columns
         // themselves are never written)
         if (NU > 1) {
+            // (consecutive lanes walk consecutive PHYSICAL rows: the row stride of 36
+            // doubles spreads them over the banks; logical order would not)
             for (int idx = tid; idx < R1 * 2 * H; idx += NT) {
-                const int r = idx / (2 * H), hh = idx - r * 2 * H;
+                const int ph = idx / (2 * H), hh = idx - ph * 2 * H;
+                const int r = (int)brev_bits((unsigned)ph, kl);
                 const bool left = hh < H;
                 const int c = left ? hh : B - 2 * H + hh;  // xi column
                 const int rn = left ? r - 1 : r + 1;
                 const double add = (rn >= 0 && rn < R1)
                                        ? T[(int)brev_bits((unsigned)rn, kl) * RS + (left ? B + H + c : c - (B - H))]
                                        : nb[hh];
-                T[(int)brev_bits((unsigned)r, kl) * RS + H + c] += add;
+                T[ph * RS + H + c] += add;
             }
         }
     } else if (!has_edge && (xw || fana)) {  // interior chunks: four rows in flight per warp (independent chains)
