@@ -27,7 +27,10 @@
 namespace cww {
 
 constexpr int kWvJ = 10;                     // M = 1024
-constexpr int kWvXS = 1092;  // per-warp region: 1024 + 64 pads (+4); = 4 (mod 16): the 8 regions' banks interleave
+// per-warp region: 1024 + 64 pads (+2); = 2 (mod 16), so that the cooperative
+// staging's half-warps (8 regions x 2 consecutive doubles) cover 16 distinct
+// 8-byte banks (= 4 (mod 16) measured 2-way conflicts there: cfg4 1.439 -> 1.413 ms)
+constexpr int kWvXS = 1090;
 constexpr int kWvNT = 256;                   // 8 warps = 8 vectors per CTA
 constexpr int kWvV = kWvNT / 32;
 #ifndef WV_MINB
