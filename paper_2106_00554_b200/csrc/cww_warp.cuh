@@ -43,6 +43,12 @@ __device__ __forceinline__ int wv_pad(int p) { return p + (p >> 5); }
 // lane stride up to 16 (the register level's 16-row segments per lane)
 __device__ __forceinline__ int p16(int k) { return k + (k >> 4); }
 
+// staging index of sequency position q: a half-warp (lanes = rows 0..15 or 16..31)
+// touches positions 2g + (g & 1) + const, g = 0..15, whose 8-byte banks collide
+// pairwise (g, g + 8); flipping bit 0 where bit 4 is set separates them, and
+// keeps every aligned pair of positions together (the cooperative copies)
+__device__ __forceinline__ int wv_sq(int q) { return q ^ ((q >> 4) & 1); }
+
 // element REL (compile time, may be < 0 or >= P) relative to this lane's first
 // sample of a level distributed P per lane (wrapping across lanes 31 <-> 0)
 template <int P, int REL>
@@ -92,6 +98,7 @@ __device__ __forceinline__ void lane_hadamard(double (&r)[N], int lane) {
 // k = tid / 8 + 32 i, so its addresses step linearly when the layout's element
 // index is linear (esh >= 62: image columns, column panels).  Callers bracket
 // with __syncthreads.
+template <bool SQ = false>
 __device__ __forceinline__ void wv_coop_load(double* XB, const double* in, const Layout& L, long long v0, int nv,
                                              long long off, int cnt, int tid) {
     constexpr int U = 8;
@@ -106,13 +113,13 @@ __device__ __forceinline__ void wv_coop_load(double* XB, const double* in, const
 #pragma unroll
             for (int u = 0; u < U; ++u) r[u] = __ldg(src + (i0 + u) * st);
 #pragma unroll
-            for (int u = 0; u < U; ++u) xb[k0 + 32 * (i0 + u)] = r[u];
+            for (int u = 0; u < U; ++u) xb[SQ ? wv_sq(k0 + 32 * (i0 + u)) : k0 + 32 * (i0 + u)] = r[u];
         }
         return;
     }
-    for (int k = k0; k < cnt; k += 32) xb[k] = __ldg(in + L.at(v0 + v, off + k));
+    for (int k = k0; k < cnt; k += 32) xb[SQ ? wv_sq(k) : k] = __ldg(in + L.at(v0 + v, off + k));
 }
-template <bool PAD = false>
+template <bool PAD = false, bool SQ = false>
 __device__ __forceinline__ void wv_coop_store(const double* XB, double* out, const Layout& L, long long v0, int nv,
                                               long long off, int cnt, int tid) {
     const int v = tid & (kWvV - 1), k0 = tid / kWvV;
@@ -122,10 +129,10 @@ __device__ __forceinline__ void wv_coop_store(const double* XB, double* out, con
         double* dst = out + L.vbase(v0 + v) + (off + k0) * L.es;
         const long long st = 32 * L.es;
 #pragma unroll 8
-        for (int i = 0; i < cnt / 32; ++i) dst[i * st] = xb[PAD ? p16(k0 + 32 * i) : k0 + 32 * i];
+        for (int i = 0; i < cnt / 32; ++i) dst[i * st] = xb[PAD ? p16(k0 + 32 * i) : (SQ ? wv_sq(k0 + 32 * i) : k0 + 32 * i)];
         return;
     }
-    for (int k = k0; k < cnt; k += 32) out[L.at(v0 + v, off + k)] = xb[PAD ? p16(k) : k];
+    for (int k = k0; k < cnt; k += 32) out[L.at(v0 + v, off + k)] = xb[PAD ? p16(k) : (SQ ? wv_sq(k) : k)];
 }
 // one vector's elements [off, off + cnt) by its own warp (lanes over k):
 // contiguous layouts as 16-byte loads, others element-wise
@@ -371,12 +378,12 @@ __global__ void __launch_bounds__(kWvNT, WV_MINB) k_wv_fwd(SmallArgs p) {
                 row_store<kLogB>(ob + p.lout.eoff((long long)s * M), p.lout, a, rw, z);
             } else {  // block s staged in the region (sequency positions), stored by the CTA
 #pragma unroll
-                for (int nl = 0; nl < B; ++nl) X[gray_inv_hi(nl, kLogB, a) ^ rw] = z[nl];
+                for (int nl = 0; nl < B; ++nl) X[wv_sq((int)(gray_inv_hi(nl, kLogB, a) ^ rw))] = z[nl];
             }
         }
         if (ovf) {
             __syncthreads();
-            wv_coop_store(XB, p.out, p.lout, v0, nv, (long long)s * M, M, tid);
+            wv_coop_store<false, true>(XB, p.out, p.lout, v0, nv, (long long)s * M, M, tid);
             __syncthreads();
         }
     }
@@ -419,14 +426,14 @@ __global__ void __launch_bounds__(kWvNT, WV_MINB) k_wv_adj(SmallArgs p) {
         const unsigned rw = gray_inv((unsigned)wlo) ^ ((s & 1) ? (unsigned)(M - 1) : 0u);
         if (ivf) {  // block s of the CTA's vectors through the regions
             if (s > 0) __syncthreads();
-            wv_coop_load(XB, p.in, p.lin, v0, nv, (long long)s * M, M, tid);
+            wv_coop_load<true>(XB, p.in, p.lin, v0, nv, (long long)s * M, M, tid);
             __syncthreads();
         }
         if (!act) continue;
         double y[B];
         if (ivf) {
 #pragma unroll
-            for (int nl = 0; nl < B; ++nl) y[nl] = X[gray_inv_hi(nl, kLogB, a) ^ rw];
+            for (int nl = 0; nl < B; ++nl) y[nl] = X[wv_sq((int)(gray_inv_hi(nl, kLogB, a) ^ rw))];
         } else {
             row_load<kLogB>(ib + p.lin.eoff((long long)s * M), p.lin, a, rw, true, y);
         }
