@@ -1685,6 +1685,8 @@ __global__ void __launch_bounds__(RNT, 2) k_normal_rows_reg(NormArgs p) {
 #pragma unroll
     for (int r = 0; r < M / RNT; ++r) cp_async8(X + pidx(tid + r * RNT), xg + (tid + r * RNT) * es);
     cp_async8(XL + tid, xg + tid * es);  // RNT == 2^RLOG
+    if (tid == 0 && p.pfd > 0 && p.es <= 0 && v + p.pfd < p.nvec)  // a later CTA's row into L2
+        l2_prefetch_span(p.in + (v + p.pfd) * p.in_vs, M, p.in, p.in + p.nvec * p.in_vs);
     cp_async_wait_all();
     __syncthreads();
     const FiltSmem<NU> F{filt};

@@ -179,6 +179,7 @@ struct NormArgs {
     // its elements are es apart (columns of row-major images: vpi = M, ivs = M^2,
     // vs = 1, es = M); es = 0 means the contiguous layout above
     long long vpi, ivs, es;
+    int pfd;  // register kernel, contiguous rows: L2 prefetch of the row pfd CTAs ahead (0: off)
 };
 cudaError_t launch_normal_rows(int nu, const NormArgs& a, cudaStream_t st);
 // fp32 I/O conversions (grid-stride)
