@@ -105,6 +105,41 @@ def test_concurrent_host_threads(cuda):
         assert torch.equal(a, b)
 
 
+def test_concurrent_threads_different_sizes(cuda):
+    """Several host threads driving operators of different sizes through the
+    same kernels at once (different shared-memory footprints per launch): a
+    per-launch cudaFuncSetAttribute raced here ("invalid argument")."""
+    import torch
+    cw = _cw()
+    ops = [_op(cw, 3, 1, j, 2, 1, 4) for j in (13, 14, 15, 16)]
+    g = torch.Generator(device="cuda").manual_seed(12)
+    xs = [torch.randn((3, A.cols()), dtype=torch.float64, device="cuda", generator=g) for A in ops]
+    want = [A.adjoint(A.forward(x)) for A, x in zip(ops, xs)]
+    torch.cuda.synchronize()
+    got = [None] * len(ops)
+    errs = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(6):
+                    got[i] = ops[i].adjoint(ops[i].forward(xs[i]))
+            s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    for _ in range(3):
+        th = [threading.Thread(target=work, args=(i,)) for i in range(len(ops))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errs, errs
+        for a, b in zip(got, want):
+            assert torch.equal(a, b)
+
+
 def test_too_large_is_rejected_cleanly(cuda):
     cw = _cw()
     with pytest.raises(cw.CwwError) as e:

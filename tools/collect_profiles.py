@@ -16,7 +16,8 @@ SRC = os.path.join(REPO, "gpurun_out", "prof")
 DST = os.path.join(REPO, "profiles")
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r02"
 
-SHORT = {"k_large_adj2": "large_adj2", "k_large_fwd2": "large_fwd2", "k_dwt_wpyr": "dwt_pyr", "k_wv_adj": "wv_adj",
+SHORT = {"k_large_adj2": "large_adj2", "k_large_fwd2": "large_fwd2", "k_large_adj1": "large_adj1",
+         "k_large_fwd1_fz": "large_fwd1", "k_dwt_wpyr": "dwt_pyr", "k_wv_adj": "wv_adj",
          "k_wv_fwd": "wv_fwd", "k_normal_rows_reg": "normal_rows", "k_small_fwd": "small_fwd",
          "k_small_adj": "small_adj"}
 
@@ -88,11 +89,12 @@ def main():
         out.setdefault(c, []).append({"kernel": short, "bytes": int(sum(per_launch) / len(per_launch)), "launch": note})
     json.dump(out, open(os.path.join(DST, f"{TAG}_traffic.json"), "w"), indent=1)
     # ncu --set full summary of the strided passes
-    rep = os.path.join(SRC, "cfg3_fwd2_adj2.ncu-rep")
-    if os.path.exists(rep):
-        txt = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_summary.py"), rep], capture_output=True,
-                             text=True).stdout
-        open(os.path.join(DST, f"{TAG}_ncu_cfg3_fwd2_adj2.txt"), "w").write(txt)
+    for name in ("cfg3_fwd2_adj2", "cfg3_pass1_pyramids", "cfg4_warp_kernels", "cfg5_normal_rows"):
+        rep = os.path.join(SRC, name + ".ncu-rep")
+        if os.path.exists(rep):
+            txt = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_summary.py"), rep],
+                                 capture_output=True, text=True).stdout
+            open(os.path.join(DST, f"{TAG}_ncu_{name}.txt"), "w").write(txt)
     print(open(os.path.join(DST, f"{TAG}_launches_cfg3_shares.csv")).read())
 
 

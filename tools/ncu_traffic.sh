@@ -18,7 +18,7 @@ for _ in range(2):
 torch.cuda.synchronize()
 PY
 # spec = config:kernel[:launches per call] -- the second call's launches are captured
-for spec in "1:k_wv_fwd" "1:k_wv_adj" "2:large_adj2" "2:k_dwt_wpyr:2" "3:large_adj2" "3:large_fwd2" "4:k_wv_adj:2" "4:k_wv_fwd:2" "5:normal_rows"; do
+for spec in "1:k_wv_fwd" "1:k_wv_adj" "2:large_adj2" "2:k_dwt_wpyr:2" "3:large_adj2" "3:large_fwd2" "3:large_adj1" "3:large_fwd1_fz" "4:k_wv_adj:2" "4:k_wv_fwd:2" "5:normal_rows"; do
   c=$(echo $spec | cut -d: -f1); k=$(echo $spec | cut -d: -f2); n=$(echo $spec | cut -d: -f3); n=${n:-1}
   python /tmp/dom.py $c
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
