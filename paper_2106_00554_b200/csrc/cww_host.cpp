@@ -953,8 +953,9 @@ cww_status analysis_chain(const cww_op* op, double* w0, double* w1, double* out,
         y.bot = bot;
         y.cb = cb;
         y.tail = tail ? 1 : 0;
-        y.wmax = cww::pyr_wmax_ana(nu, T, bot, cb, op->vmp != 0, &y.wmax2) + 1;  // +1: 16-byte phase shift
+        y.wmax = cww::pyr_wmax_ana(nu, T, bot, cb, op->vmp != 0, &y.wmax2) + 2;  // 16-byte phase shift + bulk-copy rounding
         y.wmax2 += 1;
+        y.wmax += (y.wmax + y.wmax2) & 1;  // even per-warp stride: every warp's slots start 16-byte aligned
         y.src = src;
         y.src_vs = M;
         y.y = out;

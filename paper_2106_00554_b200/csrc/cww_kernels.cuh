@@ -1217,8 +1217,9 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    const int per = 64 + p.wmax + p.wmax2;  // slot 0: windows of steps top, top-2, ...; slot 1: the others
+    const int per = 64 + p.wmax + p.wmax2 + 2;  // slot 0: windows of steps top, top-2, ...; slot 1: the others; mbarrier
     double* wb = sm + FS + wid * per;
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(wb + 64 + p.wmax + p.wmax2);  // this warp's window landed
     int* rlo = reinterpret_cast<int*>(wb);
     int* rhi = rlo + 32;
     int* xlo = rlo + 64;
@@ -1230,6 +1231,7 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
     const int lnc = p.top - p.cb;
     for (int i = tid; i < FS; i += blockDim.x) filt[i] = p.tab[p.t.o_h + i];
     if (lane == 0) {
+        mbar_init(wbar, 1);
         Win r{c << (p.bot - lnc), (c + 1) << (p.bot - lnc)};
         for (int s = p.bot + 1; s <= p.top; ++s) {
             const Win w = ana_need(NU, 1 << s, r, vmp);
@@ -1252,13 +1254,35 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
     };
     double* const S0 = X;  // slot bases (unshifted)
     double* const S1 = Y;
+    bool bulk = false;
     {
         const double* src = p.src + v * p.src_vs;
         const int lo = xlo[p.top], w = xhi[p.top] - lo, n = 1 << p.top;
         X = pair_al(S0, lo);
-        if (vmp) warp_copy_span(X, src + lo, w, lane);  // 16-byte copies when the phases agree
-        else
+        // the window as ONE bulk copy (TMA engine: full 128-byte shared-memory
+        // wavefronts, where cp.async writes land sector by sector) when source and
+        // slot share their 16-byte phase (odd nu): widened to 16-byte bounds --
+        // one sample before (slot slack) and / or after (n is even) the window
+        const double* s0 = src + lo;
+        double* d0 = X;
+        int cnt = w;
+        if (reinterpret_cast<uintptr_t>(s0) & 15) {
+            --s0;
+            --d0;
+            ++cnt;
+        }
+        cnt = (cnt + 1) & ~1;
+        bulk = vmp && (reinterpret_cast<uintptr_t>(d0) & 15) == 0 && d0 >= S0;
+        if (bulk) {
+            if (lane == 0) {
+                mbar_arrive_expect(wbar, (unsigned)(cnt * 8));
+                bulk_g2s(d0, s0, (unsigned)(cnt * 8), wbar);
+            }
+        } else if (vmp) {
+            warp_copy_span(X, src + lo, w, lane);  // 16-byte copies when the phases agree
+        } else {
             for (int t = lane; t < w; t += 32) cp_async8(X + t, src + ((lo + t) & (n - 1)));
+        }
     }
     if (p.pfd > 0 && lane == 0) {  // L2 prefetch of the window of this warp index in the CTA pfd blocks ahead
         const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + p.pfd;
@@ -1269,7 +1293,8 @@ __global__ void __launch_bounds__(256) k_dwt_wpyr(PyrArgs p) {
             l2_prefetch_span(s2 + xlo[p.top] + dc * (1ll << p.cb), xhi[p.top] - xlo[p.top], s2, s2 + (1ll << p.top));
         }
     }
-    cp_async_wait_all();
+    if (bulk) mbar_wait(wbar, 0);
+    else cp_async_wait_all();
     __syncwarp();
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);

@@ -150,7 +150,7 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
     const int nw = nchunk < 8 ? nchunk : 8;
     const dim3 grid((unsigned)(nchunk / nw), (unsigned)a.nvec);
     if (analysis) {
-        long long nb = (long long)nw * (64ll + a.wmax + a.wmax2);
+        long long nb = (long long)nw * (64ll + a.wmax + a.wmax2 + 2);
         if (a.tail && nb < (2ll << a.bot) + 2) nb = (2ll << a.bot) + 2;  // + 16-byte phase slack
         const long long smem = (FS + nb) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
