@@ -906,6 +906,11 @@ cww_status synth_chain(const cww_op* op, const double* in, Layout lin, long long
         y.bot = bot;
         y.cb = std::min(top, kWpyrLog);
         y.wmax = cww::pyr_wmax_syn(nu, y.top, y.bot, y.cb, op->vmp != 0, &y.dsum, &y.wmax2);
+        // even slot sizes (16-byte aligned slot bases) with room for the bulk copies'
+        // rounding to 16-byte bounds on both sides of every window
+        y.wmax = (y.wmax + 3) & ~1;
+        y.wmax2 = (y.wmax2 + 3) & ~1;
+        y.dsum = (y.dsum + 2 * (y.top - y.bot) + 1) & ~1;
         y.x = in;
         y.lx = lin;
         y.src_is_x = src ? 0 : 1;

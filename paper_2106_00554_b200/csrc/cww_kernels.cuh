@@ -1055,10 +1055,10 @@ __device__ __forceinline__ void warp_syn_windows(const PyrArgs& p, double* wb, i
             if (f.hi - f.lo > (((p.top - lev) & 1) ? p.wmax2 : p.wmax)) __trap();  // slot size
         }
     }
-    int off = 0;
+    int off = 0;  // even offsets, room for the bulk copies' 16-byte rounding on both sides
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {
         doff[lev] = off;
-        off += whi[lev - 1] - wlo[lev - 1];
+        off += (whi[lev - 1] - wlo[lev - 1] + 2) & ~1;
     }
     if (off > p.dsum) __trap();
 }
@@ -1080,16 +1080,37 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
     double* D = P + p.wmax + p.wmax2;
     const double* xb = p.x + p.lx.vbase(p.xv0 + v);
     const double* cs = p.src_is_x ? xb : p.src + v * p.src_vs;
-    {
-        const int lo = wlo[p.bot], w = whi[p.bot] - lo, hb = 1 << p.bot;
-        for (int t = lane; t < w; t += 32) cp_async8(P + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
-    }
-    for (int lev = p.bot + 1; lev <= p.top; ++lev) {  // details of level lev (half = 2^(lev-1))
-        const int lo = wlo[lev - 1], w = whi[lev - 1] - lo, hf = 1 << (lev - 1);
-        const double* ds = xb + hf;
-        double* dd = D + doff[lev];
-        // (16-byte window copies measured slower here: cfg2 49.8 vs 47.3 us)
-        for (int t = lane; t < w; t += 32) cp_async8(dd + t, ds + (vmp ? lo + t : ((lo + t) & (hf - 1))));
+    // Every staged window keeps sample i at an address of i's 16-byte phase
+    // (slot bases are 16-byte aligned: + (lo & 1)), so that a window is ONE bulk
+    // copy (TMA engine: full 128-byte shared-memory wavefronts, where cp.async
+    // writes land sector by sector) from lo & ~1, an even number of samples --
+    // lane 0 the level-bot coarse window, lane i the details d_{bot+i-1}; all
+    // complete on this warp's mbarrier (count = number of windows)
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(D + p.dsum);
+    const bool bulk = vmp && ((reinterpret_cast<uintptr_t>(xb) | reinterpret_cast<uintptr_t>(cs)) & 15) == 0;
+    if (bulk) {
+        if (lane <= p.top - p.bot) {
+            const int L = lane == 0 ? p.bot : p.bot + lane - 1;
+            const int lo = wlo[L], w = whi[L] - lo;
+            const double* src = lane == 0 ? cs : xb + (1 << L);
+            double* dst = lane == 0 ? P : D + doff[L + 1];
+            const int cnt = ((lo & 1) + w + 1) & ~1;
+            mbar_arrive_expect(wbar, (unsigned)(cnt * 8));
+            bulk_g2s(dst, src + (lo & ~1), (unsigned)(cnt * 8), wbar);
+        }
+    } else {
+        {
+            const int lo = wlo[p.bot], w = whi[p.bot] - lo, hb = 1 << p.bot;
+            double* pp = P + (lo & 1);
+            for (int t = lane; t < w; t += 32) cp_async8(pp + t, cs + (vmp ? lo + t : ((lo + t) & (hb - 1))));
+        }
+        for (int lev = p.bot + 1; lev <= p.top; ++lev) {  // details of level lev (half = 2^(lev-1))
+            const int lo = wlo[lev - 1], w = whi[lev - 1] - lo, hf = 1 << (lev - 1);
+            const double* ds = xb + hf;
+            double* dd = D + doff[lev] + (lo & 1);
+            // (16-byte window copies measured slower here: cfg2 49.8 vs 47.3 us)
+            for (int t = lane; t < w; t += 32) cp_async8(dd + t, ds + (vmp ? lo + t : ((lo + t) & (hf - 1))));
+        }
     }
     if (p.pfd > 0) {
         // L2 prefetch of the windows of the warp with this index in the CTA pfd
@@ -1109,18 +1130,20 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
             }
         }
     }
-    cp_async_wait_all();
+    if (bulk) mbar_wait(wbar, 0);
+    else cp_async_wait_all();
     __syncwarp();
     for (int lev = p.bot + 1; lev <= p.top; ++lev) {
         const int n = 1 << lev;
         const int clo = wlo[lev - 1], lo = wlo[lev], hi = whi[lev];
-        const double* dw = D + doff[lev];
+        const double* dw = D + doff[lev] + (clo & 1);
+        const double* cwin = lev == p.bot + 1 ? P + (clo & 1) : P;  // (computed levels start at their slot's base)
         if (lev < p.top) {
             double* q = Q - lo;
-            idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { q[i] = val; });
+            idwt_window<NU>(F, tp, cwin, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { q[i] = val; });
             __syncwarp();
         } else {
-            idwt_window<NU>(F, tp, P, dw, clo, n, lo, hi, vmp, lane, 32, put);
+            idwt_window<NU>(F, tp, cwin, dw, clo, n, lo, hi, vmp, lane, 32, put);
         }
         double* t0 = P;
         P = Q;
@@ -1139,11 +1162,14 @@ __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
     constexpr int FS = FiltSmem<NU>::SIZE;
     double* filt = sm;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5, nt = blockDim.x;
-    double* wb = sm + FS + wid * (48 + p.wmax + p.wmax2 + p.dsum);
+    double* wb = sm + FS + wid * (48 + p.wmax + p.wmax2 + p.dsum + 2);  // + this warp's mbarrier
     const int c = blockIdx.x * nw + wid, v = blockIdx.y;
     const bool vmp = p.vmp != 0;
     for (int i = tid; i < FS; i += nt) filt[i] = p.tab[p.t.o_h + i];
-    if (lane == 0) warp_syn_windows<NU>(p, wb, c << p.cb, (c + 1) << p.cb, vmp);
+    if (lane == 0) {
+        warp_syn_windows<NU>(p, wb, c << p.cb, (c + 1) << p.cb, vmp);
+        mbar_init(reinterpret_cast<uint64_t*>(wb + 48 + p.wmax + p.wmax2 + p.dsum), (unsigned)(p.top - p.bot + 1));
+    }
     __syncthreads();  // filters (CTA-wide) and the windows
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);

@@ -158,7 +158,7 @@ cudaError_t CWW_FN(launch_pyr_nu)(bool analysis, const PyrArgs& a, cudaStream_t 
         opt_in_smem(reinterpret_cast<const void*>(k));
         if (cudaError_t e = launch_k(k, grid, 32 * nw, smem, st, a); e != cudaSuccess) return e;
     } else {
-        const long long smem = (FS + (long long)nw * (48ll + a.wmax + a.wmax2 + a.dsum)) * 8;
+        const long long smem = (FS + (long long)nw * (48ll + a.wmax + a.wmax2 + a.dsum + 2)) * 8;
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         auto k = k_idwt_wpyr<CWW_NU>;
         opt_in_smem(reinterpret_cast<const void*>(k));
