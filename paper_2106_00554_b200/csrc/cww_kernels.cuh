@@ -2457,11 +2457,12 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
     // into the tile's own columns [H, B + H) -- each (row, column) is read and
     // written by one thread only, and the halo columns stay intact
     double* xw = (p.xo_is_output || fana) ? nullptr : xo + base + lane;
-    if (!has_edge && fana) {
-        // fused analysis, interior chunks: the tile's columns [H, B + H) already
-        // hold xi except for the 2H columns per row that receive a neighbour
-        // row's halo: (row, halo column) per thread, in place (the halo columns
-        // themselves are never written)
+    if (!has_edge && (fana || xw)) {
+        // interior chunks: the tile's columns [H, B + H) already hold xi except for
+        // the 2H columns per row that receive a neighbour row's halo: (row, halo
+        // column) per thread, in place (the halo columns themselves are never
+        // written); then the fused analysis reads the tile, or a plain coalesced
+        // copy sends xi to the workspace
         if (NU > 1) {
             // (consecutive lanes walk consecutive PHYSICAL rows: the row stride of 36
             // doubles spreads them over the banks; logical order would not)
@@ -2477,17 +2478,11 @@ __global__ void __launch_bounds__(NT, CWW_CONTIG_MINB) k_large_adj1(LargeArgs p)
                 T[ph * RS + H + c] += add;
             }
         }
-    } else if (!has_edge && (xw || fana)) {  // interior chunks: four rows in flight per warp (independent chains)
+        if (!fana) {
+            __syncthreads();
 #pragma unroll 4
-        for (int rl = tid >> 5; rl < R1; rl += NT / 32) {
-            const int ph = (int)brev_bits((unsigned)rl, kl);
-            double val = T[ph * RS + lane + H];
-            if (hside != 0) {
-                const int rn = rl + hside;
-                val += (rn >= 0 && rn < R1) ? T[(int)brev_bits((unsigned)rn, kl) * RS + hcol] : nbv;
-            }
-            if (fana) T[ph * RS + lane + H] = val;
-            else xw[rl * B] = val;
+            for (int rl = tid >> 5; rl < R1; rl += NT / 32)
+                xw[rl * B] = T[(int)brev_bits((unsigned)rl, kl) * RS + lane + H];
         }
     } else {
         for (int rl = tid >> 5; rl < R1; rl += NT / 32) {  // logical local row K_lo, lane = column
