@@ -922,10 +922,12 @@ __global__ void __launch_bounds__(256) k_wav_coarse(const double* tab, Tables t,
 // Fine samples [lo, hi) of level n from windows cw = c[clo .. chi), dw =
 // d[clo .. chi) (same range; periodic: entries taken modulo n/2), written to
 // out[i - lo] (or, when put != nullptr, handed to put(i, value)).
-template <int NU, class Put>
+// put2(i, a, b), i even, stores the sample pair (i, i + 1) (one 16-byte store
+// where the destination keeps sample i at i's 16-byte phase).
+template <int NU, class Put, class Put2>
 __device__ __forceinline__ void idwt_window(const FiltSmem<NU>& F, const Taps<NU>& tp, const double* cw,
                                             const double* dw, int clo, int n, int lo, int hi, bool vmp,
-                                            int t0, int nthr, Put&& put) {
+                                            int t0, int nthr, Put&& put, Put2&& put2) {
     const double* cv = cw - clo;  // absolute (logical) coarse index
     const double* dv = dw - clo;
     if (vmp && n < 8 * NU) {
@@ -963,8 +965,7 @@ __device__ __forceinline__ void idwt_window(const FiltSmem<NU>& F, const Taps<NU
     for (int m = mlo + t0; m < mhi; m += nthr) {
         double o0, o1;
         pair(m, o0, o1);
-        put(2 * m, o0);
-        put(2 * m + 1, o1);
+        put2(2 * m, o0, o1);
     }
     // the rest of [lo, hi): partial pairs at the window ends and VMP edge samples
     const int nl = 2 * mlo - lo, nr = hi - 2 * mhi;
@@ -1066,9 +1067,9 @@ __device__ __forceinline__ void warp_syn_windows(const PyrArgs& p, double* wb, i
 // part 2 (the whole warp, after the windows are visible): prefetch the
 // level-bot coarse window and every level's detail window, synthesise up to
 // level p.top and hand the top samples to put(i, value).
-template <int NU, class Put>
+template <int NU, class Put, class Put2>
 __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU>& F, const Taps<NU>& tp,
-                                             double* wb, int v, int lane, bool vmp, Put&& put) {
+                                             double* wb, int v, int lane, bool vmp, Put&& put, Put2&& put2) {
     const int* wlo = reinterpret_cast<const int*>(wb);
     const int* whi = wlo + 32;
     const int* doff = wlo + 64;
@@ -1137,13 +1138,14 @@ __device__ __forceinline__ void warp_syn_run(const PyrArgs& p, const FiltSmem<NU
         const int n = 1 << lev;
         const int clo = wlo[lev - 1], lo = wlo[lev], hi = whi[lev];
         const double* dw = D + doff[lev] + (clo & 1);
-        const double* cwin = lev == p.bot + 1 ? P + (clo & 1) : P;  // (computed levels start at their slot's base)
+        const double* cwin = P + (clo & 1);
         if (lev < p.top) {
-            double* q = Q - lo;
-            idwt_window<NU>(F, tp, cwin, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { q[i] = val; });
+            double* q = Q + (lo & 1) - lo;  // the computed window at its samples' 16-byte phase too: pair stores
+            idwt_window<NU>(F, tp, cwin, dw, clo, n, lo, hi, vmp, lane, 32, [&](int i, double val) { q[i] = val; },
+                            [&](int i, double a, double b) { *reinterpret_cast<double2*>(q + i) = make_double2(a, b); });
             __syncwarp();
         } else {
-            idwt_window<NU>(F, tp, cwin, dw, clo, n, lo, hi, vmp, lane, 32, put);
+            idwt_window<NU>(F, tp, cwin, dw, clo, n, lo, hi, vmp, lane, 32, put, put2);
         }
         double* t0 = P;
         P = Q;
@@ -1174,7 +1176,17 @@ __global__ void __launch_bounds__(256) k_idwt_wpyr(PyrArgs p) {
     const FiltSmem<NU> F{filt};
     const Taps<NU> tp(F);
     double* ob = p.out + v * p.out_vs;
-    warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) { ob[i] = val; });
+    // (16-byte pair stores when this vector's output starts 16-byte aligned)
+    const bool oal = (reinterpret_cast<uintptr_t>(ob) & 15) == 0;
+    warp_syn_run<NU>(p, F, tp, wb, v, lane, vmp, [&](int i, double val) { ob[i] = val; },
+                     [&](int i, double a, double b) {
+                         if (oal) {
+                             *reinterpret_cast<double2*>(ob + i) = make_double2(a, b);
+                         } else {
+                             ob[i] = a;
+                             ob[i + 1] = b;
+                         }
+                     });
 }
 
 // Coarse tail of an analysis pyramid launch: the last CTA of vector v to
